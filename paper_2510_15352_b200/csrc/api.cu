@@ -1,0 +1,763 @@
+// api.cu — the C ABI of include/gg.h: context, scene store, workspace and
+// the per-chunk render pipeline (K1a -> K2 -> K1b -> K3-5 -> K6).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gg.h"
+#include "gg_internal.cuh"
+
+namespace gg {
+void launch_validate(int64_t n, int K, const float* means, const float* scales, const float* quats,
+                     const float* opac, const float* sh, ValidateOut* out, cudaStream_t s);
+void launch_pack(int64_t n, int K, int sh_stride, const float* means, const float* scales,
+                 const float* quats, const float* opac, const float* sh, float4* pos_op, float4* cov_a,
+                 float4* cov_b, float2* aux, float* sh_out, cudaStream_t s);
+void launch_setup_envs(int E, const int32_t* scene_ids, const float* viewmats, const float* intr,
+                       const DevScene* scenes, int nscenes, int W, int H, int sh_degree, EnvConst* out,
+                       uint32_t* err, cudaStream_t s);
+void launch_cull_count(int e0, int ec, int nblk, const EnvConst* envs, const DevScene* scenes,
+                       const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
+void launch_scan_blocks(int ec, int nblk, uint32_t* data, uint32_t* totals, cudaStream_t s);
+void launch_project(int e0, int ec, int nblk, const EnvConst* envs, const DevScene* scenes,
+                    const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
+size_t sort_bin_smem();
+cudaError_t sort_bin_init();
+void launch_sort_bin(int ec, const RenderParams& rp, const ChunkWS& ws, int tile_passes, cudaStream_t s);
+void launch_raster(int e0, int ec, const RenderParams& rp, const ChunkWS& ws, void* rgb, float* depth,
+                   float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
+                   int dbg_eloc, cudaStream_t s);
+void launch_checksum(int E, int W, int H, const uint8_t* rgb8, const float* rgbf, const float* depth,
+                     unsigned long long* out, cudaStream_t s);
+void launch_debug_records(uint32_t V, uint64_t rb, const ChunkWS& ws, int32_t* tile_counts, float* proj,
+                          cudaStream_t s);
+void launch_debug_sorted(int ntiles, const uint2* ranges, uint64_t kb, uint64_t rb, const ChunkWS& ws,
+                         int32_t* s_tile, uint32_t* s_z, int32_t* s_gid, cudaStream_t s);
+}  // namespace gg
+
+using namespace gg;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct SceneSlot {
+  DevScene d{};
+  DevBuf pos_op, cov_a, cov_b, aux, sh;
+  bool live = false;
+};
+
+constexpr int DEFAULT_CHUNK = 512;
+
+}  // namespace
+
+struct gg_context {
+  int device = 0;
+  gg_allocator alloc{};
+  bool has_alloc = false;
+  cudaStream_t own = nullptr;   // load-time work + copy-out stream
+  std::string err;
+  int64_t launches = 0;
+  std::vector<SceneSlot> scenes;
+  DevBuf scene_table;
+  int scene_table_cap = 0;
+  int chunk = DEFAULT_CHUNK;
+  // workspace
+  DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase;
+  DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1;
+  DevBuf tk0, tv0, tk1, tv1, sorted, ranges, counters, valid_out;
+  DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval;
+  DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
+  // pinned host mirrors
+  uint32_t* h_vcnt = nullptr;
+  uint32_t* h_kcnt = nullptr;
+  uint64_t* h_rbase = nullptr;
+  uint64_t* h_kbase = nullptr;
+  uint32_t* h_err = nullptr;
+  int h_cap = 0;
+  // debug snapshot (host)
+  std::vector<int32_t> d_tc, d_stile, d_sgid, d_ranges, d_neval;
+  std::vector<uint32_t> d_sz;
+  std::vector<float> d_proj;
+  int64_t d_counters[4] = {0, 0, 0, 0};
+  // timing
+  bool timing = false;
+  float stage_ms[3] = {0, 0, 0};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_copy = nullptr;
+  int last_E = 0;
+};
+
+namespace {
+
+gg_status fail(gg_context* c, gg_status s, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return s;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(ctx, GG_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+void* dev_alloc(gg_context* ctx, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->has_alloc) return ctx->alloc.alloc(bytes, (void*)s, ctx->alloc.user);
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dev_free(gg_context* ctx, DevBuf& b, cudaStream_t s) {
+  if (b.p) {
+    if (ctx->has_alloc)
+      ctx->alloc.free(b.p, (void*)s, ctx->alloc.user);
+    else
+      cudaFreeAsync(b.p, s);
+  }
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+// grow-only buffer
+bool ensure(gg_context* ctx, DevBuf& b, size_t bytes, cudaStream_t s) {
+  if (b.bytes >= bytes && b.p) return true;
+  if (b.p) cudaDeviceSynchronize();   // growth is rare; never free under in-flight work
+  dev_free(ctx, b, s);
+  const size_t nb = std::max<size_t>(bytes + bytes / 8, 256);
+  b.p = dev_alloc(ctx, nb, s);
+  if (!b.p) return false;
+  b.bytes = nb;
+  return true;
+}
+
+bool ensure_host(gg_context* ctx, int n) {
+  if (ctx->h_cap >= n) return true;
+  cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase); cudaFreeHost(ctx->h_kbase);
+  int cap = std::max(n, 1024);
+  if (cudaMallocHost(&ctx->h_vcnt, cap * 4) != cudaSuccess) return false;
+  if (cudaMallocHost(&ctx->h_kcnt, cap * 4) != cudaSuccess) return false;
+  if (cudaMallocHost(&ctx->h_rbase, cap * 8) != cudaSuccess) return false;
+  if (cudaMallocHost(&ctx->h_kbase, cap * 8) != cudaSuccess) return false;
+  ctx->h_cap = cap;
+  return true;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int max_scene_n(const gg_context* ctx) {
+  int m = 0;
+  for (const auto& s : ctx->scenes)
+    if (s.live) m = std::max(m, s.d.n);
+  return m;
+}
+
+template <typename T>
+T* P(const DevBuf& b) {
+  return reinterpret_cast<T*>(b.p);
+}
+
+}  // namespace
+
+extern "C" {
+
+void gg_default_opts(gg_render_opts* o) {
+  if (!o) return;
+  o->near_plane = 0.01f;
+  o->far_plane = 1e10f;
+  o->background[0] = o->background[1] = o->background[2] = 0.f;
+  o->sh_degree = -1;
+  o->rgb_format = 0;
+  o->flags = 0;
+  o->debug_env = -1;
+}
+
+const char* gg_status_string(gg_status s) {
+  switch (s) {
+    case GG_OK: return "GG_OK";
+    case GG_E_INVALID: return "GG_E_INVALID";
+    case GG_E_NONFINITE: return "GG_E_NONFINITE";
+    case GG_E_OOM: return "GG_E_OOM";
+    case GG_E_CUDA: return "GG_E_CUDA";
+    case GG_E_BAD_SCENE: return "GG_E_BAD_SCENE";
+    case GG_E_CAPACITY: return "GG_E_CAPACITY";
+    case GG_E_UNSUPPORTED: return "GG_E_UNSUPPORTED";
+  }
+  return "GG_E_?";
+}
+
+const char* gg_last_error(const gg_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t gg_launch_count(const gg_context* ctx) { return ctx ? ctx->launches : 0; }
+
+gg_status gg_create(int device, const gg_allocator* a, gg_context** out) {
+  gg_context* ctx = nullptr;
+  if (!out) return GG_E_INVALID;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return GG_E_CUDA;
+  }
+  ctx = new gg_context();
+  ctx->device = device;
+  if (a && a->alloc && a->free) {
+    ctx->alloc = *a;
+    ctx->has_alloc = true;
+  }
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+  CK(sort_bin_init());
+  for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+  CK(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
+  CK(cudaMallocHost(&ctx->h_err, 4));
+  if (!ensure_host(ctx, 1024)) return fail(ctx, GG_E_OOM, "pinned host alloc failed");
+  if (!ensure(ctx, ctx->errflag, 4, ctx->own)) return fail(ctx, GG_E_OOM, "alloc");
+  CK(cudaMemsetAsync(ctx->errflag.p, 0, 4, ctx->own));
+  CK(cudaStreamSynchronize(ctx->own));
+  *out = ctx;
+  return GG_OK;
+}
+
+gg_status gg_destroy(gg_context* ctx) {
+  if (!ctx) return GG_E_INVALID;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->own;
+  cudaDeviceSynchronize();
+  for (auto& sc : ctx->scenes) {
+    dev_free(ctx, sc.pos_op, s); dev_free(ctx, sc.cov_a, s); dev_free(ctx, sc.cov_b, s);
+    dev_free(ctx, sc.aux, s); dev_free(ctx, sc.sh, s);
+  }
+  DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
+                   &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect,
+                   &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->tk0, &ctx->tv0,
+                   &ctx->tk1, &ctx->tv1, &ctx->sorted, &ctx->ranges, &ctx->counters, &ctx->valid_out,
+                   &ctx->dbg_tc, &ctx->dbg_proj, &ctx->dbg_stile, &ctx->dbg_sz, &ctx->dbg_sgid,
+                   &ctx->dbg_neval, &ctx->h_in};
+  for (DevBuf* b : all) dev_free(ctx, *b, s);
+  cudaStreamSynchronize(s);
+  cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
+  cudaFreeHost(ctx->h_kbase); cudaFreeHost(ctx->h_err);
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  cudaEventDestroy(ctx->ev_copy);
+  cudaStreamDestroy(s);
+  delete ctx;
+  return GG_OK;
+}
+
+static gg_status upload_scene_table(gg_context* ctx) {
+  const int n = (int)ctx->scenes.size();
+  std::vector<DevScene> h(n);
+  for (int i = 0; i < n; ++i) {
+    h[i] = ctx->scenes[i].d;
+    h[i].valid = ctx->scenes[i].live ? 1 : 0;
+  }
+  if (!ensure(ctx, ctx->scene_table, sizeof(DevScene) * std::max(n, 1), ctx->own))
+    return fail(ctx, GG_E_OOM, "scene table alloc");
+  CK(cudaMemcpyAsync(ctx->scene_table.p, h.data(), sizeof(DevScene) * n, cudaMemcpyHostToDevice, ctx->own));
+  CK(cudaStreamSynchronize(ctx->own));
+  return GG_OK;
+}
+
+gg_status gg_load_scene(gg_context* ctx, int64_t n, int32_t d, const float* means, const float* scales,
+                        const float* quats, const float* opac, const float* sh, int32_t* out_id) {
+  if (!ctx) return GG_E_INVALID;
+  if (!out_id || !means || !scales || !quats || !opac || !sh)
+    return fail(ctx, GG_E_INVALID, "gg_load_scene: null pointer argument");
+  if (n <= 0) return fail(ctx, GG_E_INVALID, "gg_load_scene: empty scene (n=%lld)", (long long)n);
+  if (n > (int64_t)0x7fffff00) return fail(ctx, GG_E_UNSUPPORTED, "gg_load_scene: n too large");
+  if (d < 0 || d > 3) return fail(ctx, GG_E_INVALID, "gg_load_scene: sh_degree %d not in 0..3", d);
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->own;
+  const int K = (d + 1) * (d + 1);
+  const size_t sz[5] = {(size_t)n * 3, (size_t)n * 3, (size_t)n * 4, (size_t)n, (size_t)n * K * 3};
+  const float* src[5] = {means, scales, quats, opac, sh};
+  DevBuf stage[5];
+  const float* dsrc[5];
+  for (int i = 0; i < 5; ++i) {
+    if (is_device_ptr(src[i])) {
+      dsrc[i] = src[i];
+    } else {
+      if (!ensure(ctx, stage[i], sz[i] * 4, s)) {
+        for (auto& b : stage) dev_free(ctx, b, s);
+        return fail(ctx, GG_E_OOM, "gg_load_scene: staging alloc");
+      }
+      CK(cudaMemcpyAsync(stage[i].p, src[i], sz[i] * 4, cudaMemcpyHostToDevice, s));
+      dsrc[i] = P<float>(stage[i]);
+    }
+  }
+  if (!ensure(ctx, ctx->valid_out, sizeof(ValidateOut), s)) return fail(ctx, GG_E_OOM, "alloc");
+  CK(cudaMemsetAsync(ctx->valid_out.p, 0xff, sizeof(ValidateOut), s));
+  launch_validate(n, K, dsrc[0], dsrc[1], dsrc[2], dsrc[3], dsrc[4], P<ValidateOut>(ctx->valid_out), s);
+  ctx->launches++;
+  ValidateOut vo;
+  CK(cudaMemcpyAsync(&vo, ctx->valid_out.p, sizeof vo, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const unsigned long long NONE = ~0ULL;
+  gg_status st = GG_OK;
+  if (vo.nonfinite != NONE)
+    st = fail(ctx, GG_E_NONFINITE, "gg_load_scene: non-finite value in record %llu", vo.nonfinite);
+  else if (vo.bad_scale != NONE)
+    st = fail(ctx, GG_E_INVALID, "gg_load_scene: scale <= 0 in record %llu", vo.bad_scale);
+  else if (vo.bad_opacity != NONE)
+    st = fail(ctx, GG_E_INVALID, "gg_load_scene: opacity outside [0,1] in record %llu", vo.bad_opacity);
+  else if (vo.zero_quat != NONE)
+    st = fail(ctx, GG_E_INVALID, "gg_load_scene: zero-norm quaternion in record %llu", vo.zero_quat);
+  if (st != GG_OK) {
+    for (auto& b : stage) dev_free(ctx, b, s);
+    cudaStreamSynchronize(s);
+    return st;
+  }
+  SceneSlot slot;
+  const int sh_stride = d > 0 ? ((K * 3 + 3) / 4) * 4 : 0;
+  bool ok = ensure(ctx, slot.pos_op, n * 16, s) && ensure(ctx, slot.cov_a, n * 16, s) &&
+            ensure(ctx, slot.cov_b, n * 16, s) && ensure(ctx, slot.aux, n * 8, s) &&
+            (d == 0 || ensure(ctx, slot.sh, (size_t)n * sh_stride * 4, s));
+  if (!ok) {
+    for (auto& b : stage) dev_free(ctx, b, s);
+    dev_free(ctx, slot.pos_op, s); dev_free(ctx, slot.cov_a, s); dev_free(ctx, slot.cov_b, s);
+    dev_free(ctx, slot.aux, s); dev_free(ctx, slot.sh, s);
+    return fail(ctx, GG_E_OOM, "gg_load_scene: out of device memory for %lld Gaussians", (long long)n);
+  }
+  launch_pack(n, K, sh_stride, dsrc[0], dsrc[1], dsrc[2], dsrc[3], dsrc[4], P<float4>(slot.pos_op),
+              P<float4>(slot.cov_a), P<float4>(slot.cov_b), P<float2>(slot.aux),
+              d > 0 ? P<float>(slot.sh) : nullptr, s);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  for (auto& b : stage) dev_free(ctx, b, s);
+  slot.d.pos_op = P<float4>(slot.pos_op);
+  slot.d.cov_a = P<float4>(slot.cov_a);
+  slot.d.cov_b = P<float4>(slot.cov_b);
+  slot.d.aux = P<float2>(slot.aux);
+  slot.d.sh = d > 0 ? P<float>(slot.sh) : nullptr;
+  slot.d.n = (int32_t)n;
+  slot.d.degree = d;
+  slot.d.sh_stride = sh_stride;
+  slot.d.valid = 1;
+  slot.live = true;
+  // reuse a free id if any
+  int id = -1;
+  for (size_t i = 0; i < ctx->scenes.size(); ++i)
+    if (!ctx->scenes[i].live) { id = (int)i; break; }
+  if (id < 0) {
+    id = (int)ctx->scenes.size();
+    ctx->scenes.push_back(slot);
+  } else {
+    ctx->scenes[id] = slot;
+  }
+  gg_status us = upload_scene_table(ctx);
+  if (us != GG_OK) return us;
+  *out_id = id;
+  return GG_OK;
+}
+
+gg_status gg_unload_scene(gg_context* ctx, int32_t id) {
+  if (!ctx) return GG_E_INVALID;
+  if (id < 0 || id >= (int)ctx->scenes.size() || !ctx->scenes[id].live)
+    return fail(ctx, GG_E_BAD_SCENE, "gg_unload_scene: unknown scene id %d", id);
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  SceneSlot& sc = ctx->scenes[id];
+  dev_free(ctx, sc.pos_op, ctx->own); dev_free(ctx, sc.cov_a, ctx->own); dev_free(ctx, sc.cov_b, ctx->own);
+  dev_free(ctx, sc.aux, ctx->own); dev_free(ctx, sc.sh, ctx->own);
+  sc.live = false;
+  sc.d = DevScene{};
+  return upload_scene_table(ctx);
+}
+
+gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t W, int32_t H, int32_t chunk) {
+  if (!ctx) return GG_E_INVALID;
+  if (max_envs <= 0 || W <= 0 || H <= 0 || chunk < 0) return fail(ctx, GG_E_INVALID, "gg_reserve: bad sizes");
+  if (chunk > 0) ctx->chunk = chunk;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->own;
+  const int ec = std::min(max_envs, ctx->chunk);
+  const int nmax = std::max(max_scene_n(ctx), 1);
+  const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
+  const int ntiles = ((W + TILE - 1) / TILE) * ((H + TILE - 1) / TILE);
+  bool ok = ensure(ctx, ctx->envc, sizeof(EnvConst) * max_envs, s) &&
+            ensure(ctx, ctx->flags, (size_t)ec * nblk * 8 * 4, s) &&
+            ensure(ctx, ctx->blkcnt, (size_t)ec * nblk * 4, s) && ensure(ctx, ctx->vcnt, ec * 4, s) &&
+            ensure(ctx, ctx->kcnt, ec * 4, s) && ensure(ctx, ctx->rbase, ec * 8, s) &&
+            ensure(ctx, ctx->kbase, ec * 8, s) && ensure(ctx, ctx->ranges, (size_t)ec * ntiles * 8, s) &&
+            ensure(ctx, ctx->counters, (size_t)max_envs * 32, s) && ensure_host(ctx, ec);
+  CK(cudaStreamSynchronize(s));
+  return ok ? GG_OK : fail(ctx, GG_E_OOM, "gg_reserve: allocation failed");
+}
+
+gg_status gg_set_timing(gg_context* ctx, int32_t en) {
+  if (!ctx) return GG_E_INVALID;
+  ctx->timing = en != 0;
+  return GG_OK;
+}
+
+gg_status gg_get_stage_ms(gg_context* ctx, float* out3) {
+  if (!ctx || !out3) return GG_E_INVALID;
+  for (int i = 0; i < 3; ++i) out3[i] = ctx->stage_ms[i];
+  return GG_OK;
+}
+
+// Core pipeline.  `after_chunk` (optional) is invoked after each chunk's
+// rasterize is enqueued (used by gg_render_host to stream outputs out).
+typedef gg_status (*chunk_cb)(gg_context*, int e0, int ec, void* user);
+
+static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
+                             const float* intr, int32_t W, int32_t H, const gg_render_opts* opts_in,
+                             void* rgb, float* depth, float* alpha, cudaStream_t s, chunk_cb cb,
+                             void* cb_user) {
+  gg_render_opts opts;
+  if (opts_in) opts = *opts_in; else gg_default_opts(&opts);
+  if (E <= 0 || W <= 0 || H <= 0) return fail(ctx, GG_E_INVALID, "gg_render: n_envs/width/height must be > 0");
+  if (!scene_ids || !viewmats || !intr) return fail(ctx, GG_E_INVALID, "gg_render: null input pointer");
+  if (opts.rgb_format != 0 && opts.rgb_format != 1) return fail(ctx, GG_E_INVALID, "gg_render: rgb_format");
+  if (!(opts.near_plane > 0.f) || !(opts.far_plane > opts.near_plane))
+    return fail(ctx, GG_E_INVALID, "gg_render: need 0 < near < far");
+  if (opts.sh_degree > 3) return fail(ctx, GG_E_INVALID, "gg_render: sh_degree > 3");
+  const int TX = (W + TILE - 1) / TILE, TY = (H + TILE - 1) / TILE;
+  const int ntiles = TX * TY;
+  if (ntiles > MAX_TILES || W > 65535 || H > 65535)
+    return fail(ctx, GG_E_UNSUPPORTED, "gg_render: %dx%d needs %d tiles > %d", W, H, ntiles, MAX_TILES);
+  if (ctx->scenes.empty()) return fail(ctx, GG_E_BAD_SCENE, "gg_render: no scene loaded");
+  CK(cudaSetDevice(ctx->device));
+
+  RenderParams rp;
+  rp.W = W; rp.H = H; rp.TX = TX; rp.TY = TY; rp.ntiles = ntiles;
+  rp.near_p = opts.near_plane; rp.far_p = opts.far_plane;
+  rp.bg[0] = opts.background[0]; rp.bg[1] = opts.background[1]; rp.bg[2] = opts.background[2];
+  rp.rgb_format = opts.rgb_format;
+  const bool counters = (opts.flags & GG_COUNTERS) != 0;
+  const bool keep = (opts.flags & GG_KEEP_INTERMEDIATES) != 0 && opts.debug_env >= 0 && opts.debug_env < E;
+
+  const int nmax = std::max(max_scene_n(ctx), 1);
+  const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
+  const int nwords = nblk * (PROJ_BLOCK / 32);
+  const int chunk = std::min(E, ctx->chunk);
+  int tile_bits = 0;
+  while ((1 << tile_bits) < ntiles) ++tile_bits;
+  const int tile_passes = std::max(1, (tile_bits + 7) / 8);
+
+  if (!ensure(ctx, ctx->envc, sizeof(EnvConst) * E, s) ||
+      !ensure(ctx, ctx->flags, (size_t)chunk * nwords * 4, s) ||
+      !ensure(ctx, ctx->blkcnt, (size_t)chunk * nblk * 4, s) || !ensure(ctx, ctx->vcnt, chunk * 4, s) ||
+      !ensure(ctx, ctx->kcnt, chunk * 4, s) || !ensure(ctx, ctx->rbase, chunk * 8, s) ||
+      !ensure(ctx, ctx->kbase, chunk * 8, s) || !ensure(ctx, ctx->ranges, (size_t)chunk * ntiles * 8, s) ||
+      !ensure_host(ctx, chunk) || (counters && !ensure(ctx, ctx->counters, (size_t)E * 32, s)))
+    return fail(ctx, GG_E_OOM, "gg_render: workspace allocation failed");
+  if (counters) CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)E * 32, s));
+  CK(cudaMemsetAsync(ctx->errflag.p, 0, 4, s));
+
+  launch_setup_envs(E, scene_ids, viewmats, intr, P<DevScene>(ctx->scene_table), (int)ctx->scenes.size(), W,
+                    H, opts.sh_degree, P<EnvConst>(ctx->envc), P<uint32_t>(ctx->errflag), s);
+  ctx->launches++;
+  CK(cudaGetLastError());
+
+  float ms[3] = {0, 0, 0};
+  for (int e0 = 0; e0 < E; e0 += chunk) {
+    const int ec = std::min(chunk, E - e0);
+    ChunkWS ws{};
+    ws.flags = P<uint32_t>(ctx->flags);
+    ws.blkcnt = P<uint32_t>(ctx->blkcnt);
+    ws.vcnt = P<uint32_t>(ctx->vcnt);
+    ws.kcnt = P<uint32_t>(ctx->kcnt);
+    ws.rec_base = P<uint64_t>(ctx->rbase);
+    ws.k_base = P<uint64_t>(ctx->kbase);
+    ws.ranges = P<uint2>(ctx->ranges);
+    ws.nwords = nwords;
+    ws.nblk = nblk;
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], s));
+    // K1a + K2
+    launch_cull_count(e0, ec, nblk, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
+    launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
+    ctx->launches += 2;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_vcnt, ws.vcnt, ec * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    uint64_t V = 0;
+    for (int i = 0; i < ec; ++i) { ctx->h_rbase[i] = V; V += ctx->h_vcnt[i]; }
+    if (!ensure(ctx, ctx->rec0, V * 16, s) || !ensure(ctx, ctx->rec1, V * 16, s) ||
+        !ensure(ctx, ctx->rec2, V * 16, s) || !ensure(ctx, ctx->rect, V * 8, s) ||
+        !ensure(ctx, ctx->zkey, V * 4, s) || !ensure(ctx, ctx->gid, V * 4, s) ||
+        !ensure(ctx, ctx->dk0, V * 4, s) || !ensure(ctx, ctx->dv0, V * 4, s) ||
+        !ensure(ctx, ctx->dk1, V * 4, s) || !ensure(ctx, ctx->dv1, V * 4, s))
+      return fail(ctx, GG_E_OOM, "gg_render: record workspace (%llu records) allocation failed",
+                  (unsigned long long)V);
+    CK(cudaMemcpyAsync(P<uint64_t>(ctx->rbase), ctx->h_rbase, ec * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(ws.kcnt, 0, ec * 4, s));
+    ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
+    ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey); ws.gid = P<uint32_t>(ctx->gid);
+    ws.dk0 = P<uint32_t>(ctx->dk0); ws.dv0 = P<uint32_t>(ctx->dv0);
+    ws.dk1 = P<uint32_t>(ctx->dk1); ws.dv1 = P<uint32_t>(ctx->dv1);
+    // K1b
+    launch_project(e0, ec, nblk, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_kcnt, ws.kcnt, ec * 4, cudaMemcpyDeviceToHost, s));
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaStreamSynchronize(s));
+    uint64_t K = 0;
+    for (int i = 0; i < ec; ++i) { ctx->h_kbase[i] = K; K += ctx->h_kcnt[i]; }
+    if (K > 0xffffffffull * 4)
+      return fail(ctx, GG_E_CAPACITY, "gg_render: %llu keys in one chunk", (unsigned long long)K);
+    for (int i = 0; i < ec; ++i)
+      if (ctx->h_kcnt[i] == 0xffffffffu) return fail(ctx, GG_E_CAPACITY, "gg_render: env key overflow");
+    if (!ensure(ctx, ctx->tk0, K * 4, s) || !ensure(ctx, ctx->tv0, K * 4, s) ||
+        !ensure(ctx, ctx->tk1, K * 4, s) || !ensure(ctx, ctx->tv1, K * 4, s) ||
+        !ensure(ctx, ctx->sorted, K * 4, s))
+      return fail(ctx, GG_E_OOM, "gg_render: key workspace (%llu keys) allocation failed",
+                  (unsigned long long)K);
+    CK(cudaMemcpyAsync(P<uint64_t>(ctx->kbase), ctx->h_kbase, ec * 8, cudaMemcpyHostToDevice, s));
+    ws.tk0 = P<uint32_t>(ctx->tk0); ws.tv0 = P<uint32_t>(ctx->tv0);
+    ws.tk1 = P<uint32_t>(ctx->tk1); ws.tv1 = P<uint32_t>(ctx->tv1);
+    ws.sorted = P<uint32_t>(ctx->sorted);
+    // K3-K5
+    launch_sort_bin(ec, rp, ws, tile_passes, s);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], s));
+    // K6
+    const int dbg_eloc = (keep && opts.debug_env >= e0 && opts.debug_env < e0 + ec) ? opts.debug_env - e0 : -1;
+    int32_t* dbg_neval = nullptr;
+    if (dbg_eloc >= 0 && counters) {
+      if (!ensure(ctx, ctx->dbg_neval, (size_t)W * H * 4, s)) return fail(ctx, GG_E_OOM, "debug alloc");
+      dbg_neval = P<int32_t>(ctx->dbg_neval);
+    }
+    launch_raster(e0, ec, rp, ws, rgb, depth, alpha, counters, counters ? P<unsigned long long>(ctx->counters) : nullptr,
+                  dbg_neval, dbg_eloc, s);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    if (ctx->timing) {
+      CK(cudaEventRecord(ctx->ev[3], s));
+      CK(cudaEventSynchronize(ctx->ev[3]));
+      float a, b, c;
+      cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+      cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+      cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+      ms[0] += a; ms[1] += b; ms[2] += c;
+    }
+    if (counters) {
+      // V and K per env into the counters table (host -> device, tiny)
+      std::vector<unsigned long long> vk(ec * 2);
+      for (int i = 0; i < ec; ++i) { vk[i * 2] = ctx->h_vcnt[i]; vk[i * 2 + 1] = ctx->h_kcnt[i]; }
+      CK(cudaMemcpy2DAsync(P<unsigned long long>(ctx->counters) + (size_t)e0 * 4 + 2, 32, vk.data(), 16, 16, ec,
+                           cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    if (dbg_eloc >= 0) {
+      // K8: snapshot the debug env's integer artefacts to host
+      const int32_t sid_dummy = 0;
+      (void)sid_dummy;
+      const uint32_t Vd = ctx->h_vcnt[dbg_eloc], Kd = ctx->h_kcnt[dbg_eloc];
+      const uint64_t rb = ctx->h_rbase[dbg_eloc], kb = ctx->h_kbase[dbg_eloc];
+      const int n_all = nmax;
+      if (!ensure(ctx, ctx->dbg_tc, (size_t)n_all * 4, s) || !ensure(ctx, ctx->dbg_proj, (size_t)n_all * 64, s) ||
+          !ensure(ctx, ctx->dbg_stile, (size_t)Kd * 4 + 4, s) || !ensure(ctx, ctx->dbg_sz, (size_t)Kd * 4 + 4, s) ||
+          !ensure(ctx, ctx->dbg_sgid, (size_t)Kd * 4 + 4, s))
+        return fail(ctx, GG_E_OOM, "debug alloc");
+      CK(cudaMemsetAsync(ctx->dbg_tc.p, 0, (size_t)n_all * 4, s));
+      CK(cudaMemsetAsync(ctx->dbg_proj.p, 0, (size_t)n_all * 64, s));
+      launch_debug_records(Vd, rb, ws, P<int32_t>(ctx->dbg_tc), P<float>(ctx->dbg_proj), s);
+      launch_debug_sorted(ntiles, ws.ranges + (size_t)dbg_eloc * ntiles, kb, rb, ws, P<int32_t>(ctx->dbg_stile),
+                          P<uint32_t>(ctx->dbg_sz), P<int32_t>(ctx->dbg_sgid), s);
+      ctx->launches += 2;
+      CK(cudaGetLastError());
+      // the env's scene size
+      EnvConst hc;
+      CK(cudaMemcpyAsync(&hc, P<EnvConst>(ctx->envc) + opts.debug_env, sizeof hc, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      const int nn = std::max(hc.n, 0);
+      ctx->d_tc.resize(nn); ctx->d_proj.resize((size_t)nn * 16);
+      ctx->d_stile.resize(Kd); ctx->d_sz.resize(Kd); ctx->d_sgid.resize(Kd);
+      ctx->d_ranges.resize((size_t)ntiles * 2);
+      CK(cudaMemcpy(ctx->d_tc.data(), ctx->dbg_tc.p, (size_t)nn * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ctx->d_proj.data(), ctx->dbg_proj.p, (size_t)nn * 64, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ctx->d_stile.data(), ctx->dbg_stile.p, (size_t)Kd * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ctx->d_sz.data(), ctx->dbg_sz.p, (size_t)Kd * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ctx->d_sgid.data(), ctx->dbg_sgid.p, (size_t)Kd * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(ctx->d_ranges.data(), ws.ranges + (size_t)dbg_eloc * ntiles, (size_t)ntiles * 8,
+                    cudaMemcpyDeviceToHost));
+      ctx->d_counters[2] = Vd;
+      ctx->d_counters[3] = Kd;
+      if (counters) {
+        unsigned long long c2[2];
+        CK(cudaMemcpy(c2, P<unsigned long long>(ctx->counters) + (size_t)opts.debug_env * 4, 16,
+                      cudaMemcpyDeviceToHost));
+        ctx->d_counters[0] = (int64_t)c2[0];
+        ctx->d_counters[1] = (int64_t)c2[1];
+        ctx->d_neval.resize((size_t)W * H);
+        CK(cudaMemcpy(ctx->d_neval.data(), ctx->dbg_neval.p, (size_t)W * H * 4, cudaMemcpyDeviceToHost));
+      } else {
+        ctx->d_counters[0] = ctx->d_counters[1] = -1;
+        ctx->d_neval.clear();
+      }
+    }
+    if (cb) {
+      gg_status cs = cb(ctx, e0, ec, cb_user);
+      if (cs != GG_OK) return cs;
+    }
+  }
+  if (ctx->timing) for (int i = 0; i < 3; ++i) ctx->stage_ms[i] = ms[i];
+  ctx->last_E = E;
+  // sticky device errors (bad scene ids): read at the end, after the last
+  // chunk's kernels are enqueued
+  CK(cudaMemcpyAsync(ctx->h_err, ctx->errflag.p, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (*ctx->h_err & ERR_BAD_SCENE) return fail(ctx, GG_E_BAD_SCENE, "gg_render: an env is bound to an unknown scene id");
+  return GG_OK;
+}
+
+gg_status gg_render(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
+                    const float* intr, int32_t W, int32_t H, const gg_render_opts* opts, void* rgb,
+                    float* depth, float* alpha, void* stream) {
+  if (!ctx) return GG_E_INVALID;
+  return render_impl(ctx, E, scene_ids, viewmats, intr, W, H, opts, rgb, depth, alpha,
+                     (cudaStream_t)stream, nullptr, nullptr);
+}
+
+struct HostCopy {
+  void* rgb_h; float* depth_h; float* alpha_h;
+  uint8_t* rgb_d; float* depth_d; float* alpha_d;
+  size_t rgb_px_bytes;
+  int W, H;
+  cudaStream_t s;
+};
+
+static gg_status copy_out_chunk(gg_context* ctx, int e0, int ec, void* user) {
+  HostCopy* h = (HostCopy*)user;
+  const size_t P_ = (size_t)h->W * h->H;
+  // outputs of this chunk are final once its rasterize completes: the copy
+  // stream waits for that point and overlaps the copy with the next chunk.
+  CK(cudaEventRecord(ctx->ev_copy, h->s));
+  CK(cudaStreamWaitEvent(ctx->own, ctx->ev_copy, 0));
+  if (h->rgb_h)
+    CK(cudaMemcpyAsync((uint8_t*)h->rgb_h + (size_t)e0 * P_ * h->rgb_px_bytes, h->rgb_d + (size_t)e0 * P_ * h->rgb_px_bytes,
+                       (size_t)ec * P_ * h->rgb_px_bytes, cudaMemcpyDeviceToHost, ctx->own));
+  if (h->depth_h)
+    CK(cudaMemcpyAsync(h->depth_h + (size_t)e0 * P_, h->depth_d + (size_t)e0 * P_, (size_t)ec * P_ * 4,
+                       cudaMemcpyDeviceToHost, ctx->own));
+  if (h->alpha_h)
+    CK(cudaMemcpyAsync(h->alpha_h + (size_t)e0 * P_, h->alpha_d + (size_t)e0 * P_, (size_t)ec * P_ * 4,
+                       cudaMemcpyDeviceToHost, ctx->own));
+  return GG_OK;
+}
+
+gg_status gg_render_host(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
+                         const float* intr, int32_t W, int32_t H, const gg_render_opts* opts, void* rgb,
+                         float* depth, float* alpha, void* stream) {
+  if (!ctx) return GG_E_INVALID;
+  if (E <= 0 || W <= 0 || H <= 0) return fail(ctx, GG_E_INVALID, "gg_render_host: bad sizes");
+  if (!scene_ids || !viewmats || !intr) return fail(ctx, GG_E_INVALID, "gg_render_host: null input pointer");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int fmt = opts ? opts->rgb_format : 0;
+  const size_t px = (size_t)W * H;
+  const size_t rgb_px = fmt == 1 ? 12 : 3;
+  const size_t in_bytes = (size_t)E * (4 + 64 + 16);
+  const size_t out_rgb = rgb ? (size_t)E * px * rgb_px : 0;
+  const size_t out_d = depth ? (size_t)E * px * 4 : 0;
+  const size_t out_a = alpha ? (size_t)E * px * 4 : 0;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t total = al(in_bytes) + al(out_rgb) + al(out_d) + al(out_a);
+  if (!ensure(ctx, ctx->h_in, total, s)) return fail(ctx, GG_E_OOM, "gg_render_host: device staging");
+  uint8_t* base = P<uint8_t>(ctx->h_in);
+  int32_t* d_ids = (int32_t*)base;
+  float* d_vm = (float*)(base + (size_t)E * 4);
+  float* d_in = (float*)(base + (size_t)E * 68);
+  uint8_t* d_rgb = base + al(in_bytes);
+  float* d_depth = (float*)(base + al(in_bytes) + al(out_rgb));
+  float* d_alpha = (float*)(base + al(in_bytes) + al(out_rgb) + al(out_d));
+  CK(cudaMemcpyAsync(d_ids, scene_ids, (size_t)E * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_vm, viewmats, (size_t)E * 64, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_in, intr, (size_t)E * 16, cudaMemcpyHostToDevice, s));
+  HostCopy hc{rgb, depth, alpha, d_rgb, d_depth, d_alpha, rgb_px, W, H, s};
+  gg_status st = render_impl(ctx, E, d_ids, d_vm, d_in, W, H, opts, rgb ? (void*)d_rgb : nullptr,
+                             depth ? d_depth : nullptr, alpha ? d_alpha : nullptr, s, copy_out_chunk, &hc);
+  if (st != GG_OK) return st;
+  CK(cudaStreamSynchronize(ctx->own));
+  CK(cudaStreamSynchronize(s));
+  return GG_OK;
+}
+
+gg_status gg_checksum(gg_context* ctx, int32_t E, int32_t W, int32_t H, const void* rgb, int32_t fmt,
+                      const float* depth, uint64_t* out, void* stream) {
+  if (!ctx) return GG_E_INVALID;
+  if (E <= 0 || W <= 0 || H <= 0 || !out) return fail(ctx, GG_E_INVALID, "gg_checksum: bad args");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(out, 0, (size_t)E * 8, s));
+  launch_checksum(E, W, H, fmt == 0 ? (const uint8_t*)rgb : nullptr, fmt == 1 ? (const float*)rgb : nullptr, depth,
+                  (unsigned long long*)out, s);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+gg_status gg_check_errors(gg_context* ctx, void* stream) {
+  if (!ctx) return GG_E_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(ctx->h_err, ctx->errflag.p, 4, cudaMemcpyDeviceToHost));
+  if (*ctx->h_err & ERR_BAD_SCENE) return fail(ctx, GG_E_BAD_SCENE, "device error: unknown scene id");
+  if (*ctx->h_err & ERR_CAPACITY) return fail(ctx, GG_E_CAPACITY, "device error: capacity");
+  return GG_OK;
+}
+
+gg_status gg_get_counters(gg_context* ctx, int32_t E, int64_t* dst) {
+  if (!ctx || !dst || E <= 0) return GG_E_INVALID;
+  if (E > ctx->last_E || !ctx->counters.p || ctx->counters.bytes < (size_t)E * 32)
+    return fail(ctx, GG_E_INVALID, "gg_get_counters: no counters for %d envs", E);
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(dst, ctx->counters.p, (size_t)E * 32, cudaMemcpyDeviceToHost));
+  return GG_OK;
+}
+
+gg_status gg_debug_dump(gg_context* ctx, int32_t kind, void* dst, int64_t cap, int64_t* out_len) {
+  if (!ctx || !out_len) return GG_E_INVALID;
+  const void* src = nullptr;
+  size_t n = 0, es = 4;
+  switch (kind) {
+    case GG_DUMP_TILE_COUNTS: src = ctx->d_tc.data(); n = ctx->d_tc.size(); break;
+    case GG_DUMP_SORTED_TILE: src = ctx->d_stile.data(); n = ctx->d_stile.size(); break;
+    case GG_DUMP_SORTED_ZBITS: src = ctx->d_sz.data(); n = ctx->d_sz.size(); break;
+    case GG_DUMP_SORTED_GIDS: src = ctx->d_sgid.data(); n = ctx->d_sgid.size(); break;
+    case GG_DUMP_RANGES: src = ctx->d_ranges.data(); n = ctx->d_ranges.size(); break;
+    case GG_DUMP_COUNTERS: src = ctx->d_counters; n = 4; es = 8; break;
+    case GG_DUMP_N_EVAL: src = ctx->d_neval.data(); n = ctx->d_neval.size(); break;
+    case GG_DUMP_PROJ: src = ctx->d_proj.data(); n = ctx->d_proj.size(); break;
+    default: return fail(ctx, GG_E_INVALID, "gg_debug_dump: unknown kind %d", kind);
+  }
+  *out_len = (int64_t)n;
+  if (dst && cap > 0) memcpy(dst, src, std::min<size_t>(n, (size_t)cap) * es);
+  return GG_OK;
+}
+
+}  // extern "C"

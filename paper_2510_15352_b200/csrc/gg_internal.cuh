@@ -1,0 +1,88 @@
+// gg_internal.cuh — device-side data layout shared by the kernels of libgg.
+// (Product path only; shares nothing with the CPU checker.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gg {
+
+constexpr int TILE = 16;               // SPEC.md:183 "Tile size 16x16"
+constexpr int TILE_PX = TILE * TILE;
+constexpr int PROJ_BLOCK = 256;        // Gaussians per projection block (flag words = 8)
+constexpr int MAX_TILES = 8192;        // tile table limit (e.g. 1024x2048 px)
+
+// Scene store (SoA, 16-B aligned; DESIGN.md §4 "HBM layout").  O1 results
+// (Sigma3, DC colour) are precomputed at load (K0 scene_pack).
+struct DevScene {
+  const float4* pos_op;  // (x, y, z, opacity)
+  const float4* cov_a;   // (Sxx, Sxy, Sxz, Syy)
+  const float4* cov_b;   // (Syz, Szz, dc_r, dc_g)
+  const float2* aux;     // (dc_b, max_j s_j^2)
+  const float* sh;       // [n][sh_stride] coefficient-major (k, ch), zero padded; null if d = 0
+  int32_t n;
+  int32_t degree;
+  int32_t sh_stride;     // floats per Gaussian (multiple of 4)
+  int32_t valid;
+};
+
+// Per-env camera constants (setup_envs).  f32 values follow the canonical
+// order of DESIGN.md §2.1 (they feed integer decisions).
+struct EnvConst {
+  float R[9];          // world->camera rotation, row-major
+  float t[3];
+  float fx, fy, cx, cy;
+  float lim_xp, lim_xn, lim_yp, lim_yn;   // Jacobian clamp limits (reading R4)
+  float C[3];          // camera centre -R^T t (SH view direction)
+  int32_t scene;       // index into the scene table, -1 if invalid
+  int32_t n;           // Gaussians in that scene (0 if invalid)
+  int32_t degree;      // SH degree used at render
+  int32_t pad;
+};
+
+struct RenderParams {
+  int W, H, TX, TY, ntiles;
+  float near_p, far_p;
+  float bg[3];
+  int rgb_format;
+};
+
+// Workspace pointers for one env chunk (indices are chunk-local envs).
+struct ChunkWS {
+  // pass 1 / scan
+  uint32_t* flags;      // [Ec][nwords]
+  uint32_t* blkcnt;     // [Ec][nblk] -> exclusive offsets in place
+  uint32_t* vcnt;       // [Ec]
+  uint32_t* kcnt;       // [Ec]
+  // records (global index = rec_base[e] + local)
+  const uint64_t* rec_base;  // [Ec]
+  const uint64_t* k_base;    // [Ec]
+  float4* rec0;         // (u, v, opacity, z)
+  float4* rec1;         // (conic A, B, C, ext_x)
+  float4* rec2;         // (r, g, b, ext_y)
+  uint2* rect;          // (x0 | x1<<16, y0 | y1<<16)
+  uint32_t* zkey;       // f32 bits of z
+  uint32_t* gid;        // Gaussian index
+  // depth-sort scratch [V]
+  uint32_t* dk0; uint32_t* dv0; uint32_t* dk1; uint32_t* dv1;
+  // tile-sort scratch [K]
+  uint32_t* tk0; uint32_t* tv0; uint32_t* tk1; uint32_t* tv1;
+  uint32_t* sorted;     // [K] final record-local indices, tile-major
+  uint2* ranges;        // [Ec][ntiles] [start,end) relative to k_base[e]
+  int nwords, nblk;
+};
+
+// gg_load_scene validation: first offending record per class (atomicMin)
+struct ValidateOut {
+  unsigned long long nonfinite, bad_scale, bad_opacity, zero_quat;
+};
+
+// sticky error bits
+enum { ERR_BAD_SCENE = 1, ERR_CAPACITY = 2 };
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace gg
