@@ -18,19 +18,19 @@ void launch_validate(int64_t n, int K, const float* means, const float* scales, 
 void launch_pack(int64_t n, int K, int sh_stride, const float* means, const float* scales,
                  const float* quats, const float* opac, const float* sh, float4* pos_op, float4* cov_a,
                  float4* cov_b, float2* aux, float* sh_out, cudaStream_t s);
-void launch_setup_envs(int E, const int32_t* scene_ids, const float* viewmats, const float* intr,
-                       const DevScene* scenes, int nscenes, int W, int H, int sh_degree, EnvConst* out,
-                       uint32_t* err, cudaStream_t s);
-void launch_cull_count(int e0, int ec, int nblk, const EnvConst* envs, const DevScene* scenes,
-                       const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
+void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, const float* viewmats,
+                       const float* intr, const DevScene* scenes, int nscenes, int W, int H, int sh_degree,
+                       EnvConst* out, uint32_t* err, cudaStream_t s);
+void launch_cull_count(int e0, int ngroups, int nblk, const EnvGroup* groups, const EnvConst* envs,
+                       const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
 void launch_scan_blocks(int ec, int nblk, uint32_t* data, uint32_t* totals, cudaStream_t s);
-void launch_project(int e0, int ec, int nblk, const EnvConst* envs, const DevScene* scenes,
-                    const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
-size_t sort_bin_smem();
+void launch_project(int e0, int ngroups, int nblk, int max_degree, const EnvGroup* groups, const EnvConst* envs,
+                    const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
+cudaError_t project_init();
 cudaError_t sort_bin_init();
-void launch_sort_bin(int ec, const RenderParams& rp, const ChunkWS& ws, int tile_passes, cudaStream_t s);
-void launch_raster(int e0, int ec, const RenderParams& rp, const ChunkWS& ws, void* rgb, float* depth,
-                   float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
+void launch_sort_bin(int ec, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
+void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
+                   float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s);
 void launch_checksum(int E, int W, int H, const uint8_t* rgb8, const float* rgbf, const float* depth,
                      unsigned long long* out, cudaStream_t s);
@@ -73,7 +73,7 @@ struct gg_context {
   // workspace
   DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase;
   DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1;
-  DevBuf tk0, tv0, tk1, tv1, sorted, ranges, counters, valid_out;
+  DevBuf sorted, ranges, counters, valid_out, perm, groups;
   DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval;
   DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
   // pinned host mirrors
@@ -82,6 +82,9 @@ struct gg_context {
   uint64_t* h_rbase = nullptr;
   uint64_t* h_kbase = nullptr;
   uint32_t* h_err = nullptr;
+  int32_t* h_ids = nullptr;
+  int32_t* h_perm = nullptr;
+  EnvGroup* h_groups = nullptr;
   int h_cap = 0;
   // debug snapshot (host)
   std::vector<int32_t> d_tc, d_stile, d_sgid, d_ranges, d_neval;
@@ -154,7 +157,11 @@ bool ensure(gg_context* ctx, DevBuf& b, size_t bytes, cudaStream_t s) {
 bool ensure_host(gg_context* ctx, int n) {
   if (ctx->h_cap >= n) return true;
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase); cudaFreeHost(ctx->h_kbase);
+  cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups);
   int cap = std::max(n, 1024);
+  if (cudaMallocHost(&ctx->h_ids, cap * 4) != cudaSuccess) return false;
+  if (cudaMallocHost(&ctx->h_perm, cap * 4) != cudaSuccess) return false;
+  if (cudaMallocHost(&ctx->h_groups, cap * sizeof(EnvGroup)) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_vcnt, cap * 4) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_kcnt, cap * 4) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_rbase, cap * 8) != cudaSuccess) return false;
@@ -235,6 +242,7 @@ gg_status gg_create(int device, const gg_allocator* a, gg_context** out) {
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
   CK(sort_bin_init());
+  CK(project_init());
   for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
   CK(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
   CK(cudaMallocHost(&ctx->h_err, 4));
@@ -257,14 +265,15 @@ gg_status gg_destroy(gg_context* ctx) {
   }
   DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
                    &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect,
-                   &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->tk0, &ctx->tv0,
-                   &ctx->tk1, &ctx->tv1, &ctx->sorted, &ctx->ranges, &ctx->counters, &ctx->valid_out,
+                   &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->perm, &ctx->groups,
+                   &ctx->sorted, &ctx->ranges, &ctx->counters, &ctx->valid_out,
                    &ctx->dbg_tc, &ctx->dbg_proj, &ctx->dbg_stile, &ctx->dbg_sz, &ctx->dbg_sgid,
                    &ctx->dbg_neval, &ctx->h_in};
   for (DevBuf* b : all) dev_free(ctx, *b, s);
   cudaStreamSynchronize(s);
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
   cudaFreeHost(ctx->h_kbase); cudaFreeHost(ctx->h_err);
+  cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev_copy);
   cudaStreamDestroy(s);
@@ -459,28 +468,63 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   const int nwords = nblk * (PROJ_BLOCK / 32);
   const int chunk = std::min(E, ctx->chunk);
-  int tile_bits = 0;
-  while ((1 << tile_bits) < ntiles) ++tile_bits;
-  const int tile_passes = std::max(1, (tile_bits + 7) / 8);
 
-  if (!ensure(ctx, ctx->envc, sizeof(EnvConst) * E, s) ||
+  if (!ensure(ctx, ctx->envc, sizeof(EnvConst) * E, s) || !ensure(ctx, ctx->perm, (size_t)E * 4, s) ||
+      !ensure(ctx, ctx->groups, sizeof(EnvGroup) * (size_t)chunk, s) ||
       !ensure(ctx, ctx->flags, (size_t)chunk * nwords * 4, s) ||
       !ensure(ctx, ctx->blkcnt, (size_t)chunk * nblk * 4, s) || !ensure(ctx, ctx->vcnt, chunk * 4, s) ||
       !ensure(ctx, ctx->kcnt, chunk * 4, s) || !ensure(ctx, ctx->rbase, chunk * 8, s) ||
       !ensure(ctx, ctx->kbase, chunk * 8, s) || !ensure(ctx, ctx->ranges, (size_t)chunk * ntiles * 8, s) ||
-      !ensure_host(ctx, chunk) || (counters && !ensure(ctx, ctx->counters, (size_t)E * 32, s)))
+      !ensure_host(ctx, std::max(E, chunk)) || (counters && !ensure(ctx, ctx->counters, (size_t)E * 32, s)))
     return fail(ctx, GG_E_OOM, "gg_render: workspace allocation failed");
   if (counters) CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)E * 32, s));
   CK(cudaMemsetAsync(ctx->errflag.p, 0, 4, s));
 
-  launch_setup_envs(E, scene_ids, viewmats, intr, P<DevScene>(ctx->scene_table), (int)ctx->scenes.size(), W,
-                    H, opts.sh_degree, P<EnvConst>(ctx->envc), P<uint32_t>(ctx->errflag), s);
+  // Scene-sorted env order (stable): envs bound to one scene become
+  // contiguous, so the projection kernels can share each Gaussian load
+  // across a group of envs.  Outputs are still written at the caller's
+  // env index (EnvConst.out_index).
+  CK(cudaMemcpyAsync(ctx->h_ids, scene_ids, (size_t)E * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int nsc = (int)ctx->scenes.size();
+  auto key = [&](int e) {
+    const int id = ctx->h_ids[e];
+    return (id < 0 || id >= nsc || !ctx->scenes[id].live) ? -1 : id;
+  };
+  std::vector<int32_t> order(E);
+  for (int e = 0; e < E; ++e) order[e] = e;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
+  int dbg_pos = -1;
+  for (int p = 0; p < E; ++p) {
+    ctx->h_perm[p] = order[p];
+    if (keep && order[p] == opts.debug_env) dbg_pos = p;
+  }
+  CK(cudaMemcpyAsync(ctx->perm.p, ctx->h_perm, (size_t)E * 4, cudaMemcpyHostToDevice, s));
+  launch_setup_envs(E, P<int32_t>(ctx->perm), scene_ids, viewmats, intr, P<DevScene>(ctx->scene_table), nsc, W, H,
+                    opts.sh_degree, P<EnvConst>(ctx->envc), P<uint32_t>(ctx->errflag), s);
   ctx->launches++;
   CK(cudaGetLastError());
+  if (keep && !ensure(ctx, ctx->gid, 16, s)) return fail(ctx, GG_E_OOM, "alloc");
 
   float ms[3] = {0, 0, 0};
   for (int e0 = 0; e0 < E; e0 += chunk) {
     const int ec = std::min(chunk, E - e0);
+    // env groups: runs of one scene, <= ENV_GROUP envs
+    int ngroups = 0, max_deg = 0;
+    for (int i = 0; i < ec;) {
+      const int k0 = key(order[e0 + i]);
+      int j = i + 1;
+      while (j < ec && j - i < ENV_GROUP && key(order[e0 + j]) == k0) ++j;
+      ctx->h_groups[ngroups].elo = i;
+      ctx->h_groups[ngroups].cnt = j - i;
+      ++ngroups;
+      if (k0 >= 0) {
+        const int d = ctx->scenes[k0].d.degree;
+        max_deg = std::max(max_deg, opts.sh_degree < 0 ? d : std::min(d, opts.sh_degree));
+      }
+      i = j;
+    }
+    CK(cudaMemcpyAsync(ctx->groups.p, ctx->h_groups, sizeof(EnvGroup) * ngroups, cudaMemcpyHostToDevice, s));
     ChunkWS ws{};
     ws.flags = P<uint32_t>(ctx->flags);
     ws.blkcnt = P<uint32_t>(ctx->blkcnt);
@@ -491,9 +535,10 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ws.ranges = P<uint2>(ctx->ranges);
     ws.nwords = nwords;
     ws.nblk = nblk;
+    const EnvGroup* groups = P<EnvGroup>(ctx->groups);
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], s));
     // K1a + K2
-    launch_cull_count(e0, ec, nblk, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
+    launch_cull_count(e0, ngroups, nblk, groups, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
     ctx->launches += 2;
     CK(cudaGetLastError());
@@ -503,7 +548,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     for (int i = 0; i < ec; ++i) { ctx->h_rbase[i] = V; V += ctx->h_vcnt[i]; }
     if (!ensure(ctx, ctx->rec0, V * 16, s) || !ensure(ctx, ctx->rec1, V * 16, s) ||
         !ensure(ctx, ctx->rec2, V * 16, s) || !ensure(ctx, ctx->rect, V * 8, s) ||
-        !ensure(ctx, ctx->zkey, V * 4, s) || !ensure(ctx, ctx->gid, V * 4, s) ||
+        !ensure(ctx, ctx->zkey, V * 4, s) || (keep && !ensure(ctx, ctx->gid, V * 4, s)) ||
         !ensure(ctx, ctx->dk0, V * 4, s) || !ensure(ctx, ctx->dv0, V * 4, s) ||
         !ensure(ctx, ctx->dk1, V * 4, s) || !ensure(ctx, ctx->dv1, V * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: record workspace (%llu records) allocation failed",
@@ -511,11 +556,13 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     CK(cudaMemcpyAsync(P<uint64_t>(ctx->rbase), ctx->h_rbase, ec * 8, cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(ws.kcnt, 0, ec * 4, s));
     ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
-    ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey); ws.gid = P<uint32_t>(ctx->gid);
+    ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
+    ws.gid = keep ? P<uint32_t>(ctx->gid) : nullptr;
     ws.dk0 = P<uint32_t>(ctx->dk0); ws.dv0 = P<uint32_t>(ctx->dv0);
     ws.dk1 = P<uint32_t>(ctx->dk1); ws.dv1 = P<uint32_t>(ctx->dv1);
     // K1b
-    launch_project(e0, ec, nblk, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
+    launch_project(e0, ngroups, nblk, max_deg, groups, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp,
+                   ws, s);
     ctx->launches++;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->h_kcnt, ws.kcnt, ec * 4, cudaMemcpyDeviceToHost, s));
@@ -523,33 +570,26 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     CK(cudaStreamSynchronize(s));
     uint64_t K = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_kbase[i] = K; K += ctx->h_kcnt[i]; }
-    if (K > 0xffffffffull * 4)
-      return fail(ctx, GG_E_CAPACITY, "gg_render: %llu keys in one chunk", (unsigned long long)K);
     for (int i = 0; i < ec; ++i)
-      if (ctx->h_kcnt[i] == 0xffffffffu) return fail(ctx, GG_E_CAPACITY, "gg_render: env key overflow");
-    if (!ensure(ctx, ctx->tk0, K * 4, s) || !ensure(ctx, ctx->tv0, K * 4, s) ||
-        !ensure(ctx, ctx->tk1, K * 4, s) || !ensure(ctx, ctx->tv1, K * 4, s) ||
-        !ensure(ctx, ctx->sorted, K * 4, s))
-      return fail(ctx, GG_E_OOM, "gg_render: key workspace (%llu keys) allocation failed",
-                  (unsigned long long)K);
+      if (ctx->h_kcnt[i] >= 0xfffffff0u) return fail(ctx, GG_E_CAPACITY, "gg_render: env key overflow");
+    if (!ensure(ctx, ctx->sorted, K * 4, s))
+      return fail(ctx, GG_E_OOM, "gg_render: key workspace (%llu keys) allocation failed", (unsigned long long)K);
     CK(cudaMemcpyAsync(P<uint64_t>(ctx->kbase), ctx->h_kbase, ec * 8, cudaMemcpyHostToDevice, s));
-    ws.tk0 = P<uint32_t>(ctx->tk0); ws.tv0 = P<uint32_t>(ctx->tv0);
-    ws.tk1 = P<uint32_t>(ctx->tk1); ws.tv1 = P<uint32_t>(ctx->tv1);
     ws.sorted = P<uint32_t>(ctx->sorted);
     // K3-K5
-    launch_sort_bin(ec, rp, ws, tile_passes, s);
+    launch_sort_bin(ec, rp, ws, s);
     ctx->launches++;
     CK(cudaGetLastError());
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], s));
     // K6
-    const int dbg_eloc = (keep && opts.debug_env >= e0 && opts.debug_env < e0 + ec) ? opts.debug_env - e0 : -1;
+    const int dbg_eloc = (dbg_pos >= e0 && dbg_pos < e0 + ec) ? dbg_pos - e0 : -1;
     int32_t* dbg_neval = nullptr;
     if (dbg_eloc >= 0 && counters) {
       if (!ensure(ctx, ctx->dbg_neval, (size_t)W * H * 4, s)) return fail(ctx, GG_E_OOM, "debug alloc");
       dbg_neval = P<int32_t>(ctx->dbg_neval);
     }
-    launch_raster(e0, ec, rp, ws, rgb, depth, alpha, counters, counters ? P<unsigned long long>(ctx->counters) : nullptr,
-                  dbg_neval, dbg_eloc, s);
+    launch_raster(e0, ec, P<EnvConst>(ctx->envc), rp, ws, rgb, depth, alpha, counters,
+                  counters ? P<unsigned long long>(ctx->counters) : nullptr, dbg_neval, dbg_eloc, s);
     ctx->launches++;
     CK(cudaGetLastError());
     if (ctx->timing) {
@@ -561,18 +601,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
       ms[0] += a; ms[1] += b; ms[2] += c;
     }
-    if (counters) {
-      // V and K per env into the counters table (host -> device, tiny)
-      std::vector<unsigned long long> vk(ec * 2);
-      for (int i = 0; i < ec; ++i) { vk[i * 2] = ctx->h_vcnt[i]; vk[i * 2 + 1] = ctx->h_kcnt[i]; }
-      CK(cudaMemcpy2DAsync(P<unsigned long long>(ctx->counters) + (size_t)e0 * 4 + 2, 32, vk.data(), 16, 16, ec,
-                           cudaMemcpyHostToDevice, s));
-      CK(cudaStreamSynchronize(s));
-    }
     if (dbg_eloc >= 0) {
       // K8: snapshot the debug env's integer artefacts to host
-      const int32_t sid_dummy = 0;
-      (void)sid_dummy;
       const uint32_t Vd = ctx->h_vcnt[dbg_eloc], Kd = ctx->h_kcnt[dbg_eloc];
       const uint64_t rb = ctx->h_rbase[dbg_eloc], kb = ctx->h_kbase[dbg_eloc];
       const int n_all = nmax;
@@ -587,9 +617,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
                           P<uint32_t>(ctx->dbg_sz), P<int32_t>(ctx->dbg_sgid), s);
       ctx->launches += 2;
       CK(cudaGetLastError());
-      // the env's scene size
       EnvConst hc;
-      CK(cudaMemcpyAsync(&hc, P<EnvConst>(ctx->envc) + opts.debug_env, sizeof hc, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(&hc, P<EnvConst>(ctx->envc) + dbg_pos, sizeof hc, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       const int nn = std::max(hc.n, 0);
       ctx->d_tc.resize(nn); ctx->d_proj.resize((size_t)nn * 16);
@@ -624,8 +653,6 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   }
   if (ctx->timing) for (int i = 0; i < 3; ++i) ctx->stage_ms[i] = ms[i];
   ctx->last_E = E;
-  // sticky device errors (bad scene ids): read at the end, after the last
-  // chunk's kernels are enqueued
   CK(cudaMemcpyAsync(ctx->h_err, ctx->errflag.p, 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (*ctx->h_err & ERR_BAD_SCENE) return fail(ctx, GG_E_BAD_SCENE, "gg_render: an env is bound to an unknown scene id");

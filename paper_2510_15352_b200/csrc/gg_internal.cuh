@@ -36,7 +36,15 @@ struct EnvConst {
   int32_t scene;       // index into the scene table, -1 if invalid
   int32_t n;           // Gaussians in that scene (0 if invalid)
   int32_t degree;      // SH degree used at render
-  int32_t pad;
+  int32_t out_index;   // caller's env index (outputs, counters); envs are processed scene-sorted
+};
+
+// A run of <= ENV_GROUP chunk-local envs bound to the same scene; the
+// projection kernels load each Gaussian once and test it against the group.
+constexpr int ENV_GROUP = 16;
+struct EnvGroup {
+  int32_t elo;   // first chunk-local env
+  int32_t cnt;   // envs in the group (1..ENV_GROUP)
 };
 
 struct RenderParams {
@@ -61,7 +69,7 @@ struct ChunkWS {
   float4* rec2;         // (r, g, b, ext_y)
   uint2* rect;          // (x0 | x1<<16, y0 | y1<<16)
   uint32_t* zkey;       // f32 bits of z
-  uint32_t* gid;        // Gaussian index
+  uint32_t* gid;        // Gaussian index (debug dumps only; may be null)
   // depth-sort scratch [V]
   uint32_t* dk0; uint32_t* dv0; uint32_t* dk1; uint32_t* dv1;
   // tile-sort scratch [K]

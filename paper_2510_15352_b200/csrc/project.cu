@@ -8,23 +8,33 @@
 // lambda1, r, rect, depth bits) is computed in the canonical f32 order of
 // DESIGN.md §2.1 with non-contracting intrinsics (canonical.cuh).
 //
-// Work decomposition (DESIGN.md §4 K1): grid = (Gaussian blocks of 256,
-// envs of the chunk).  Pass 1 (cull_count) does the exact near/far test and
-// a CONSERVATIVE footprint test (never rejects a Gaussian the canonical rect
-// keeps), writes one visibility bit per (env, Gaussian) and per-block counts.
-// A per-env exclusive scan turns the counts into offsets, so pass 2
-// (project) compacts the records deterministically in Gaussian order.
+// Work decomposition (DESIGN.md §4 K1).  Envs are processed scene-sorted and
+// split into groups of <= 16 envs bound to one scene.  A CTA owns one block
+// of 256 Gaussians x one env group, and the grid runs env groups fastest so
+// consecutive CTAs reuse the same Gaussian block from L2 (the scene is read
+// from HBM about once per chunk, not once per env):
+//   K1a cull_count: each thread holds one Gaussian in registers and tests it
+//       against every camera of the group — exact near/far test plus a
+//       CONSERVATIVE footprint test that never rejects a Gaussian the
+//       canonical rect keeps — one ballot word per (env, 32 Gaussians) and a
+//       count per (env, block).
+//   K2  scan: per-env exclusive scan of the block counts (compaction offsets).
+//   K1b project: the CTA stages its 256 Gaussians (geometry + SH) in shared
+//       memory, flattens the visible (env, Gaussian) pairs of the group in
+//       (env, Gaussian) order, and projects them with full warps, writing
+//       each record at its compacted, Gaussian-ordered slot.
 #include "gg_internal.cuh"
 #include "canonical.cuh"
 
 namespace gg {
 
-__global__ void setup_envs_kernel(int E, const int32_t* __restrict__ scene_ids,
+__global__ void setup_envs_kernel(int E, const int32_t* __restrict__ perm, const int32_t* __restrict__ scene_ids,
                                   const float* __restrict__ viewmats, const float* __restrict__ intr,
                                   const DevScene* __restrict__ scenes, int nscenes, int W, int H,
                                   int sh_degree, EnvConst* out, uint32_t* err) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= E) return;
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= E) return;
+  const int e = perm ? perm[pos] : pos;
   EnvConst c;
   const float* V = viewmats + (size_t)e * 16;
 #pragma unroll
@@ -45,7 +55,7 @@ __global__ void setup_envs_kernel(int E, const int32_t* __restrict__ scene_ids,
   for (int k = 0; k < 3; ++k)
     c.C[k] = -(c.R[0 * 3 + k] * c.t[0] + c.R[1 * 3 + k] * c.t[1] + c.R[2 * 3 + k] * c.t[2]);
   const int sid = scene_ids[e];
-  c.pad = 0;
+  c.out_index = e;
   if (sid < 0 || sid >= nscenes || !scenes[sid].valid) {
     c.scene = -1; c.n = 0; c.degree = 0;
     atomicOr(err, (uint32_t)ERR_BAD_SCENE);
@@ -55,7 +65,7 @@ __global__ void setup_envs_kernel(int E, const int32_t* __restrict__ scene_ids,
     const int d = scenes[sid].degree;
     c.degree = sh_degree < 0 ? d : min(sh_degree, d);
   }
-  out[e] = c;
+  out[pos] = c;
 }
 
 // p = R mu + t in the canonical order: ((R_k0 mu_x + R_k1 mu_y) + R_k2 mu_z) + t_k
@@ -67,55 +77,71 @@ __device__ __forceinline__ float3 to_cam(const EnvConst& c, float4 g) {
   return p;
 }
 
-__global__ void __launch_bounds__(PROJ_BLOCK)
-cull_count_kernel(int e0, const EnvConst* __restrict__ envs, const DevScene* __restrict__ scenes,
-                  RenderParams rp, ChunkWS ws) {
-  const int eloc = blockIdx.y;
-  const EnvConst& c = envs[e0 + eloc];
-  const int i = blockIdx.x * PROJ_BLOCK + threadIdx.x;
-  bool keep = false;
-  if (i < c.n) {
-    const DevScene& sc = scenes[c.scene];
-    const float4 g = __ldg(&sc.pos_op[i]);
-    const float3 p = to_cam(c, g);
-    if (p.z > rp.near_p && p.z <= rp.far_p) {
-      const float rz = fd(1.f, p.z);
-      const float u = fa(fm(fm(c.fx, p.x), rz), c.cx);
-      const float v = fa(fm(fm(c.fy, p.y), rz), c.cy);
-      // conservative radius bound: lambda1 <= a + c + sqrt(0.1) and
-      // a + c <= s_max^2 |T|_F^2 + 0.6 (DESIGN.md §4 K1a); margins cover f32.
-      const float txz = fminf(c.lim_xp, fmaxf(-c.lim_xn, p.x * rz));
-      const float tyz = fminf(c.lim_yp, fmaxf(-c.lim_yn, p.y * rz));
-      const float J00 = c.fx * rz, J11 = c.fy * rz;
-      const float J02 = -c.fx * txz * rz, J12 = -c.fy * tyz * rz;
-      float nT = 0.f;
+__device__ __forceinline__ void load_group_cams(EnvConst* cams, const EnvConst* __restrict__ envs, int e0,
+                                                EnvGroup grp) {
+  const int words = sizeof(EnvConst) / 4;
+  const int* src = reinterpret_cast<const int*>(envs + e0 + grp.elo);
+  int* dst = reinterpret_cast<int*>(cams);
+  for (int i = threadIdx.x; i < grp.cnt * words; i += blockDim.x) dst[i] = src[i];
+}
+
+// conservative footprint test (DESIGN.md §4 K1a): lambda1 <= a + c + sqrt(0.1)
+// and a + c <= s_max^2 |T|_F^2 + 0.6; generous margins absorb f32 rounding.
+__device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float smax2, const RenderParams& rp) {
+  const float3 p = to_cam(c, g);
+  if (!(p.z > rp.near_p && p.z <= rp.far_p)) return false;   // exact (canonical p_z)
+  const float rz = 1.f / p.z;
+  const float u = c.fx * p.x * rz + c.cx;
+  const float v = c.fy * p.y * rz + c.cy;
+  const float txz = fminf(c.lim_xp, fmaxf(-c.lim_xn, p.x * rz));
+  const float tyz = fminf(c.lim_yp, fmaxf(-c.lim_yn, p.y * rz));
+  const float J00 = c.fx * rz, J11 = c.fy * rz;
+  const float J02 = -c.fx * txz * rz, J12 = -c.fy * tyz * rz;
+  float nT = 0.f;
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const float t0 = J00 * c.R[j] + J02 * c.R[6 + j];
-        const float t1 = J11 * c.R[3 + j] + J12 * c.R[6 + j];
-        nT += t0 * t0 + t1 * t1;
-      }
-      const float smax2 = __ldg(&sc.aux[i]).y;
-      const float lam_b = (smax2 * nT + 0.9163f) * 1.001f + 0.01f;
-      const float rb = 3.f * sqrtf(lam_b) * 1.001f + 1.5f;
-      keep = (u + rb > 0.f) && (u - rb < (float)(rp.TX * TILE)) && (v + rb > 0.f) &&
-             (v - rb < (float)(rp.TY * TILE));
+  for (int j = 0; j < 3; ++j) {
+    const float t0 = J00 * c.R[j] + J02 * c.R[6 + j];
+    const float t1 = J11 * c.R[3 + j] + J12 * c.R[6 + j];
+    nT += t0 * t0 + t1 * t1;
+  }
+  const float lam_b = (smax2 * nT + 0.9163f) * 1.001f + 0.01f;
+  const float rb = 3.f * sqrtf(lam_b) * 1.001f + 2.f;
+  return (u + rb > 0.f) && (u - rb < (float)(rp.TX * TILE)) && (v + rb > 0.f) && (v - rb < (float)(rp.TY * TILE));
+}
+
+__global__ void __launch_bounds__(PROJ_BLOCK)
+cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
+                  const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
+  __shared__ EnvConst cams[ENV_GROUP];
+  __shared__ uint32_t wc[ENV_GROUP][PROJ_BLOCK / 32];
+  const EnvGroup grp = groups[blockIdx.x];
+  load_group_cams(cams, envs, e0, grp);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.y * PROJ_BLOCK + threadIdx.x;
+  const int n = cams[0].n;
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+  float smax2 = 0.f;
+  if (i < n) {
+    const DevScene& sc = scenes[cams[0].scene];
+    g = __ldg(&sc.pos_op[i]);
+    smax2 = __ldg(&sc.aux[i]).y;
+  }
+  const int wi = blockIdx.y * (PROJ_BLOCK / 32) + warp;
+  for (int k = 0; k < grp.cnt; ++k) {
+    const bool keep = i < n && maybe_visible(cams[k], g, smax2, rp);
+    const uint32_t word = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) {
+      ws.flags[(size_t)(grp.elo + k) * ws.nwords + wi] = word;
+      wc[k][warp] = __popc(word);
     }
   }
-  const uint32_t word = __ballot_sync(0xffffffffu, keep);
-  __shared__ uint32_t wc[PROJ_BLOCK / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wi = blockIdx.x * (PROJ_BLOCK / 32) + warp;
-  if (lane == 0) {
-    ws.flags[(size_t)eloc * ws.nwords + wi] = word;
-    wc[warp] = __popc(word);
-  }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < grp.cnt) {
     uint32_t s = 0;
 #pragma unroll
-    for (int w = 0; w < PROJ_BLOCK / 32; ++w) s += wc[w];
-    ws.blkcnt[(size_t)eloc * ws.nblk + blockIdx.x] = s;
+    for (int w = 0; w < PROJ_BLOCK / 32; ++w) s += wc[threadIdx.x][w];
+    ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blockIdx.y] = s;
   }
 }
 
@@ -181,29 +207,106 @@ __device__ __forceinline__ void sh_eval(int deg, float x, float y, float z, floa
   Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
 }
 
+constexpr int SH_MAX = 48;              // floats per Gaussian at degree 3
+constexpr int SH_PITCH = PROJ_BLOCK + 1;
+
+struct ProjSmem {
+  EnvConst cams[ENV_GROUP];
+  float4 pos[PROJ_BLOCK], ca[PROJ_BLOCK], cb[PROJ_BLOCK];
+  float dcb[PROJ_BLOCK];
+  uint32_t cnt[ENV_GROUP * 8];       // popc per (env, word), then exclusive prefix
+  uint32_t kacc[ENV_GROUP];
+  uint32_t total;
+  uint16_t list[ENV_GROUP * PROJ_BLOCK];   // (k << 8) | local
+  float sh[1];                       // [SH_MAX][SH_PITCH] when degree > 0 (dynamic tail)
+};
+
 __global__ void __launch_bounds__(PROJ_BLOCK)
-project_kernel(int e0, const EnvConst* __restrict__ envs, const DevScene* __restrict__ scenes,
-               RenderParams rp, ChunkWS ws) {
-  const int eloc = blockIdx.y;
-  const EnvConst& c = envs[e0 + eloc];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i = blockIdx.x * PROJ_BLOCK + threadIdx.x;
-  const uint32_t word = ws.flags[(size_t)eloc * ws.nwords + blockIdx.x * (PROJ_BLOCK / 32) + warp];
-  __shared__ uint32_t wc[PROJ_BLOCK / 32];
-  __shared__ uint32_t ktot[PROJ_BLOCK / 32];
-  if (lane == 0) wc[warp] = __popc(word);
+project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
+               const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ProjSmem& sm = *reinterpret_cast<ProjSmem*>(smem_raw);
+  const EnvGroup grp = groups[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int gblk = blockIdx.y;
+  const int i0 = gblk * PROJ_BLOCK;
+  load_group_cams(sm.cams, envs, e0, grp);
+  // visibility words of the group -> (env, Gaussian) list in (env, gid) order
+  if (tid < ENV_GROUP * 8) {
+    const int k = tid >> 3, w = tid & 7;
+    uint32_t word = 0;
+    if (k < grp.cnt) word = ws.flags[(size_t)(grp.elo + k) * ws.nwords + gblk * 8 + w];
+    sm.cnt[tid] = __popc(word);
+  }
+  if (tid < ENV_GROUP) sm.kacc[tid] = 0;
   __syncthreads();
-  uint32_t wpre = 0;
-  for (int w = 0; w < warp; ++w) wpre += wc[w];
-  uint32_t ntiles = 0;
-  if ((word >> lane) & 1u) {
-    const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + blockIdx.x] + wpre +
-                     __popc(word & lanemask_lt());
-    const DevScene& sc = scenes[c.scene];
-    const float4 g = __ldg(&sc.pos_op[i]);
-    const float4 ca = __ldg(&sc.cov_a[i]);
-    const float4 cb = __ldg(&sc.cov_b[i]);
-    const float2 ax = __ldg(&sc.aux[i]);
+  if (tid < 32) {   // exclusive scan of 128 counts (4 per lane)
+    uint32_t c0 = sm.cnt[tid * 4], c1 = sm.cnt[tid * 4 + 1], c2 = sm.cnt[tid * 4 + 2], c3 = sm.cnt[tid * 4 + 3];
+    const uint32_t loc = c0 + c1 + c2 + c3;
+    uint32_t s = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (tid >= o) s += y;
+    }
+    uint32_t ex = s - loc;
+    sm.cnt[tid * 4] = ex; ex += c0;
+    sm.cnt[tid * 4 + 1] = ex; ex += c1;
+    sm.cnt[tid * 4 + 2] = ex; ex += c2;
+    sm.cnt[tid * 4 + 3] = ex;
+    if (tid == 31) sm.total = s;
+  }
+  __syncthreads();
+  const uint32_t total = sm.total;
+  if (total == 0) return;
+  if (tid < ENV_GROUP * 8) {
+    const int k = tid >> 3, w = tid & 7;
+    if (k < grp.cnt) {
+      uint32_t word = ws.flags[(size_t)(grp.elo + k) * ws.nwords + gblk * 8 + w];
+      uint32_t o = sm.cnt[tid];
+      while (word) {
+        const int b = __ffs(word) - 1;
+        word &= word - 1;
+        sm.list[o++] = (uint16_t)((k << 8) | (w * 32 + b));
+      }
+    }
+  }
+  // stage the block's Gaussians (visible in at least one env of the group)
+  const EnvConst& c0 = sm.cams[0];
+  const DevScene& sc = scenes[c0.scene];
+  const int deg = c0.degree;
+  const int K = (deg + 1) * (deg + 1);
+  {
+    const int i = i0 + tid;
+    if (i < c0.n) {
+      sm.pos[tid] = __ldg(&sc.pos_op[i]);
+      sm.ca[tid] = __ldg(&sc.cov_a[i]);
+      sm.cb[tid] = __ldg(&sc.cov_b[i]);
+      sm.dcb[tid] = __ldg(&sc.aux[i]).x;
+    }
+    if (deg > 0) {
+      // coalesced copy of [256][stride] -> transposed [K*3][SH_PITCH]
+      const int nf = K * 3;
+      const int nl = min(PROJ_BLOCK, c0.n - i0);
+      const float* src = sc.sh + (size_t)i0 * sc.sh_stride;
+      for (int x = tid; x < nl * sc.sh_stride; x += PROJ_BLOCK) {
+        const int l = x / sc.sh_stride, j = x - l * sc.sh_stride;
+        if (j < nf) sm.sh[j * SH_PITCH + l] = __ldg(&src[x]);
+      }
+    }
+  }
+  __syncthreads();
+
+  for (uint32_t s = tid; s < total; s += PROJ_BLOCK) {
+    const uint32_t ent = sm.list[s];
+    const int k = ent >> 8, l = ent & 255;
+    const EnvConst& c = sm.cams[k];
+    const int eloc = grp.elo + k;
+    const uint32_t rank = s - sm.cnt[k * 8];
+    const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + rank;
+    const float4 g = sm.pos[l];
+    const float4 ca = sm.ca[l];
+    const float4 cb = sm.cb[l];
     // O2.1 p = R mu + t, 1/z (canonical)
     const float3 p = to_cam(c, g);
     const float rz = fd(1.f, p.z);
@@ -251,33 +354,34 @@ project_kernel(int e0, const EnvConst* __restrict__ envs, const DevScene* __rest
       const float fy1 = fminf(fmaxf(ceilf(fm(fa(v, rr), 0.0625f)), 0.f), (float)rp.TY);
       if (fx0 < fx1 && fy0 < fy1) {
         x0 = (uint32_t)fx0; x1 = (uint32_t)fx1; y0 = (uint32_t)fy0; y1 = (uint32_t)fy1;
-        ntiles = (x1 - x0) * (y1 - y0);
       }
     }
+    const uint32_t ntiles = (x1 - x0) * (y1 - y0);
     // O2.8 colour
     float col[3];
-    if (c.degree == 0) {
-      col[0] = cb.z; col[1] = cb.w; col[2] = ax.x;
+    if (deg == 0) {
+      col[0] = cb.z; col[1] = cb.w; col[2] = sm.dcb[l];
     } else {
       float dx = g.x - c.C[0], dy = g.y - c.C[1], dz = g.z - c.C[2];
       const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
       dx *= inv; dy *= inv; dz *= inv;
       float Y[16];
-      sh_eval(c.degree, dx, dy, dz, Y);
-      const int K = (c.degree + 1) * (c.degree + 1);
-      const float* f = sc.sh + (size_t)i * sc.sh_stride;
+      sh_eval(deg, dx, dy, dz, Y);
       float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-      for (int k = 0; k < K; ++k) {
-        s0 += Y[k] * __ldg(&f[k * 3 + 0]);
-        s1 += Y[k] * __ldg(&f[k * 3 + 1]);
-        s2 += Y[k] * __ldg(&f[k * 3 + 2]);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q < K) {
+          s0 += Y[q] * sm.sh[(q * 3 + 0) * SH_PITCH + l];
+          s1 += Y[q] * sm.sh[(q * 3 + 1) * SH_PITCH + l];
+          s2 += Y[q] * sm.sh[(q * 3 + 2) * SH_PITCH + l];
+        }
       }
       col[0] = fminf(1.f, fmaxf(0.f, s0 + 0.5f));
       col[1] = fminf(1.f, fmaxf(0.f, s1 + 0.5f));
       col[2] = fminf(1.f, fmaxf(0.f, s2 + 0.5f));
     }
-    // blend-side culling extents: alpha >= 1/255 needs q <= 2 ln(255 o);
-    // the ellipse's half extents are sqrt(qmax * Sigma2_xx), sqrt(qmax * Sigma2_yy)
+    // blend-side culling extents: alpha >= 1/255 needs q <= 2 ln(255 o); the
+    // ellipse's half extents are sqrt(qmax Sigma2_xx), sqrt(qmax Sigma2_yy)
     // (+ margins, so the skip never changes a blend decision).
     const float o = g.w;
     float ex = -1.f, ey = -1.f;
@@ -291,41 +395,43 @@ project_kernel(int e0, const EnvConst* __restrict__ envs, const DevScene* __rest
     ws.rec2[r] = make_float4(col[0], col[1], col[2], ey);
     ws.rect[r] = make_uint2(x0 | (x1 << 16), y0 | (y1 << 16));
     ws.zkey[r] = __float_as_uint(p.z);
-    ws.gid[r] = (uint32_t)i;
+    if (ws.gid) ws.gid[r] = (uint32_t)(i0 + l);
+    if (ntiles) atomicAdd(&sm.kacc[k], ntiles);
   }
-  // per-env key count (integer atomics: order-independent, deterministic)
-  uint32_t s = ntiles;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) ktot[warp] = s;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t t = 0;
-#pragma unroll
-    for (int w = 0; w < PROJ_BLOCK / 32; ++w) t += ktot[w];
-    if (t) atomicAdd(&ws.kcnt[eloc], t);
-  }
+  if (tid < grp.cnt && sm.kacc[tid]) atomicAdd(&ws.kcnt[grp.elo + tid], sm.kacc[tid]);
 }
 
-void launch_setup_envs(int E, const int32_t* scene_ids, const float* viewmats, const float* intr,
-                       const DevScene* scenes, int nscenes, int W, int H, int sh_degree, EnvConst* out,
-                       uint32_t* err, cudaStream_t s) {
-  setup_envs_kernel<<<(E + 127) / 128, 128, 0, s>>>(E, scene_ids, viewmats, intr, scenes, nscenes, W, H,
+size_t project_smem(int degree) {
+  size_t base = offsetof(ProjSmem, sh);
+  base = (base + 15) & ~(size_t)15;
+  return base + (degree > 0 ? (size_t)SH_MAX * SH_PITCH * 4 : 16);
+}
+
+cudaError_t project_init() {
+  return cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)project_smem(3));
+}
+
+void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, const float* viewmats,
+                       const float* intr, const DevScene* scenes, int nscenes, int W, int H, int sh_degree,
+                       EnvConst* out, uint32_t* err, cudaStream_t s) {
+  setup_envs_kernel<<<(E + 127) / 128, 128, 0, s>>>(E, perm, scene_ids, viewmats, intr, scenes, nscenes, W, H,
                                                     sh_degree, out, err);
 }
 
-void launch_cull_count(int e0, int ec, int nblk, const EnvConst* envs, const DevScene* scenes,
-                       const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
-  cull_count_kernel<<<dim3(nblk, ec), PROJ_BLOCK, 0, s>>>(e0, envs, scenes, rp, ws);
+void launch_cull_count(int e0, int ngroups, int nblk, const EnvGroup* groups, const EnvConst* envs,
+                       const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
+  cull_count_kernel<<<dim3(ngroups, nblk), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws);
 }
 
 void launch_scan_blocks(int ec, int nblk, uint32_t* data, uint32_t* totals, cudaStream_t s) {
   scan_blocks_kernel<<<ec, 1024, 0, s>>>(data, nblk, totals);
 }
 
-void launch_project(int e0, int ec, int nblk, const EnvConst* envs, const DevScene* scenes,
-                    const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
-  project_kernel<<<dim3(nblk, ec), PROJ_BLOCK, 0, s>>>(e0, envs, scenes, rp, ws);
+void launch_project(int e0, int ngroups, int nblk, int max_degree, const EnvGroup* groups, const EnvConst* envs,
+                    const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
+  project_kernel<<<dim3(ngroups, nblk), PROJ_BLOCK, project_smem(max_degree), s>>>(e0, groups, envs, scenes, rp,
+                                                                                    ws);
 }
 
 }  // namespace gg

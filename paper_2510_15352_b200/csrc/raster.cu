@@ -35,12 +35,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 template <bool COUNTERS>
 __global__ void __launch_bounds__(TILE_PX)
-raster_kernel(int e0, RenderParams rp, ChunkWS ws, void* __restrict__ rgb, float* __restrict__ depth,
-              float* __restrict__ alpha_out, CounterOut co) {
+raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
+              float* __restrict__ depth, float* __restrict__ alpha_out, CounterOut co) {
   __shared__ float4 s0[TILE_PX], s1[TILE_PX], s2[TILE_PX];
   const int eloc = blockIdx.y;
   const int tile = blockIdx.x;
-  const int e = e0 + eloc;
+  const int e = envs[e0 + eloc].out_index;   // caller's env index
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tx = tile % rp.TX, ty = tile / rp.TX;
   const int bx = warp & 1, by = warp >> 1;
@@ -135,18 +135,22 @@ raster_kernel(int e0, RenderParams rp, ChunkWS ws, void* __restrict__ rgb, float
       atomicAdd(&co.env_counts[(size_t)e * 4 + 0], a);
       atomicAdd(&co.env_counts[(size_t)e * 4 + 1], c);
     }
+    if (tid == 0 && tile == 0 && co.env_counts) {
+      co.env_counts[(size_t)e * 4 + 2] = ws.vcnt[eloc];
+      co.env_counts[(size_t)e * 4 + 3] = ws.kcnt[eloc];
+    }
   }
 }
 
-void launch_raster(int e0, int ec, const RenderParams& rp, const ChunkWS& ws, void* rgb, float* depth,
-                   float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
+void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
+                   float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s) {
   CounterOut co{env_counts, dbg_neval, dbg_eloc};
   dim3 grid(rp.ntiles, ec);
   if (counters)
-    raster_kernel<true><<<grid, TILE_PX, 0, s>>>(e0, rp, ws, rgb, depth, alpha, co);
+    raster_kernel<true><<<grid, TILE_PX, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha, co);
   else
-    raster_kernel<false><<<grid, TILE_PX, 0, s>>>(e0, rp, ws, rgb, depth, alpha, co);
+    raster_kernel<false><<<grid, TILE_PX, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha, co);
 }
 
 }  // namespace gg
