@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -28,7 +29,9 @@ void launch_project(int e0, int ngroups, int nblk, int max_degree, const EnvGrou
                     const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
 cudaError_t project_init();
 cudaError_t sort_bin_init();
-void launch_sort_bin(int ec, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
+uint32_t sort_blocks(uint32_t V);
+int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, const RenderParams& rp, const ChunkWS& ws,
+                    uint32_t* ghist, uint32_t* thist, cudaStream_t s);
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s);
@@ -73,7 +76,7 @@ struct gg_context {
   // workspace
   DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase;
   DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1;
-  DevBuf sorted, ranges, counters, valid_out, perm, groups;
+  DevBuf sorted, ranges, counters, valid_out, perm, groups, blkbase, ghist, thist;
   DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval;
   DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
   // pinned host mirrors
@@ -85,6 +88,7 @@ struct gg_context {
   int32_t* h_ids = nullptr;
   int32_t* h_perm = nullptr;
   EnvGroup* h_groups = nullptr;
+  uint32_t* h_blkbase = nullptr;
   int h_cap = 0;
   // debug snapshot (host)
   std::vector<int32_t> d_tc, d_stile, d_sgid, d_ranges, d_neval;
@@ -157,8 +161,9 @@ bool ensure(gg_context* ctx, DevBuf& b, size_t bytes, cudaStream_t s) {
 bool ensure_host(gg_context* ctx, int n) {
   if (ctx->h_cap >= n) return true;
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase); cudaFreeHost(ctx->h_kbase);
-  cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups);
+  cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
   int cap = std::max(n, 1024);
+  if (cudaMallocHost(&ctx->h_blkbase, (cap + 1) * 4) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_ids, cap * 4) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_perm, cap * 4) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_groups, cap * sizeof(EnvGroup)) != cudaSuccess) return false;
@@ -266,6 +271,7 @@ gg_status gg_destroy(gg_context* ctx) {
   DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
                    &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect,
                    &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->perm, &ctx->groups,
+                   &ctx->blkbase, &ctx->ghist, &ctx->thist,
                    &ctx->sorted, &ctx->ranges, &ctx->counters, &ctx->valid_out,
                    &ctx->dbg_tc, &ctx->dbg_proj, &ctx->dbg_stile, &ctx->dbg_sz, &ctx->dbg_sgid,
                    &ctx->dbg_neval, &ctx->h_in};
@@ -273,7 +279,7 @@ gg_status gg_destroy(gg_context* ctx) {
   cudaStreamSynchronize(s);
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
   cudaFreeHost(ctx->h_kbase); cudaFreeHost(ctx->h_err);
-  cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups);
+  cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev_copy);
   cudaStreamDestroy(s);
@@ -576,9 +582,16 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       return fail(ctx, GG_E_OOM, "gg_render: key workspace (%llu keys) allocation failed", (unsigned long long)K);
     CK(cudaMemcpyAsync(P<uint64_t>(ctx->kbase), ctx->h_kbase, ec * 8, cudaMemcpyHostToDevice, s));
     ws.sorted = P<uint32_t>(ctx->sorted);
-    // K3-K5
-    launch_sort_bin(ec, rp, ws, s);
-    ctx->launches++;
+    // K3-K5: sort blocks of 8192 records, never straddling an env
+    uint32_t nb = 0;
+    for (int i = 0; i < ec; ++i) { ctx->h_blkbase[i] = nb; nb += sort_blocks(ctx->h_vcnt[i]); }
+    ctx->h_blkbase[ec] = nb;
+    if (!ensure(ctx, ctx->blkbase, (size_t)(ec + 1) * 4, s) || !ensure(ctx, ctx->ghist, (size_t)nb * 256 * 4, s) ||
+        !ensure(ctx, ctx->thist, (size_t)nb * ntiles * 4, s))
+      return fail(ctx, GG_E_OOM, "gg_render: sort workspace allocation failed");
+    CK(cudaMemcpyAsync(ctx->blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, cudaMemcpyHostToDevice, s));
+    ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->blkbase), rp, ws, P<uint32_t>(ctx->ghist),
+                                     P<uint32_t>(ctx->thist), s);
     CK(cudaGetLastError());
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], s));
     // K6

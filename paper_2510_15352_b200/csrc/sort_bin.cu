@@ -1,43 +1,75 @@
 // sort_bin.cu — K3-K5: per-env depth presort, stable tile placement and tile
-// ranges, one CTA per environment.
+// ranges, as massively parallel passes over a whole env chunk.
 //
 // Defines the per-tile lists of SPEC.md:136-144 (bin_and_sort: "each tile
 // lists every gaussian whose 3-sigma footprint intersects it, sorted
 // ascending by view_depth; ties broken by input index (stable)").  The
 // canonical list (DESIGN.md §2 O3) is the triples (tile, depth bits, gid) in
 // ascending order.  We produce it without ever materialising 64-bit keys:
-//   0. one pass over the env's records builds the four 8-bit digit
-//      histograms of the depth bits and the tile histogram; an exclusive
-//      scan of the latter IS the tile-range table (K5)
-//   1. stable LSD radix sort of the records (already in gid order) by the
-//      f32 depth bits, skipping passes whose digit is constant  -> (z, gid)
-//   2. walk the records in that order; each record's tiles are appended to
-//      a shared-memory list in record order, and ONE warp places the list
-//      32 entries at a time: __match_any_sync groups equal tiles, the group
-//      leader advances that tile's cursor.  Every tile's entries therefore
-//      land in (z, gid) order at their final position: (tile, z, gid).
-// Deterministic: no float math, no order-dependent atomics.
+//   1. stable LSD radix sort of every env's records (already in gid order)
+//      by the f32 depth bits: 4 passes of 8 bits               -> (z, gid)
+//   2. stable bucketing of the records' tiles (row-major) by tile id, the
+//      records taken in depth order                          -> (tile, z, gid)
+//   3. the per-env tile totals' exclusive scan is the range table (K5).
+//
+// Each pass is three launches over the chunk's records, split into blocks
+// of 8192 that never straddle an env segment:
+//   upsweep   — per-block histogram (digit or tile) -> global table
+//   scan      — one CTA per env: exclusive prefix over (digit, block) in
+//               digit-major order = each block's output offset per digit
+//   downsweep — the block ranks its elements stably (warp-owned 256-element
+//               slices, ballot multisplit, per-warp counters, prefix over
+//               warps), stages them in shared memory in digit order, and
+//               writes contiguous per-digit runs at the block's offsets.
+// Thousands of independent blocks per pass keep HBM busy; staged runs keep
+// the writes coalesced.  No float math, no order-dependent atomics:
+// identical inputs give bit-identical lists.
 #include "gg_internal.cuh"
 
 namespace gg {
 
-constexpr int SB_THREADS = 256;
-constexpr int SB_WARPS = SB_THREADS / 32;
+constexpr int SB_THREADS = 1024;
+constexpr int SB_WARPS = 32;
 constexpr int SB_IPT = 8;
-constexpr int SB_TILE = SB_THREADS * SB_IPT;
-constexpr int SB_CAP = 2048;     // placement list capacity (pairs)
+constexpr int SB_BLK = SB_THREADS * SB_IPT;   // 8192 elements / records per block
 
-struct SortSmem {
-  uint32_t hist[4][256];
-  uint32_t wcnt[SB_WARPS][256];
-  uint32_t wsum[SB_WARPS];
-  uint32_t cur[256];
-  uint2 list[SB_CAP];             // (tile, record)
-  uint32_t tcur[1];               // [ntiles] tile cursors (dynamic tail)
+// blocks of the chunk: env of block b is the e with blk_base[e] <= b < blk_base[e+1]
+struct BlockTable {
+  const uint32_t* blk_base;   // [ec + 1]
+  int ec;
 };
 
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* wsum, uint32_t* total) {
+__device__ __forceinline__ int block_env(const BlockTable& bt, uint32_t b) {
+  int lo = 0, hi = bt.ec;   // last e with blk_base[e] <= b
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (bt.blk_base[mid] <= b) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t peers_of(uint32_t v, int bits, uint32_t active) {
+  uint32_t peers = active;
+#pragma unroll 8
+  for (int b = 0; b < bits; ++b) {
+    const bool bit = (v >> b) & 1u;
+    const uint32_t m = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
+struct RankSmem {
+  uint32_t wcnt[SB_WARPS][256];   // per-warp digit counts -> offsets
+  uint32_t dstart[256];
+  uint32_t dcnt[256];
+  uint32_t wsum[SB_WARPS];
+};
+
+// exclusive scan over the block (all threads call); *total = block sum
+__device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* wsum, uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
   uint32_t s = x;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -47,214 +79,359 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* wsum, 
   if (lane == 31) wsum[warp] = s;
   __syncthreads();
   if (warp == 0) {
-    uint32_t t = lane < SB_WARPS ? wsum[lane] : 0u;
+    uint32_t t = lane < nw ? wsum[lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
       if (lane >= o) t += y;
     }
-    if (lane < SB_WARPS) wsum[lane] = t;
+    if (lane < nw) wsum[lane] = t;
   }
   __syncthreads();
   const uint32_t excl = (warp ? wsum[warp - 1] : 0u) + s - x;
-  *total = wsum[SB_WARPS - 1];
+  *total = wsum[nw - 1];
   __syncthreads();
   return excl;
 }
 
-// One stable counting pass on digit (key >> shift) & 255 with a precomputed
-// histogram.  vin == nullptr means identity values; kout == nullptr skips
-// writing keys (last pass).
-__device__ void radix_pass(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                           uint32_t* __restrict__ kout, uint32_t* __restrict__ vout, uint32_t n, int shift,
-                           const uint32_t* hist, SortSmem& sm) {
+// Block-local stable ranking of up to 8192 elements: element (warp w, round
+// j, lane l) has block index 256 w + 32 j + l and digit d[j] < 2^bits.  On
+// return lpos[j] is its position in the block sorted stably by digit, and
+// rs.dstart / rs.dcnt hold digit starts / counts.  rs.wcnt is zero on entry
+// and on return.
+__device__ __forceinline__ void block_rank(const uint32_t (&d)[SB_IPT], uint32_t n, int bits,
+                                           uint32_t (&lpos)[SB_IPT], RankSmem& rs) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // exclusive scan of the 256-bin histogram -> cursors
-  {
-    const uint32_t x = hist[tid];
-    uint32_t total;
-    const uint32_t ex = block_excl_scan(x, sm.wsum, &total);
-    sm.cur[tid] = ex;
+  const uint32_t lt = lanemask_lt();
+  uint32_t rk[SB_IPT];
+#pragma unroll
+  for (int j = 0; j < SB_IPT; ++j) {
+    const uint32_t e = warp * 32 * SB_IPT + j * 32 + lane;
+    const bool ok = e < n;
+    const uint32_t active = __ballot_sync(0xffffffffu, ok);
+    rk[j] = 0;
+    if (active) {
+      const uint32_t peers = peers_of(d[j], bits, active);
+      const uint32_t before = ok ? rs.wcnt[warp][d[j]] : 0u;
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) rs.wcnt[warp][d[j]] = before + __popc(peers);
+      __syncwarp();
+      rk[j] = before + __popc(peers & lt);
+    }
   }
   __syncthreads();
-  for (uint32_t base = 0; base < n; base += SB_TILE) {
-    const uint32_t wbase = base + warp * 32 * SB_IPT;
-    uint32_t k[SB_IPT], v[SB_IPT], rk[SB_IPT];
-#pragma unroll
-    for (int j = 0; j < SB_IPT; ++j) {
-      const uint32_t idx = wbase + j * 32 + lane;
-      const bool valid = idx < n;
-      k[j] = valid ? kin[idx] : 0u;
-      v[j] = valid ? (vin ? vin[idx] : idx) : 0u;
+  const int radix = 1 << bits;
+  uint32_t c = 0;
+  if (tid < radix) {
+#pragma unroll 8
+    for (int w = 0; w < SB_WARPS; ++w) {
+      const uint32_t x = rs.wcnt[w][tid];
+      rs.wcnt[w][tid] = c;
+      c += x;
     }
-#pragma unroll
-    for (int j = 0; j < SB_IPT; ++j) {
-      const uint32_t idx = wbase + j * 32 + lane;
-      const bool valid = idx < n;
-      const uint32_t d = valid ? ((k[j] >> shift) & 255u) : 256u;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      const uint32_t before = valid ? sm.wcnt[warp][d] : 0u;
-      __syncwarp();
-      if (valid && lane == __ffs(peers) - 1) sm.wcnt[warp][d] = before + __popc(peers);
-      __syncwarp();
-      rk[j] = before + __popc(peers & lanemask_lt());
-    }
-    __syncthreads();
-    {   // per-digit prefix over warps, starting at the global cursor
-      uint32_t run = sm.cur[tid];
-#pragma unroll
-      for (int w = 0; w < SB_WARPS; ++w) {
-        const uint32_t t = sm.wcnt[w][tid];
-        sm.wcnt[w][tid] = run;
-        run += t;
-      }
-      sm.cur[tid] = run;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < SB_IPT; ++j) {
-      const uint32_t idx = wbase + j * 32 + lane;
-      if (idx < n) {
-        const uint32_t d = (k[j] >> shift) & 255u;
-        const uint32_t pos = sm.wcnt[warp][d] + rk[j];
-        if (kout) kout[pos] = k[j];
-        vout[pos] = v[j];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int w = 0; w < SB_WARPS; ++w) sm.wcnt[w][tid] = 0u;
-    __syncthreads();
+    rs.dcnt[tid] = c;
   }
+  uint32_t total;
+  const uint32_t ex = block_scan(tid < radix ? c : 0u, rs.wsum, &total);
+  if (tid < radix) rs.dstart[tid] = ex;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < SB_IPT; ++j) {
+    const uint32_t e = warp * 32 * SB_IPT + j * 32 + lane;
+    lpos[j] = e < n ? rs.dstart[d[j]] + rs.wcnt[warp][d[j]] + rk[j] : 0u;
+  }
+  __syncthreads();
+  if (tid < radix)
+#pragma unroll 8
+    for (int w = 0; w < SB_WARPS; ++w) rs.wcnt[w][tid] = 0u;
 }
 
 __device__ __forceinline__ void unpack_rect(uint2 r, uint32_t& x0, uint32_t& x1, uint32_t& y0, uint32_t& y1) {
   x0 = r.x & 0xffffu; x1 = r.x >> 16; y0 = r.y & 0xffffu; y1 = r.y >> 16;
 }
 
+// Input / output arrays of depth pass p (all indexed rec_base[e] + j).
+struct DepthIO {
+  const uint32_t* kin;   // keys in
+  const uint32_t* vin;   // values in (null = identity j)
+  uint32_t* kout;        // keys out (null on the last pass)
+  uint32_t* vout;
+};
+
+// ---- depth passes --------------------------------------------------------
 __global__ void __launch_bounds__(SB_THREADS)
-sort_bin_kernel(RenderParams rp, ChunkWS ws) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
-  const int eloc = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t rb = ws.rec_base[eloc];
-  const uint64_t kb = ws.k_base[eloc];
-  const uint32_t V = ws.vcnt[eloc];
-  for (int i = tid; i < 4 * 256; i += SB_THREADS) (&sm.hist[0][0])[i] = 0u;
-  for (int w = 0; w < SB_WARPS; ++w) sm.wcnt[w][tid] = 0u;
-  for (int i = tid; i < rp.ntiles; i += SB_THREADS) sm.tcur[i] = 0u;
+depth_upsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, uint32_t* ghist) {
+  __shared__ uint32_t h[256];
+  const uint32_t b = blockIdx.x;
+  const int e = block_env(bt, b);
+  const uint32_t j0 = (b - bt.blk_base[e]) * SB_BLK;
+  const uint32_t V = ws.vcnt[e];
+  const uint32_t n = min((uint32_t)SB_BLK, V - j0);
+  const uint64_t rb = ws.rec_base[e];
+  if (threadIdx.x < 256) h[threadIdx.x] = 0;
   __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += SB_THREADS)
+    atomicAdd(&h[(io.kin[rb + j0 + i] >> shift) & 255u], 1u);
+  __syncthreads();
+  if (threadIdx.x < 256) ghist[(size_t)b * 256 + threadIdx.x] = h[threadIdx.x];
+}
 
-  // ---- 0. digit histograms of the depth bits + tile histogram ----------
-  const uint32_t* zk = ws.zkey + rb;
-  const uint2* rect = ws.rect + rb;
-  for (uint32_t j = tid; j < V; j += SB_THREADS) {
-    const uint32_t z = zk[j];
-    atomicAdd(&sm.hist[0][z & 255u], 1u);
-    atomicAdd(&sm.hist[1][(z >> 8) & 255u], 1u);
-    atomicAdd(&sm.hist[2][(z >> 16) & 255u], 1u);
-    atomicAdd(&sm.hist[3][z >> 24], 1u);
-    uint32_t x0, x1, y0, y1;
-    unpack_rect(rect[j], x0, x1, y0, y1);
-    for (uint32_t ty = y0; ty < y1; ++ty)
-      for (uint32_t tx = x0; tx < x1; ++tx) atomicAdd(&sm.tcur[ty * rp.TX + tx], 1u);
+// one CTA (256 threads = digits) per env: ghist[b][d] -> output offset of
+// (block b, digit d) relative to the env's segment
+__global__ void __launch_bounds__(256) depth_scan_kernel(BlockTable bt, uint32_t* ghist) {
+  __shared__ uint32_t wsum[8];
+  const int e = blockIdx.x;
+  const uint32_t b0 = bt.blk_base[e], b1 = bt.blk_base[e + 1];
+  const int d = threadIdx.x;
+  uint32_t run = 0;
+  for (uint32_t b = b0; b < b1; ++b) {
+    const uint32_t x = ghist[(size_t)b * 256 + d];
+    ghist[(size_t)b * 256 + d] = run;
+    run += x;
   }
-  __syncthreads();
-  // ---- K5: tile ranges = exclusive scan of the tile histogram ----------
-  {
-    uint32_t carry = 0;
-    for (int base = 0; base < rp.ntiles; base += SB_THREADS) {
-      const int t = base + tid;
-      const uint32_t c = t < rp.ntiles ? sm.tcur[t] : 0u;
-      uint32_t total;
-      const uint32_t ex = carry + block_excl_scan(c, sm.wsum, &total);
-      if (t < rp.ntiles) {
-        ws.ranges[(size_t)eloc * rp.ntiles + t] = make_uint2(ex, ex + c);
-        sm.tcur[t] = ex;          // becomes the placement cursor
-      }
-      carry += total;
-    }
-  }
-  // which depth digits vary?  (a constant digit leaves the order unchanged)
-  __shared__ uint32_t live_mask;
-  if (tid == 0) live_mask = 0;
-  __syncthreads();
+  // digit-major exclusive scan of the totals (256 threads = 8 warps)
+  const int lane = d & 31, warp = d >> 5;
+  uint32_t s = run;
 #pragma unroll
-  for (int p = 0; p < 4; ++p)
-    if (sm.hist[p][tid] == V && V > 0) atomicOr(&live_mask, 1u << (4 + p));   // bit 4+p: constant
-  __syncthreads();
-  const uint32_t constant = live_mask >> 4;
-
-  // ---- 1. stable LSD depth sort ------------------------------------------
-  const uint32_t* ck = zk;
-  const uint32_t* cv = nullptr;   // identity (records are in gid order)
-  uint32_t* bufk[2] = {ws.dk0 + rb, ws.dk1 + rb};
-  uint32_t* bufv[2] = {ws.dv0 + rb, ws.dv1 + rb};
-  int last = -1;
-  for (int p = 0; p < 4; ++p)
-    if (!((constant >> p) & 1u)) last = p;
-  int nb = 0;
-  for (int p = 0; p < 4; ++p) {
-    if ((constant >> p) & 1u) continue;
-    radix_pass(ck, cv, p == last ? nullptr : bufk[nb], bufv[nb], V, p * 8, sm.hist[p], sm);
-    ck = bufk[nb];
-    cv = bufv[nb];
-    nb ^= 1;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= o) s += y;
   }
+  if (lane == 31) wsum[warp] = s;
+  __syncthreads();
+  uint32_t off = 0;
+  for (int w = 0; w < warp; ++w) off += wsum[w];
+  const uint32_t base = off + s - run;
+  for (uint32_t b = b0; b < b1; ++b) ghist[(size_t)b * 256 + d] += base;
+}
 
-  // ---- 2. stable placement in (z, gid) order ------------------------------
-  uint32_t* out = ws.sorted + kb;
-  for (uint32_t base = 0; base < V; base += SB_THREADS) {
-    const uint32_t j = base + tid;
+struct DownSmem {
+  RankSmem rs;
+  uint32_t sk[SB_BLK];
+  uint32_t sv[SB_BLK];
+};
+
+__global__ void __launch_bounds__(SB_THREADS)
+depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const uint32_t* ghist) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  DownSmem& sm = *reinterpret_cast<DownSmem*>(smem_raw);
+  const uint32_t b = blockIdx.x;
+  const int e = block_env(bt, b);
+  const uint32_t j0 = (b - bt.blk_base[e]) * SB_BLK;
+  const uint32_t V = ws.vcnt[e];
+  const uint32_t n = min((uint32_t)SB_BLK, V - j0);
+  const uint64_t rb = ws.rec_base[e];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < SB_WARPS * 256; i += SB_THREADS) (&sm.rs.wcnt[0][0])[i] = 0u;
+  __syncthreads();
+  uint32_t k[SB_IPT], v[SB_IPT], d[SB_IPT], lp[SB_IPT];
+#pragma unroll
+  for (int j = 0; j < SB_IPT; ++j) {
+    const uint32_t i = warp * 32 * SB_IPT + j * 32 + lane;
+    const bool ok = i < n;
+    k[j] = ok ? io.kin[rb + j0 + i] : 0u;
+    v[j] = ok ? (io.vin ? io.vin[rb + j0 + i] : j0 + i) : 0u;
+    d[j] = (k[j] >> shift) & 255u;
+  }
+  block_rank(d, n, 8, lp, sm.rs);
+#pragma unroll
+  for (int j = 0; j < SB_IPT; ++j) {
+    const uint32_t i = warp * 32 * SB_IPT + j * 32 + lane;
+    if (i < n) { sm.sk[lp[j]] = k[j]; sm.sv[lp[j]] = v[j]; }
+  }
+  __syncthreads();
+  const uint32_t* off = ghist + (size_t)b * 256;
+  for (uint32_t q = tid; q < n; q += SB_THREADS) {
+    const uint32_t kk = sm.sk[q];
+    const uint32_t dd = (kk >> shift) & 255u;
+    const uint64_t pos = rb + off[dd] + (q - sm.rs.dstart[dd]);
+    if (io.kout) io.kout[pos] = kk;
+    io.vout[pos] = sm.sv[q];
+  }
+}
+
+// ---- tile placement ------------------------------------------------------
+// order[rb + j] = record (gid-ordered local index) of depth rank j
+__global__ void __launch_bounds__(SB_THREADS)
+place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntiles, int TX, uint32_t* thist) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
+  const uint32_t b = blockIdx.x;
+  const int e = block_env(bt, b);
+  const uint32_t j0 = (b - bt.blk_base[e]) * SB_BLK;
+  const uint32_t n = min((uint32_t)SB_BLK, ws.vcnt[e] - j0);
+  const uint64_t rb = ws.rec_base[e];
+  for (int i = threadIdx.x; i < ntiles; i += SB_THREADS) h[i] = 0u;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += SB_THREADS) {
+    const uint2 r = ws.rect[rb + order[rb + j0 + i]];
+    uint32_t x0, x1, y0, y1;
+    unpack_rect(r, x0, x1, y0, y1);
+    for (uint32_t ty = y0; ty < y1; ++ty)
+      for (uint32_t tx = x0; tx < x1; ++tx) atomicAdd(&h[ty * TX + tx], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ntiles; i += SB_THREADS) thist[(size_t)b * ntiles + i] = h[i];
+}
+
+// one CTA per env: thist[b][t] -> output offset (relative to k_base[e]) of
+// (block b, tile t); ranges[e][t] = [start, end)
+__global__ void __launch_bounds__(SB_THREADS) place_scan_kernel(BlockTable bt, ChunkWS ws, uint32_t* thist,
+                                                                int ntiles) {
+  __shared__ uint32_t wsum[SB_WARPS];
+  const int e = blockIdx.x;
+  const uint32_t b0 = bt.blk_base[e], b1 = bt.blk_base[e + 1];
+  uint32_t carry = 0;
+  for (int base = 0; base < ntiles; base += SB_THREADS) {
+    const int t = base + threadIdx.x;
+    uint32_t run = 0;
+    if (t < ntiles)
+      for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t x = thist[(size_t)b * ntiles + t];
+        thist[(size_t)b * ntiles + t] = run;
+        run += x;
+      }
+    uint32_t total;
+    const uint32_t ex = carry + block_scan(t < ntiles ? run : 0u, wsum, &total);
+    if (t < ntiles) {
+      ws.ranges[(size_t)e * ntiles + t] = make_uint2(ex, ex + run);
+      for (uint32_t b = b0; b < b1; ++b) thist[(size_t)b * ntiles + t] += ex;
+    }
+    carry += total;
+  }
+}
+
+struct PlaceSmem {
+  RankSmem rs;
+  uint32_t sk[SB_BLK];
+  uint32_t sv[SB_BLK];
+  uint32_t tcur[1];     // [ntiles] cursors, then [ntiles] run starts (dynamic tail)
+};
+
+__global__ void __launch_bounds__(SB_THREADS)
+place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderParams rp, const uint32_t* thist) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PlaceSmem& sm = *reinterpret_cast<PlaceSmem*>(smem_raw);
+  const int nt = rp.ntiles;
+  uint32_t* tcur = sm.tcur;
+  uint32_t* trun = sm.tcur + nt;
+  const uint32_t b = blockIdx.x;
+  const int e = block_env(bt, b);
+  const uint32_t j0 = (b - bt.blk_base[e]) * SB_BLK;
+  const uint32_t nrec = min((uint32_t)SB_BLK, ws.vcnt[e] - j0);
+  const uint64_t rb = ws.rec_base[e];
+  uint32_t* out = ws.sorted + ws.k_base[e];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < SB_WARPS * 256; i += SB_THREADS) (&sm.rs.wcnt[0][0])[i] = 0u;
+  for (int i = tid; i < nt; i += SB_THREADS) tcur[i] = thist[(size_t)b * nt + i];
+  int tb = 0;
+  while ((1 << tb) < nt) ++tb;
+  const int lo_bits = tb < 7 ? tb : 7;
+  const int hi_bits = tb - lo_bits;
+  __syncthreads();
+  // records in rounds of 1024 (one per thread), pairs flattened in record order
+  for (uint32_t r0 = 0; r0 < nrec; r0 += SB_THREADS) {
+    const uint32_t j = r0 + tid;
     uint32_t idx = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
-    if (j < V) {
-      idx = cv ? cv[j] : j;
-      unpack_rect(rect[idx], x0, x1, y0, y1);
+    if (j < nrec) {
+      idx = order[rb + j0 + j];
+      unpack_rect(ws.rect[rb + idx], x0, x1, y0, y1);
     }
     const uint32_t w = x1 - x0;
-    const uint32_t n = w * (y1 - y0);
+    const uint32_t np = w * (y1 - y0);
     uint32_t total;
-    const uint32_t excl = block_excl_scan(n, sm.wsum, &total);
-    for (uint32_t w0 = 0; w0 < total; w0 += SB_CAP) {
-      // this thread's pairs with flattened position in [w0, w0 + CAP)
+    const uint32_t excl = block_scan(np, sm.rs.wsum, &total);
+    for (uint32_t w0 = 0; w0 < total; w0 += SB_BLK) {
+      const uint32_t n = min((uint32_t)SB_BLK, total - w0);
       const uint32_t qa = excl >= w0 ? 0u : w0 - excl;
-      const uint32_t qb = min(n, w0 + SB_CAP > excl ? w0 + SB_CAP - excl : 0u);
+      const uint32_t qb = min(np, w0 + SB_BLK > excl ? w0 + SB_BLK - excl : 0u);
       for (uint32_t q = qa; q < qb; ++q) {
         const uint32_t ty = y0 + q / w, tx = x0 + q % w;
-        sm.list[excl + q - w0] = make_uint2(ty * rp.TX + tx, idx);
+        sm.sk[excl + q - w0] = ty * rp.TX + tx;
+        sm.sv[excl + q - w0] = idx;
       }
       __syncthreads();
-      if (warp == 0) {
-        const uint32_t m = min((uint32_t)SB_CAP, total - w0);
-        for (uint32_t g = 0; g < m; g += 32) {
-          const bool valid = g + lane < m;
-          const uint2 e = valid ? sm.list[g + lane] : make_uint2(0xffffffffu, 0u);
-          const uint32_t peers = __match_any_sync(0xffffffffu, e.x);
-          const uint32_t before = valid ? sm.tcur[e.x] : 0u;
-          __syncwarp();
-          if (valid && lane == __ffs(peers) - 1) sm.tcur[e.x] = before + __popc(peers);
-          __syncwarp();
-          if (valid) out[before + __popc(peers & lanemask_lt())] = e.y;
+      for (int pass = 0; pass < (hi_bits > 0 ? 2 : 1); ++pass) {
+        const int sh = pass == 0 ? 0 : lo_bits;
+        const int bits = pass == 0 ? lo_bits : hi_bits;
+        uint32_t t[SB_IPT], v[SB_IPT], d[SB_IPT], lp[SB_IPT];
+#pragma unroll
+        for (int jj = 0; jj < SB_IPT; ++jj) {
+          const uint32_t i = warp * 32 * SB_IPT + jj * 32 + lane;
+          t[jj] = i < n ? sm.sk[i] : 0u;
+          v[jj] = i < n ? sm.sv[i] : 0u;
+          d[jj] = (t[jj] >> sh) & ((1u << bits) - 1u);
         }
+        block_rank(d, n, bits, lp, sm.rs);
+#pragma unroll
+        for (int jj = 0; jj < SB_IPT; ++jj) {
+          const uint32_t i = warp * 32 * SB_IPT + jj * 32 + lane;
+          if (i < n) { sm.sk[lp[jj]] = t[jj]; sm.sv[lp[jj]] = v[jj]; }
+        }
+        __syncthreads();
+      }
+      for (uint32_t q = tid; q < n; q += SB_THREADS) {
+        const uint32_t tt = sm.sk[q];
+        if (q == 0 || sm.sk[q - 1] != tt) trun[tt] = q;
+      }
+      __syncthreads();
+      for (uint32_t q = tid; q < n; q += SB_THREADS) {
+        const uint32_t tt = sm.sk[q];
+        out[tcur[tt] + (q - trun[tt])] = sm.sv[q];
+      }
+      __syncthreads();
+      for (uint32_t q = tid; q < n; q += SB_THREADS) {
+        const uint32_t tt = sm.sk[q];
+        if (q == n - 1 || sm.sk[q + 1] != tt) tcur[tt] += q - trun[tt] + 1;
       }
       __syncthreads();
     }
   }
 }
 
-size_t sort_bin_smem(int ntiles) {
-  size_t base = offsetof(SortSmem, tcur);
-  return base + (size_t)ntiles * 4;
-}
+// ---- host side -------------------------------------------------------------
+size_t depth_down_smem() { return sizeof(DownSmem); }
+size_t place_down_smem(int ntiles) { return offsetof(PlaceSmem, tcur) + (size_t)ntiles * 8; }
 
 cudaError_t sort_bin_init() {
-  return cudaFuncSetAttribute(sort_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sort_bin_smem(MAX_TILES));
+  cudaError_t e = cudaFuncSetAttribute(depth_downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)depth_down_smem());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(place_downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)place_down_smem(MAX_TILES));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(place_upsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(MAX_TILES * 4));
 }
 
-void launch_sort_bin(int ec, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
-  sort_bin_kernel<<<ec, SB_THREADS, sort_bin_smem(rp.ntiles), s>>>(rp, ws);
+uint32_t sort_blocks(uint32_t V) { return (V + SB_BLK - 1) / SB_BLK; }
+
+// Enqueue K3-K5 for a chunk.  blk_base: device [ec+1] block prefix; nb total
+// blocks; ghist >= nb*256 u32; thist >= nb*ntiles u32.  Returns launches.
+int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, const RenderParams& rp, const ChunkWS& ws,
+                    uint32_t* ghist, uint32_t* thist, cudaStream_t s) {
+  if (nb == 0) {
+    cudaMemsetAsync(ws.ranges, 0, (size_t)ec * rp.ntiles * sizeof(uint2), s);
+    return 0;
+  }
+  BlockTable bt{blk_base, ec};
+  int launches = 0;
+  for (int p = 0; p < 4; ++p) {
+    DepthIO io;
+    io.kin = p == 0 ? ws.zkey : ((p & 1) ? ws.dk0 : ws.dk1);
+    io.vin = p == 0 ? nullptr : ((p & 1) ? ws.dv0 : ws.dv1);
+    io.kout = p == 3 ? nullptr : ((p & 1) ? ws.dk1 : ws.dk0);
+    io.vout = (p & 1) ? ws.dv1 : ws.dv0;
+    depth_upsweep_kernel<<<nb, SB_THREADS, 0, s>>>(bt, ws, io, 8 * p, ghist);
+    depth_scan_kernel<<<ec, 256, 0, s>>>(bt, ghist);
+    depth_downsweep_kernel<<<nb, SB_THREADS, depth_down_smem(), s>>>(bt, ws, io, 8 * p, ghist);
+    launches += 3;
+  }
+  const uint32_t* order = ws.dv1;   // values of the last depth pass
+  place_upsweep_kernel<<<nb, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
+  place_scan_kernel<<<ec, SB_THREADS, 0, s>>>(bt, ws, thist, rp.ntiles);
+  place_downsweep_kernel<<<nb, SB_THREADS, place_down_smem(rp.ntiles), s>>>(bt, ws, order, rp, thist);
+  return launches + 3;
 }
 
 }  // namespace gg
