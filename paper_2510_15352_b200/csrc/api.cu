@@ -77,7 +77,7 @@ struct gg_context {
   DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase;
   DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1;
   DevBuf sorted, ranges, counters, valid_out, perm, groups, blkbase, ghist, thist;
-  DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval;
+  DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval, dconic;
   DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
   // pinned host mirrors
   uint32_t* h_vcnt = nullptr;
@@ -274,7 +274,7 @@ gg_status gg_destroy(gg_context* ctx) {
                    &ctx->blkbase, &ctx->ghist, &ctx->thist,
                    &ctx->sorted, &ctx->ranges, &ctx->counters, &ctx->valid_out,
                    &ctx->dbg_tc, &ctx->dbg_proj, &ctx->dbg_stile, &ctx->dbg_sz, &ctx->dbg_sgid,
-                   &ctx->dbg_neval, &ctx->h_in};
+                   &ctx->dbg_neval, &ctx->dconic, &ctx->h_in};
   for (DevBuf* b : all) dev_free(ctx, *b, s);
   cudaStreamSynchronize(s);
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
@@ -555,6 +555,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     if (!ensure(ctx, ctx->rec0, V * 16, s) || !ensure(ctx, ctx->rec1, V * 16, s) ||
         !ensure(ctx, ctx->rec2, V * 16, s) || !ensure(ctx, ctx->rect, V * 8, s) ||
         !ensure(ctx, ctx->zkey, V * 4, s) || (keep && !ensure(ctx, ctx->gid, V * 4, s)) ||
+        (keep && !ensure(ctx, ctx->dconic, V * 16, s)) ||
         !ensure(ctx, ctx->dk0, V * 4, s) || !ensure(ctx, ctx->dv0, V * 4, s) ||
         !ensure(ctx, ctx->dk1, V * 4, s) || !ensure(ctx, ctx->dv1, V * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: record workspace (%llu records) allocation failed",
@@ -564,6 +565,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
     ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
     ws.gid = keep ? P<uint32_t>(ctx->gid) : nullptr;
+    ws.dconic = keep ? P<float4>(ctx->dconic) : nullptr;
     ws.dk0 = P<uint32_t>(ctx->dk0); ws.dv0 = P<uint32_t>(ctx->dv0);
     ws.dk1 = P<uint32_t>(ctx->dk1); ws.dv1 = P<uint32_t>(ctx->dv1);
     // K1b

@@ -64,16 +64,15 @@ struct ChunkWS {
   // records (global index = rec_base[e] + local)
   const uint64_t* rec_base;  // [Ec]
   const uint64_t* k_base;    // [Ec]
-  float4* rec0;         // (u, v, opacity, z)
-  float4* rec1;         // (conic A, B, C, ext_x)
+  float4* rec0;         // (u, v, log2 opacity, z)
+  float4* rec1;         // (A', B', C', ext_x): conic pre-scaled so -q/2 log2(e) = A'dx^2 + B'dxdy + C'dy^2
   float4* rec2;         // (r, g, b, ext_y)
+  float4* dconic;       // debug only (null unless intermediates are kept): raw conic A, B, C, opacity
   uint2* rect;          // (x0 | x1<<16, y0 | y1<<16)
   uint32_t* zkey;       // f32 bits of z
   uint32_t* gid;        // Gaussian index (debug dumps only; may be null)
   // depth-sort scratch [V]
   uint32_t* dk0; uint32_t* dv0; uint32_t* dk1; uint32_t* dv1;
-  // tile-sort scratch [K]
-  uint32_t* tk0; uint32_t* tv0; uint32_t* tk1; uint32_t* tv1;
   uint32_t* sorted;     // [K] final record-local indices, tile-major
   uint2* ranges;        // [Ec][ntiles] [start,end) relative to k_base[e]
   int nwords, nblk;

@@ -49,12 +49,12 @@ __global__ void debug_records_kernel(uint32_t V, uint64_t rb, const ChunkWS ws, 
     const uint32_t g = ws.gid[r];
     tile_counts[g] = (int32_t)nt;
     if (nt) {
-      const float4 a = ws.rec0[r], b = ws.rec1[r], c = ws.rec2[r];
+      const float4 a = ws.rec0[r], b = ws.dconic[r], c = ws.rec2[r];
       float* d = proj + (size_t)g * 16;
       d[0] = 1.f; d[1] = a.x; d[2] = a.y; d[3] = b.x; d[4] = b.y; d[5] = b.z; d[6] = a.w;
       d[7] = 0.f;   // radius is not stored by the product path
       d[8] = (float)x0; d[9] = (float)x1; d[10] = (float)y0; d[11] = (float)y1;
-      d[12] = c.x; d[13] = c.y; d[14] = c.z; d[15] = a.z;
+      d[12] = c.x; d[13] = c.y; d[14] = c.z; d[15] = b.w;
     }
   }
 }

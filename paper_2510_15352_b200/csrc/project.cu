@@ -390,12 +390,17 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
       ex = sqrtf(qmax * a) * 1.002f + 0.02f;
       ey = sqrtf(qmax * cc) * 1.002f + 0.02f;
     }
-    ws.rec0[r] = make_float4(u, v, o, p.z);
-    ws.rec1[r] = make_float4(cA, cB, cC, ex);
+    // record for the blend (DESIGN.md §4 K6): alpha = min(.99, 2^(A'dx^2 + B'dxdy + C'dy^2 + log2 o))
+    const float kq = -0.72134752044448170f;   // -0.5 log2(e)
+    ws.rec0[r] = make_float4(u, v, log2f(o), p.z);
+    ws.rec1[r] = make_float4(cA * kq, 2.f * cB * kq, cC * kq, ex);
     ws.rec2[r] = make_float4(col[0], col[1], col[2], ey);
     ws.rect[r] = make_uint2(x0 | (x1 << 16), y0 | (y1 << 16));
     ws.zkey[r] = __float_as_uint(p.z);
-    if (ws.gid) ws.gid[r] = (uint32_t)(i0 + l);
+    if (ws.gid) {
+      ws.gid[r] = (uint32_t)(i0 + l);
+      ws.dconic[r] = make_float4(cA, cB, cC, o);
+    }
     if (ntiles) atomicAdd(&sm.kacc[k], ntiles);
   }
   __syncthreads();

@@ -8,15 +8,21 @@
 //     w = alpha T; C += w c; D += w z; A += w; T = T'
 //   rgb = C + T bg (R15); depth = D / A or 0 (R14); alpha = A
 //
+// Arithmetic in the log2 domain: the record carries the conic pre-scaled
+// by -log2(e)/2 and log2(o), so x = A'dx^2 + B'dxdy + C'dy^2 + log2 o is the
+// base-2 log of o exp(-q/2); the cutoff is the compare x < log2(1/255)
+// BEFORE the exponential, and alpha = min(0.99, ex2(x)) (MUFU.EX2) only for
+// Gaussians that can contribute.
+//
 // Decomposition: one CTA of 256 threads per (tile, env), one pixel per
-// thread; warp w covers an 8x4 pixel block.  Records are staged in shared
-// memory 256 at a time (3 x 128-bit loads each, gathered through the
-// tile's sorted index list).  Each record carries the half extents of its
-// alpha >= 1/255 ellipse (computed in K1b with safety margins), so a warp
-// whose 8x4 block lies outside skips it with one uniform branch — this
-// never changes a blend decision, it only avoids evaluating pixels whose
-// alpha is below the cutoff.  Early-out: warp vote (__all_sync) ends a
-// warp's walk; __syncthreads_count ends the tile.
+// thread; warp w covers an 8x4 pixel block.  Records are gathered through
+// the tile's sorted index list into shared memory 256 at a time; the
+// loading thread also computes an 8-bit mask of the warps whose 8x4 block
+// intersects the record's alpha >= 1/255 ellipse box (K1b stores its half
+// extents with safety margins).  Each warp then walks only its own records
+// (ballot over 32-record groups + ffs), so work is spent only where the
+// cutoff can be passed — this never changes a blend decision.  Early-out:
+// warp vote ends a warp's walk; __syncthreads_count ends the tile.
 #include "gg_internal.cuh"
 
 namespace gg {
@@ -33,11 +39,40 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+constexpr float LOG2_CUTOFF = -7.99435343685885793f;   // log2(1/255)
+
+// One pixel-Gaussian step; returns true if the pixel blended it.
+__device__ __forceinline__ void blend_step(const float4 a0, const float4 a1, const float4 a2, float fpx, float fpy,
+                                           float& T, float& Cr, float& Cg, float& Cb, float& Dn, float& Aw,
+                                           bool& done, uint32_t& nc) {
+  const float dx = a0.x - fpx, dy = a0.y - fpy;
+  // x = log2(o) - q log2(e)/2, with q >= 0 enforced as x <= log2(o)
+  float x = fmaf(dx, fmaf(a1.x, dx, a1.y * dy), a1.z * dy * dy);
+  x = fminf(x, 0.f) + a0.z;
+  if (x >= LOG2_CUTOFF) {
+    const float al = fminf(0.99f, ex2_approx(x));
+    const float w = al * T;
+    const float Tn = T - w;
+    if (Tn < 1e-4f) {
+      done = true;
+    } else {
+      Cr = fmaf(w, a2.x, Cr);
+      Cg = fmaf(w, a2.y, Cg);
+      Cb = fmaf(w, a2.z, Cb);
+      Dn = fmaf(w, a0.w, Dn);
+      Aw += w;
+      T = Tn;
+      ++nc;
+    }
+  }
+}
+
 template <bool COUNTERS>
 __global__ void __launch_bounds__(TILE_PX)
 raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
               float* __restrict__ depth, float* __restrict__ alpha_out, CounterOut co) {
   __shared__ float4 s0[TILE_PX], s1[TILE_PX], s2[TILE_PX];
+  __shared__ uint8_t smask[TILE_PX];
   const int eloc = blockIdx.y;
   const int tile = blockIdx.x;
   const int e = envs[e0 + eloc].out_index;   // caller's env index
@@ -48,8 +83,8 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
   const int py = ty * TILE + by * 4 + (lane >> 3);
   const bool inside = px < rp.W && py < rp.H;
   const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
-  const float wx0 = (float)(tx * TILE + bx * 8) + 0.5f, wx1 = wx0 + 7.f;
-  const float wy0 = (float)(ty * TILE + by * 4) + 0.5f, wy1 = wy0 + 3.f;
+  // pixel-centre extents of the tile's warp blocks (columns: 2 x 8 px, rows: 4 x 4 px)
+  const float tx0 = (float)(tx * TILE) + 0.5f, ty0 = (float)(ty * TILE) + 0.5f;
 
   const uint2 rg = ws.ranges[(size_t)eloc * rp.ntiles + tile];
   const uint64_t kb = ws.k_base[eloc];
@@ -59,48 +94,54 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
   float T = 1.f, Cr = 0.f, Cg = 0.f, Cb = 0.f, Dn = 0.f, Aw = 0.f;
   bool done = !inside;
   uint32_t ne = 0, nc = 0;
-  const float kExp = -0.72134752044448170f;   // -0.5 * log2(e)
 
   for (uint32_t b = rg.x; b < rg.y; b += TILE_PX) {
     const uint32_t n = min((uint32_t)TILE_PX, rg.y - b);
     __syncthreads();
     if (tid < n) {
       const uint64_t r = rb + __ldg(&list[b + tid]);
-      s0[tid] = __ldg(&ws.rec0[r]);
-      s1[tid] = __ldg(&ws.rec1[r]);
-      s2[tid] = __ldg(&ws.rec2[r]);
+      const float4 a0 = __ldg(&ws.rec0[r]);
+      const float4 a1 = __ldg(&ws.rec1[r]);
+      const float4 a2 = __ldg(&ws.rec2[r]);
+      s0[tid] = a0;
+      s1[tid] = a1;
+      s2[tid] = a2;
+      uint32_t m = 0;
+      if (a1.w >= 0.f) {
+        const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
+        uint32_t cm = 0, rm = 0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          if (xh >= tx0 + 8.f * c && xl <= tx0 + 8.f * c + 7.f) cm |= 1u << c;
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4)
+          if (yh >= ty0 + 4.f * r4 && yl <= ty0 + 4.f * r4 + 3.f) rm |= 1u << r4;
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4)
+          if ((rm >> r4) & 1u) m |= cm << (2 * r4);
+      }
+      smask[tid] = (uint8_t)m;
     }
     __syncthreads();
-    if (!__all_sync(0xffffffffu, done)) {
-      for (uint32_t j = 0; j < n; ++j) {
-        const float4 a0 = s0[j];
-        const float4 a1 = s1[j];
-        const float4 a2 = s2[j];
-        if (COUNTERS && !done) ++ne;
-        // warp-uniform: is this warp's 8x4 block outside the alpha >= 1/255 box?
-        if (a1.w < 0.f || a0.x + a1.w < wx0 || a0.x - a1.w > wx1 || a0.y + a2.w < wy0 ||
-            a0.y - a2.w > wy1)
-          continue;
-        if (!done) {
-          const float dx = a0.x - fpx, dy = a0.y - fpy;
-          float q = a1.x * dx * dx + 2.f * a1.y * dx * dy + a1.z * dy * dy;
-          q = fmaxf(q, 0.f);
-          const float al = fminf(0.99f, a0.z * ex2_approx(kExp * q));
-          if (al >= (1.f / 255.f)) {
-            const float Tn = T * (1.f - al);
-            if (Tn < 1e-4f) {
-              done = true;
-            } else {
-              const float w = al * T;
-              Cr += w * a2.x; Cg += w * a2.y; Cb += w * a2.z;
-              Dn += w * a0.w;
-              Aw += w;
-              T = Tn;
-              if (COUNTERS) ++nc;
-            }
-          }
+    if (COUNTERS) {
+      // reference walk: every record in order (counts n_eval exactly as defined)
+      if (!__all_sync(0xffffffffu, done)) {
+        for (uint32_t j = 0; j < n; ++j) {
+          if (!done) ++ne;
+          if (!((smask[j] >> warp) & 1u)) continue;
+          if (!done) blend_step(s0[j], s1[j], s2[j], fpx, fpy, T, Cr, Cg, Cb, Dn, Aw, done, nc);
+          if ((j & 7) == 7 && __all_sync(0xffffffffu, done)) break;
         }
-        if ((j & 7) == 7 && __all_sync(0xffffffffu, done)) break;
+      }
+    } else {
+      for (uint32_t g = 0; g < n && !__all_sync(0xffffffffu, done); g += 32) {
+        const uint32_t j = g + lane;
+        uint32_t mine = __ballot_sync(0xffffffffu, j < n && ((smask[j < n ? j : 0] >> warp) & 1u));
+        while (mine) {
+          const uint32_t jj = g + __ffs(mine) - 1;
+          mine &= mine - 1;
+          if (!done) blend_step(s0[jj], s1[jj], s2[jj], fpx, fpy, T, Cr, Cg, Cb, Dn, Aw, done, nc);
+        }
       }
     }
     if (__syncthreads_count(done) == TILE_PX) break;
@@ -108,7 +149,7 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
 
   if (inside) {
     const size_t p = ((size_t)e * rp.H + py) * rp.W + px;
-    const float r = Cr + T * rp.bg[0], g = Cg + T * rp.bg[1], bl = Cb + T * rp.bg[2];
+    const float r = fmaf(T, rp.bg[0], Cr), g = fmaf(T, rp.bg[1], Cg), bl = fmaf(T, rp.bg[2], Cb);
     if (rgb) {
       if (rp.rgb_format == 0) {
         uint8_t* o = reinterpret_cast<uint8_t*>(rgb) + p * 3;
