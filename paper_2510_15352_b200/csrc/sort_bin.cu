@@ -301,20 +301,21 @@ __global__ void __launch_bounds__(SB_THREADS) place_scan_kernel(BlockTable bt, C
   }
 }
 
-struct PlaceSmem {
-  RankSmem rs;
-  uint32_t sk[SB_BLK];
-  uint32_t sv[SB_BLK];
-  uint32_t tcur[1];     // [ntiles] cursors, then [ntiles] run starts (dynamic tail)
-};
-
+// Placement downsweep.  Warp w < S owns a contiguous segment of the block's
+// records (in depth order).  Phase 1: per-warp tile histograms (u16 pairs
+// packed in u32 words).  Phase 2: per tile, prefix over warps starting at
+// the block's offset from place_scan -> per-warp cursors.  Phase 3: each
+// warp walks its records in order, 32 (record, tile) pairs per step, ranks
+// equal tiles among the lanes with a ballot multisplit and writes each
+// record index at its final slot; no block barrier inside the walk.
 __global__ void __launch_bounds__(SB_THREADS)
-place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderParams rp, const uint32_t* thist) {
+place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderParams rp, const uint32_t* thist,
+                       int S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PlaceSmem& sm = *reinterpret_cast<PlaceSmem*>(smem_raw);
   const int nt = rp.ntiles;
-  uint32_t* tcur = sm.tcur;
-  uint32_t* trun = sm.tcur + nt;
+  const int nw2 = (nt + 1) >> 1;                     // packed words per warp
+  uint32_t* gb = reinterpret_cast<uint32_t*>(smem_raw);   // [nt] block offsets (rel. to k_base)
+  uint32_t* wh = gb + nt;                                  // [S][nw2] packed u16 counters / cursors
   const uint32_t b = blockIdx.x;
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SB_BLK;
@@ -322,76 +323,103 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
   const uint64_t rb = ws.rec_base[e];
   uint32_t* out = ws.sorted + ws.k_base[e];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < SB_WARPS * 256; i += SB_THREADS) (&sm.rs.wcnt[0][0])[i] = 0u;
-  for (int i = tid; i < nt; i += SB_THREADS) tcur[i] = thist[(size_t)b * nt + i];
-  int tb = 0;
-  while ((1 << tb) < nt) ++tb;
-  const int lo_bits = tb < 7 ? tb : 7;
-  const int hi_bits = tb - lo_bits;
+  for (int i = tid; i < nt; i += SB_THREADS) gb[i] = thist[(size_t)b * nt + i];
+  for (int i = tid; i < S * nw2; i += SB_THREADS) wh[i] = 0u;
+  // segment of warp w: records [w*Ls, (w+1)*Ls) of the block, Ls multiple of 32
+  const uint32_t Ls = ((nrec + S * 32 - 1) / (S * 32)) * 32;
+  const uint32_t s0 = warp < S ? min(nrec, warp * Ls) : nrec;
+  const uint32_t s1 = warp < S ? min(nrec, s0 + Ls) : nrec;
   __syncthreads();
-  // records in rounds of 1024 (one per thread), pairs flattened in record order
-  for (uint32_t r0 = 0; r0 < nrec; r0 += SB_THREADS) {
-    const uint32_t j = r0 + tid;
+  // phase 1: per-warp tile histogram over the warp's segment
+  if (warp < S) {
+    uint32_t* h = wh + (size_t)warp * nw2;
+    for (uint32_t j = s0 + lane; j < s1; j += 32) {
+      const uint2 r = ws.rect[rb + order[rb + j0 + j]];
+      const uint32_t x0 = r.x & 0xffffu, x1 = r.x >> 16, y0 = r.y & 0xffffu, y1 = r.y >> 16;
+      for (uint32_t ty = y0; ty < y1; ++ty)
+        for (uint32_t tx = x0; tx < x1; ++tx) {
+          const uint32_t t = ty * rp.TX + tx;
+          atomicAdd(&h[t >> 1], 1u << (16 * (t & 1)));
+        }
+    }
+  }
+  __syncthreads();
+  // phase 2: per-warp cursors relative to the block's run of each tile
+  for (int q = tid; q < nw2; q += SB_THREADS) {
+    uint32_t run0 = 0, run1 = 0;
+    for (int w = 0; w < S; ++w) {
+      const uint32_t c = wh[(size_t)w * nw2 + q];
+      wh[(size_t)w * nw2 + q] = run0 | (run1 << 16);
+      run0 += c & 0xffffu;
+      run1 += c >> 16;
+    }
+  }
+  __syncthreads();
+  // phase 3: ordered walk, 32 records per step, their pairs 32 at a time
+  if (warp >= S) return;
+  uint32_t* h = wh + (size_t)warp * nw2;
+  int tile_bits = 0;
+  while ((1 << tile_bits) < nt) ++tile_bits;
+  const uint32_t lt = lanemask_lt();
+  for (uint32_t base = s0; base < s1; base += 32) {
+    const uint32_t j = base + lane;
     uint32_t idx = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
-    if (j < nrec) {
+    if (j < s1) {
       idx = order[rb + j0 + j];
-      unpack_rect(ws.rect[rb + idx], x0, x1, y0, y1);
+      const uint2 r = ws.rect[rb + idx];
+      x0 = r.x & 0xffffu; x1 = r.x >> 16; y0 = r.y & 0xffffu; y1 = r.y >> 16;
     }
     const uint32_t w = x1 - x0;
     const uint32_t np = w * (y1 - y0);
-    uint32_t total;
-    const uint32_t excl = block_scan(np, sm.rs.wsum, &total);
-    for (uint32_t w0 = 0; w0 < total; w0 += SB_BLK) {
-      const uint32_t n = min((uint32_t)SB_BLK, total - w0);
-      const uint32_t qa = excl >= w0 ? 0u : w0 - excl;
-      const uint32_t qb = min(np, w0 + SB_BLK > excl ? w0 + SB_BLK - excl : 0u);
-      for (uint32_t q = qa; q < qb; ++q) {
-        const uint32_t ty = y0 + q / w, tx = x0 + q % w;
-        sm.sk[excl + q - w0] = ty * rp.TX + tx;
-        sm.sv[excl + q - w0] = idx;
-      }
-      __syncthreads();
-      for (int pass = 0; pass < (hi_bits > 0 ? 2 : 1); ++pass) {
-        const int sh = pass == 0 ? 0 : lo_bits;
-        const int bits = pass == 0 ? lo_bits : hi_bits;
-        uint32_t t[SB_IPT], v[SB_IPT], d[SB_IPT], lp[SB_IPT];
+    uint32_t incl = np;
 #pragma unroll
-        for (int jj = 0; jj < SB_IPT; ++jj) {
-          const uint32_t i = warp * 32 * SB_IPT + jj * 32 + lane;
-          t[jj] = i < n ? sm.sk[i] : 0u;
-          v[jj] = i < n ? sm.sv[i] : 0u;
-          d[jj] = (t[jj] >> sh) & ((1u << bits) - 1u);
-        }
-        block_rank(d, n, bits, lp, sm.rs);
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    for (uint32_t f0 = 0; f0 < tot; f0 += 32) {
+      const uint32_t f = f0 + lane;
+      const bool ok = f < tot;
+      int src = 0;   // first lane whose inclusive pair count exceeds f
 #pragma unroll
-        for (int jj = 0; jj < SB_IPT; ++jj) {
-          const uint32_t i = warp * 32 * SB_IPT + jj * 32 + lane;
-          if (i < n) { sm.sk[lp[jj]] = t[jj]; sm.sv[lp[jj]] = v[jj]; }
-        }
-        __syncthreads();
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, src + step - 1);
+        if (v <= f) src += step;
       }
-      for (uint32_t q = tid; q < n; q += SB_THREADS) {
-        const uint32_t tt = sm.sk[q];
-        if (q == 0 || sm.sk[q - 1] != tt) trun[tt] = q;
+      const uint32_t o_incl = __shfl_sync(0xffffffffu, incl, src);
+      const uint32_t o_np = __shfl_sync(0xffffffffu, np, src);
+      const uint32_t o_w = __shfl_sync(0xffffffffu, w, src);
+      const uint32_t o_x0 = __shfl_sync(0xffffffffu, x0, src);
+      const uint32_t o_y0 = __shfl_sync(0xffffffffu, y0, src);
+      const uint32_t o_idx = __shfl_sync(0xffffffffu, idx, src);
+      uint32_t t = 0;
+      if (ok) {
+        const uint32_t qq = f - (o_incl - o_np);
+        t = (o_y0 + qq / o_w) * rp.TX + o_x0 + qq % o_w;
       }
-      __syncthreads();
-      for (uint32_t q = tid; q < n; q += SB_THREADS) {
-        const uint32_t tt = sm.sk[q];
-        out[tcur[tt] + (q - trun[tt])] = sm.sv[q];
-      }
-      __syncthreads();
-      for (uint32_t q = tid; q < n; q += SB_THREADS) {
-        const uint32_t tt = sm.sk[q];
-        if (q == n - 1 || sm.sk[q + 1] != tt) tcur[tt] += q - trun[tt] + 1;
-      }
-      __syncthreads();
+      const uint32_t active = __ballot_sync(0xffffffffu, ok);
+      const uint32_t peers = peers_of(t, tile_bits, active);
+      const uint32_t before = ok ? (h[t >> 1] >> (16 * (t & 1))) & 0xffffu : 0u;
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) atomicAdd(&h[t >> 1], __popc(peers) << (16 * (t & 1)));
+      __syncwarp();
+      if (ok) out[gb[t] + before + __popc(peers & lt)] = o_idx;
     }
   }
 }
 
 // ---- host side -------------------------------------------------------------
 size_t depth_down_smem() { return sizeof(DownSmem); }
-size_t place_down_smem(int ntiles) { return offsetof(PlaceSmem, tcur) + (size_t)ntiles * 8; }
+// placement segments per block: as many warps as the packed counter table allows
+int place_segments(int ntiles) {
+  const size_t budget = 200 * 1024 - (size_t)ntiles * 4;
+  const int s = (int)(budget / (((size_t)ntiles + 1) / 2 * 4));
+  return s < 1 ? 1 : (s > SB_WARPS ? SB_WARPS : s);
+}
+size_t place_down_smem(int ntiles) {
+  return (size_t)ntiles * 4 + (size_t)place_segments(ntiles) * ((ntiles + 1) / 2) * 4;
+}
 
 cudaError_t sort_bin_init() {
   cudaError_t e = cudaFuncSetAttribute(depth_downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -430,7 +458,8 @@ int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, const RenderP
   const uint32_t* order = ws.dv1;   // values of the last depth pass
   place_upsweep_kernel<<<nb, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
   place_scan_kernel<<<ec, SB_THREADS, 0, s>>>(bt, ws, thist, rp.ntiles);
-  place_downsweep_kernel<<<nb, SB_THREADS, place_down_smem(rp.ntiles), s>>>(bt, ws, order, rp, thist);
+  place_downsweep_kernel<<<nb, SB_THREADS, place_down_smem(rp.ntiles), s>>>(bt, ws, order, rp, thist,
+                                                                            place_segments(rp.ntiles));
   return launches + 3;
 }
 
