@@ -360,8 +360,8 @@ void* or_render_env(const void* scene, const float* view, const float* intr, int
                     const OrOpts* opt) {
   const Scene& S = *(const Scene*)scene;
   if (W <= 0 || H <= 0) return nullptr;
-  const int dr = opt->sh_degree < 0 ? S.d : opt->sh_degree;
-  if (dr > S.d) return nullptr;
+  // reading R29: opts.sh_degree caps the scene's degree
+  const int dr = opt->sh_degree < 0 ? S.d : std::min<int>(opt->sh_degree, S.d);
   Cam cam;
   for (int i = 0; i < 3; ++i) {
     for (int j = 0; j < 3; ++j) { cam.Rf[i][j] = view[i * 4 + j]; cam.R[i][j] = view[i * 4 + j]; }
