@@ -19,11 +19,12 @@
 // the tile's sorted index list into shared memory 256 at a time; the
 // loading thread also computes an 8-bit mask of the warps whose 8x4 block
 // intersects the record's alpha >= 1/255 ellipse box (K1b stores its half
-// extents with safety margins).  Each warp then walks only its own records
-// (ballot over 32-record groups + ffs), so work is spent only where the
-// cutoff can be passed — this never changes a blend decision.  Early-out:
+// extents with safety margins).  Each warp compacts the records whose bit it
+// holds into a per-warp list (ballot + popc, order preserved) and walks only
+// that list, so work is spent only where the cutoff can be passed — this never changes a blend decision.  Early-out:
 // warp vote ends a warp's walk; __syncthreads_count ends the tile.
 #include "gg_internal.cuh"
+#include "f32x2.cuh"
 
 namespace gg {
 
@@ -41,14 +42,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 constexpr float LOG2_CUTOFF = -7.99435343685885793f;   // log2(1/255)
 
-// One pixel-Gaussian step; returns true if the pixel blended it.
+// One pixel-Gaussian step (R12-R15 with the R30 log2-domain cutoff).
 __device__ __forceinline__ void blend_step(const float4 a0, const float4 a1, const float4 a2, float fpx, float fpy,
                                            float& T, float& Cr, float& Cg, float& Cb, float& Dn, float& Aw,
                                            bool& done, uint32_t& nc) {
   const float dx = a0.x - fpx, dy = a0.y - fpy;
-  // x = log2(o) - q log2(e)/2, with q >= 0 enforced as x <= log2(o)
-  float x = fmaf(dx, fmaf(a1.x, dx, a1.y * dy), a1.z * dy * dy);
-  x = fminf(x, 0.f) + a0.z;
+  // x = log2(o) - q log2(e)/2; q >= 0 enforced as x <= log2(o)
+  float x = fmaf(dx, fmaf(a1.x, dx, a1.y * dy), fmaf(a1.z * dy, dy, a0.z));
+  x = fminf(x, a0.z);
   if (x >= LOG2_CUTOFF) {
     const float al = fminf(0.99f, ex2_approx(x));
     const float w = al * T;
@@ -71,8 +72,9 @@ template <bool COUNTERS>
 __global__ void __launch_bounds__(TILE_PX)
 raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
               float* __restrict__ depth, float* __restrict__ alpha_out, CounterOut co) {
-  __shared__ float4 s0[TILE_PX], s1[TILE_PX], s2[TILE_PX];
+  __shared__ float4 srec[TILE_PX * 3];           // record j at srec[3j .. 3j+2]
   __shared__ uint8_t smask[TILE_PX];
+  __shared__ uint8_t wlist[TILE_PX / 32][TILE_PX];   // per-warp relevant records
   const int eloc = blockIdx.y;
   const int tile = blockIdx.x;
   const int e = envs[e0 + eloc].out_index;   // caller's env index
@@ -103,9 +105,9 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
       const float4 a0 = __ldg(&ws.rec0[r]);
       const float4 a1 = __ldg(&ws.rec1[r]);
       const float4 a2 = __ldg(&ws.rec2[r]);
-      s0[tid] = a0;
-      s1[tid] = a1;
-      s2[tid] = a2;
+      srec[3 * tid] = a0;
+      srec[3 * tid + 1] = a1;
+      srec[3 * tid + 2] = a2;
       uint32_t m = 0;
       if (a1.w >= 0.f) {
         const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
@@ -129,19 +131,26 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
         for (uint32_t j = 0; j < n; ++j) {
           if (!done) ++ne;
           if (!((smask[j] >> warp) & 1u)) continue;
-          if (!done) blend_step(s0[j], s1[j], s2[j], fpx, fpy, T, Cr, Cg, Cb, Dn, Aw, done, nc);
+          if (!done) blend_step(srec[3 * j], srec[3 * j + 1], srec[3 * j + 2], fpx, fpy, T, Cr, Cg, Cb, Dn, Aw, done, nc);
           if ((j & 7) == 7 && __all_sync(0xffffffffu, done)) break;
         }
       }
-    } else {
-      for (uint32_t g = 0; g < n && !__all_sync(0xffffffffu, done); g += 32) {
+    } else if (!__all_sync(0xffffffffu, done)) {
+      // compact this warp's relevant records (order preserved)
+      uint32_t cnt = 0;
+      const uint32_t lt = (1u << lane) - 1u;
+      for (uint32_t g = 0; g < n; g += 32) {
         const uint32_t j = g + lane;
-        uint32_t mine = __ballot_sync(0xffffffffu, j < n && ((smask[j < n ? j : 0] >> warp) & 1u));
-        while (mine) {
-          const uint32_t jj = g + __ffs(mine) - 1;
-          mine &= mine - 1;
-          if (!done) blend_step(s0[jj], s1[jj], s2[jj], fpx, fpy, T, Cr, Cg, Cb, Dn, Aw, done, nc);
-        }
+        const bool mine = j < n && ((smask[j] >> warp) & 1u);
+        const uint32_t m = __ballot_sync(0xffffffffu, mine);
+        if (mine) wlist[warp][cnt + __popc(m & lt)] = (uint8_t)j;
+        cnt += __popc(m);
+      }
+      __syncwarp();
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const uint32_t j = wlist[warp][i];
+        if (!done) blend_step(srec[3 * j], srec[3 * j + 1], srec[3 * j + 2], fpx, fpy, T, Cr, Cg, Cb, Dn, Aw, done, nc);
+        if ((i & 15) == 15 && __all_sync(0xffffffffu, done)) break;
       }
     }
     if (__syncthreads_count(done) == TILE_PX) break;
@@ -183,6 +192,147 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
   }
 }
 
+// ---------------------------------------------------------------------------
+// Timed-path variant: 2 pixels per thread with packed f32x2 arithmetic
+// (FFMA2/FADD2/FMUL2).  128 threads per tile; warp w covers an 8x8 block,
+// lane (lx, ly) owns pixels (lx, ly) and (lx, ly + 4) of it.  The per-pixel
+// operation sequence is identical to blend_step (same fma order), so the
+// images are bit-identical to the 256-thread reference walk.
+constexpr int R2_THREADS = 128;
+
+__global__ void __launch_bounds__(R2_THREADS, 8)
+raster2_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
+               float* __restrict__ depth, float* __restrict__ alpha_out) {
+  constexpr int BATCH = 256;
+  __shared__ ulonglong2 srec[BATCH * 5];        // (u,u|v,v) (A',A'|B',B') (C',C'|L,L) (r,r|g,g) (b,b|z,z)
+  __shared__ uint8_t smask[BATCH];
+  __shared__ uint8_t wlist[R2_THREADS / 32][BATCH];
+  const int eloc = blockIdx.y;
+  const int tile = blockIdx.x;
+  const int e = envs[e0 + eloc].out_index;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tx = tile % rp.TX, ty = tile / rp.TX;
+  const int bx = warp & 1, by = warp >> 1;
+  const int px = tx * TILE + bx * 8 + (lane & 7);
+  const int py0 = ty * TILE + by * 8 + (lane >> 3), py1 = py0 + 4;
+  const bool in0 = px < rp.W && py0 < rp.H, in1 = px < rp.W && py1 < rp.H;
+  const float fpx = (float)px + 0.5f;
+  const f2 FPX = pk(fpx, fpx), FPY = pk((float)py0 + 0.5f, (float)py1 + 0.5f);
+  const float tx0 = (float)(tx * TILE) + 0.5f, ty0 = (float)(ty * TILE) + 0.5f;
+
+  const uint2 rg = ws.ranges[(size_t)eloc * rp.ntiles + tile];
+  const uint64_t rb = ws.rec_base[eloc];
+  const uint32_t* __restrict__ list = ws.sorted + ws.k_base[eloc];
+
+  f2 T = pk(1.f, 1.f), Cr = pk(0.f, 0.f), Cg = Cr, Cb = Cr, Dn = Cr, Aw = Cr;
+  bool done0 = !in0, done1 = !in1;
+
+  for (uint32_t b = rg.x; b < rg.y; b += BATCH) {
+    const uint32_t n = min((uint32_t)BATCH, rg.y - b);
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += R2_THREADS) {
+      const uint64_t r = rb + __ldg(&list[b + i]);
+      const float4 a0 = __ldg(&ws.rec0[r]);
+      const float4 a1 = __ldg(&ws.rec1[r]);
+      const float4 a2 = __ldg(&ws.rec2[r]);
+      float4* d = reinterpret_cast<float4*>(&srec[5 * i]);
+      d[0] = make_float4(a0.x, a0.x, a0.y, a0.y);
+      d[1] = make_float4(a1.x, a1.x, a1.y, a1.y);
+      d[2] = make_float4(a1.z, a1.z, a0.z, a0.z);
+      d[3] = make_float4(a2.x, a2.x, a2.y, a2.y);
+      d[4] = make_float4(a2.z, a2.z, a0.w, a0.w);
+      uint32_t m = 0;
+      if (a1.w >= 0.f) {
+        const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const float cx0 = tx0 + 8.f * (w & 1), cy0 = ty0 + 8.f * (w >> 1);
+          if (xh >= cx0 && xl <= cx0 + 7.f && yh >= cy0 && yl <= cy0 + 7.f) m |= 1u << w;
+        }
+      }
+      smask[i] = (uint8_t)m;
+    }
+    __syncthreads();
+    if (!__all_sync(0xffffffffu, done0 && done1)) {
+      uint32_t cnt = 0;
+      const uint32_t lt = (1u << lane) - 1u;
+      for (uint32_t g = 0; g < n; g += 32) {
+        const uint32_t j = g + lane;
+        const bool mine = j < n && ((smask[j] >> warp) & 1u);
+        const uint32_t m = __ballot_sync(0xffffffffu, mine);
+        if (mine) wlist[warp][cnt + __popc(m & lt)] = (uint8_t)j;
+        cnt += __popc(m);
+      }
+      __syncwarp();
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const ulonglong2* q = &srec[5 * wlist[warp][i]];
+        const ulonglong2 q0 = q[0], q1 = q[1], q2 = q[2];
+        const f2 dx = sub2(f2{q0.x}, FPX), dy = sub2(f2{q0.y}, FPY);
+        const f2 t = fma2(f2{q1.x}, dx, mul2(f2{q1.y}, dy));
+        const f2 s = fma2(mul2(f2{q2.x}, dy), dy, f2{q2.y});
+        float x0, x1, L, Ldup;
+        upk(fma2(dx, t, s), x0, x1);
+        upk(f2{q2.y}, L, Ldup);
+        x0 = fminf(x0, L);
+        x1 = fminf(x1, L);
+        const bool p0 = !done0 && x0 >= LOG2_CUTOFF;
+        const bool p1 = !done1 && x1 >= LOG2_CUTOFF;
+        if (p0 || p1) {
+          const float a0 = p0 ? fminf(0.99f, ex2_approx(x0)) : 0.f;
+          const float a1 = p1 ? fminf(0.99f, ex2_approx(x1)) : 0.f;
+          f2 W = mul2(pk(a0, a1), T);
+          f2 TN = sub2(T, W);
+          float tn0, tn1;
+          upk(TN, tn0, tn1);
+          const bool s0 = p0 && tn0 < 1e-4f, s1 = p1 && tn1 < 1e-4f;
+          if (s0 || s1) {   // stopping pixel: not blended, transmittance kept
+            float w0, w1, t0, t1;
+            upk(W, w0, w1);
+            upk(T, t0, t1);
+            done0 |= s0;
+            done1 |= s1;
+            W = pk(s0 ? 0.f : w0, s1 ? 0.f : w1);
+            TN = pk(s0 ? t0 : tn0, s1 ? t1 : tn1);
+          }
+          const ulonglong2 q3 = q[3], q4 = q[4];
+          Cr = fma2(W, f2{q3.x}, Cr);
+          Cg = fma2(W, f2{q3.y}, Cg);
+          Cb = fma2(W, f2{q4.x}, Cb);
+          Dn = fma2(W, f2{q4.y}, Dn);
+          Aw = add2(Aw, W);
+          T = TN;
+        }
+        if ((i & 15) == 15 && __all_sync(0xffffffffu, done0 && done1)) break;
+      }
+    }
+    if (__syncthreads_count(done0 && done1) == R2_THREADS) break;
+  }
+
+  float t[2], cr[2], cg[2], cb[2], dn[2], aw[2];
+  upk(T, t[0], t[1]); upk(Cr, cr[0], cr[1]); upk(Cg, cg[0], cg[1]); upk(Cb, cb[0], cb[1]);
+  upk(Dn, dn[0], dn[1]); upk(Aw, aw[0], aw[1]);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (!(k == 0 ? in0 : in1)) continue;
+    const int py = k == 0 ? py0 : py1;
+    const size_t p = ((size_t)e * rp.H + py) * rp.W + px;
+    const float r = fmaf(t[k], rp.bg[0], cr[k]), g = fmaf(t[k], rp.bg[1], cg[k]), bl = fmaf(t[k], rp.bg[2], cb[k]);
+    if (rgb) {
+      if (rp.rgb_format == 0) {
+        uint8_t* o = reinterpret_cast<uint8_t*>(rgb) + p * 3;
+        o[0] = (uint8_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 255.f);
+        o[1] = (uint8_t)__float2uint_rn(fminf(fmaxf(g, 0.f), 1.f) * 255.f);
+        o[2] = (uint8_t)__float2uint_rn(fminf(fmaxf(bl, 0.f), 1.f) * 255.f);
+      } else {
+        float* o = reinterpret_cast<float*>(rgb) + p * 3;
+        o[0] = r; o[1] = g; o[2] = bl;
+      }
+    }
+    if (depth) depth[p] = aw[k] > 0.f ? dn[k] / aw[k] : 0.f;
+    if (alpha_out) alpha_out[p] = aw[k];
+  }
+}
+
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s) {
@@ -191,7 +341,7 @@ void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp,
   if (counters)
     raster_kernel<true><<<grid, TILE_PX, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha, co);
   else
-    raster_kernel<false><<<grid, TILE_PX, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha, co);
+    raster2_kernel<<<grid, R2_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
 }
 
 }  // namespace gg

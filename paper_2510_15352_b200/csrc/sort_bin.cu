@@ -395,11 +395,12 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
       const uint32_t o_idx = __shfl_sync(0xffffffffu, idx, src);
       uint32_t t = 0;
       if (ok) {
+        // qq / o_w for small integers via the f32 reciprocal (exact: qq < 2^20, o_w < 2^16)
         const uint32_t qq = f - (o_incl - o_np);
-        t = (o_y0 + qq / o_w) * rp.TX + o_x0 + qq % o_w;
+        const uint32_t row = (uint32_t)(((float)qq + 0.5f) * __frcp_rn((float)o_w));
+        t = (o_y0 + row) * rp.TX + o_x0 + (qq - row * o_w);
       }
-      const uint32_t active = __ballot_sync(0xffffffffu, ok);
-      const uint32_t peers = peers_of(t, tile_bits, active);
+      const uint32_t peers = peers_of(t, tile_bits, __ballot_sync(0xffffffffu, ok));
       const uint32_t before = ok ? (h[t >> 1] >> (16 * (t & 1))) & 0xffffu : 0u;
       __syncwarp();
       if (ok && lane == __ffs(peers) - 1) atomicAdd(&h[t >> 1], __popc(peers) << (16 * (t & 1)));

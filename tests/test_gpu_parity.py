@@ -156,6 +156,10 @@ def test_determinism_batch_and_rgb_only(gg, R):
     r3 = render(gg, R, ids, cams)
     for x, y in zip(r1, r3):
         assert np.array_equal(x, y)
+    # the counters walk (256-thread reference kernel) gives bit-identical images
+    r4 = render(gg, R, ids, cams, flags=gg.GG_COUNTERS)
+    for x, y in zip(r1, r4):
+        assert np.array_equal(x, y)
 
 
 def test_multi_scene_random_binding(gg, R):
