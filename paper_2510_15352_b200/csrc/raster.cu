@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(R2_THREADS, 8)
 raster2_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
                float* __restrict__ depth, float* __restrict__ alpha_out) {
   constexpr int BATCH = 256;
-  __shared__ ulonglong2 srec[BATCH * 5];        // (u,u|v,v) (A',A'|B',B') (C',C'|L,L) (r,r|g,g) (b,b|z,z)
+  __shared__ float4 srec[BATCH * 3];            // rec0 (u,v,L,z), rec1 (A',B',C',ex), rec2 (r,g,b,ey)
   __shared__ uint8_t smask[BATCH];
   __shared__ uint8_t wlist[R2_THREADS / 32][BATCH];
   const int eloc = blockIdx.y;
@@ -235,12 +235,9 @@ raster2_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, Chunk
       const float4 a0 = __ldg(&ws.rec0[r]);
       const float4 a1 = __ldg(&ws.rec1[r]);
       const float4 a2 = __ldg(&ws.rec2[r]);
-      float4* d = reinterpret_cast<float4*>(&srec[5 * i]);
-      d[0] = make_float4(a0.x, a0.x, a0.y, a0.y);
-      d[1] = make_float4(a1.x, a1.x, a1.y, a1.y);
-      d[2] = make_float4(a1.z, a1.z, a0.z, a0.z);
-      d[3] = make_float4(a2.x, a2.x, a2.y, a2.y);
-      d[4] = make_float4(a2.z, a2.z, a0.w, a0.w);
+      srec[3 * i] = a0;
+      srec[3 * i + 1] = a1;
+      srec[3 * i + 2] = a2;
       uint32_t m = 0;
       if (a1.w >= 0.f) {
         const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
@@ -265,14 +262,15 @@ raster2_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, Chunk
       }
       __syncwarp();
       for (uint32_t i = 0; i < cnt; ++i) {
-        const ulonglong2* q = &srec[5 * wlist[warp][i]];
-        const ulonglong2 q0 = q[0], q1 = q[1], q2 = q[2];
-        const f2 dx = sub2(f2{q0.x}, FPX), dy = sub2(f2{q0.y}, FPY);
-        const f2 t = fma2(f2{q1.x}, dx, mul2(f2{q1.y}, dy));
-        const f2 s = fma2(mul2(f2{q2.x}, dy), dy, f2{q2.y});
-        float x0, x1, L, Ldup;
+        // scalar record fields broadcast to both lanes (FFMA2 .F32 operands)
+        const float4* q = &srec[3 * wlist[warp][i]];
+        const float4 r0 = q[0], r1 = q[1];
+        const float L = r0.z;
+        const f2 dx = sub2(pk(r0.x, r0.x), FPX), dy = sub2(pk(r0.y, r0.y), FPY);
+        const f2 t = fma2(pk(r1.x, r1.x), dx, mul2(pk(r1.y, r1.y), dy));
+        const f2 s = fma2(mul2(pk(r1.z, r1.z), dy), dy, pk(L, L));
+        float x0, x1;
         upk(fma2(dx, t, s), x0, x1);
-        upk(f2{q2.y}, L, Ldup);
         x0 = fminf(x0, L);
         x1 = fminf(x1, L);
         const bool p0 = !done0 && x0 >= LOG2_CUTOFF;
@@ -294,11 +292,11 @@ raster2_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, Chunk
             W = pk(s0 ? 0.f : w0, s1 ? 0.f : w1);
             TN = pk(s0 ? t0 : tn0, s1 ? t1 : tn1);
           }
-          const ulonglong2 q3 = q[3], q4 = q[4];
-          Cr = fma2(W, f2{q3.x}, Cr);
-          Cg = fma2(W, f2{q3.y}, Cg);
-          Cb = fma2(W, f2{q4.x}, Cb);
-          Dn = fma2(W, f2{q4.y}, Dn);
+          const float4 r2 = q[2];
+          Cr = fma2(W, pk(r2.x, r2.x), Cr);
+          Cg = fma2(W, pk(r2.y, r2.y), Cg);
+          Cb = fma2(W, pk(r2.z, r2.z), Cb);
+          Dn = fma2(W, pk(r0.w, r0.w), Dn);
           Aw = add2(Aw, W);
           T = TN;
         }
