@@ -200,7 +200,7 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
 // images are bit-identical to the 256-thread reference walk.
 constexpr int R2_THREADS = 128;
 
-__global__ void __launch_bounds__(R2_THREADS, 8)
+__global__ void __launch_bounds__(R2_THREADS, 10)
 raster2_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
                float* __restrict__ depth, float* __restrict__ alpha_out) {
   constexpr int BATCH = 256;
