@@ -30,8 +30,10 @@ void launch_project(int e0, int ngroups, int nblk, int max_degree, const EnvGrou
 cudaError_t project_init();
 cudaError_t sort_bin_init();
 uint32_t sort_blocks(uint32_t V);
-int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, const RenderParams& rp, const ChunkWS& ws,
-                    uint32_t* ghist, uint32_t* thist, cudaStream_t s);
+size_t sort_ghist_words();
+int depth_passes(uint32_t span);
+int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, const RenderParams& rp,
+                    const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s);
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s);
@@ -74,7 +76,7 @@ struct gg_context {
   int scene_table_cap = 0;
   int chunk = DEFAULT_CHUNK;
   // workspace
-  DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase;
+  DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase, zmm;
   DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1;
   DevBuf sorted, ranges, counters, valid_out, perm, groups, blkbase, ghist, thist;
   DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval, dconic;
@@ -89,6 +91,7 @@ struct gg_context {
   int32_t* h_perm = nullptr;
   EnvGroup* h_groups = nullptr;
   uint32_t* h_blkbase = nullptr;
+  uint32_t* h_zmm = nullptr;
   int h_cap = 0;
   // debug snapshot (host)
   std::vector<int32_t> d_tc, d_stile, d_sgid, d_ranges, d_neval;
@@ -162,8 +165,10 @@ bool ensure_host(gg_context* ctx, int n) {
   if (ctx->h_cap >= n) return true;
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase); cudaFreeHost(ctx->h_kbase);
   cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
+  cudaFreeHost(ctx->h_zmm);
   int cap = std::max(n, 1024);
   if (cudaMallocHost(&ctx->h_blkbase, (cap + 1) * 4) != cudaSuccess) return false;
+  if (cudaMallocHost(&ctx->h_zmm, cap * 8) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_ids, cap * 4) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_perm, cap * 4) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_groups, cap * sizeof(EnvGroup)) != cudaSuccess) return false;
@@ -268,7 +273,7 @@ gg_status gg_destroy(gg_context* ctx) {
     dev_free(ctx, sc.pos_op, s); dev_free(ctx, sc.cov_a, s); dev_free(ctx, sc.cov_b, s);
     dev_free(ctx, sc.aux, s); dev_free(ctx, sc.sh, s);
   }
-  DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
+  DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->zmm, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
                    &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect,
                    &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->perm, &ctx->groups,
                    &ctx->blkbase, &ctx->ghist, &ctx->thist,
@@ -280,6 +285,7 @@ gg_status gg_destroy(gg_context* ctx) {
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
   cudaFreeHost(ctx->h_kbase); cudaFreeHost(ctx->h_err);
   cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
+  cudaFreeHost(ctx->h_zmm);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev_copy);
   cudaStreamDestroy(s);
@@ -481,7 +487,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       !ensure(ctx, ctx->blkcnt, (size_t)chunk * nblk * 4, s) || !ensure(ctx, ctx->vcnt, chunk * 4, s) ||
       !ensure(ctx, ctx->kcnt, chunk * 4, s) || !ensure(ctx, ctx->rbase, chunk * 8, s) ||
       !ensure(ctx, ctx->kbase, chunk * 8, s) || !ensure(ctx, ctx->ranges, (size_t)chunk * ntiles * 8, s) ||
-      !ensure_host(ctx, std::max(E, chunk)) || (counters && !ensure(ctx, ctx->counters, (size_t)E * 32, s)))
+      !ensure(ctx, ctx->zmm, (size_t)chunk * 8, s) || !ensure_host(ctx, std::max(E, chunk)) || (counters && !ensure(ctx, ctx->counters, (size_t)E * 32, s)))
     return fail(ctx, GG_E_OOM, "gg_render: workspace allocation failed");
   if (counters) CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)E * 32, s));
   CK(cudaMemsetAsync(ctx->errflag.p, 0, 4, s));
@@ -539,9 +545,13 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ws.rec_base = P<uint64_t>(ctx->rbase);
     ws.k_base = P<uint64_t>(ctx->kbase);
     ws.ranges = P<uint2>(ctx->ranges);
+    ws.zmin = P<uint32_t>(ctx->zmm);
+    ws.zmax = P<uint32_t>(ctx->zmm) + chunk;
     ws.nwords = nwords;
     ws.nblk = nblk;
     const EnvGroup* groups = P<EnvGroup>(ctx->groups);
+    CK(cudaMemsetAsync(ws.zmin, 0xff, ec * 4, s));
+    CK(cudaMemsetAsync(ws.zmax, 0, ec * 4, s));
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], s));
     // K1a + K2
     launch_cull_count(e0, ngroups, nblk, groups, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
@@ -574,6 +584,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ctx->launches++;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->h_kcnt, ws.kcnt, ec * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->h_zmm, ws.zmin, ec * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->h_zmm + ctx->h_cap, ws.zmax, ec * 4, cudaMemcpyDeviceToHost, s));
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], s));
     CK(cudaStreamSynchronize(s));
     uint64_t K = 0;
@@ -588,11 +600,16 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     uint32_t nb = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_blkbase[i] = nb; nb += sort_blocks(ctx->h_vcnt[i]); }
     ctx->h_blkbase[ec] = nb;
-    if (!ensure(ctx, ctx->blkbase, (size_t)(ec + 1) * 4, s) || !ensure(ctx, ctx->ghist, (size_t)nb * 256 * 4, s) ||
+    uint32_t span = 0;
+    for (int i = 0; i < ec; ++i)
+      if (ctx->h_vcnt[i]) span = std::max(span, ctx->h_zmm[ctx->h_cap + i] - ctx->h_zmm[i]);
+    const int passes = depth_passes(span);
+    if (!ensure(ctx, ctx->blkbase, (size_t)(ec + 1) * 4, s) ||
+        !ensure(ctx, ctx->ghist, (size_t)nb * sort_ghist_words() * 4, s) ||
         !ensure(ctx, ctx->thist, (size_t)nb * ntiles * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: sort workspace allocation failed");
     CK(cudaMemcpyAsync(ctx->blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, cudaMemcpyHostToDevice, s));
-    ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->blkbase), rp, ws, P<uint32_t>(ctx->ghist),
+    ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->blkbase), passes, rp, ws, P<uint32_t>(ctx->ghist),
                                      P<uint32_t>(ctx->thist), s);
     CK(cudaGetLastError());
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], s));

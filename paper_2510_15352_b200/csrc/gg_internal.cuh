@@ -70,6 +70,8 @@ struct ChunkWS {
   float4* dconic;       // debug only (null unless intermediates are kept): raw conic A, B, C, opacity
   uint2* rect;          // (x0 | x1<<16, y0 | y1<<16)
   uint32_t* zkey;       // f32 bits of z
+  uint32_t* zmin;       // [Ec] min / max depth bits per env (depth-sort key offset)
+  uint32_t* zmax;
   uint32_t* gid;        // Gaussian index (debug dumps only; may be null)
   // depth-sort scratch [V]
   uint32_t* dk0; uint32_t* dv0; uint32_t* dk1; uint32_t* dv1;

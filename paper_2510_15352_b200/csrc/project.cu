@@ -87,8 +87,10 @@ __device__ __forceinline__ void load_group_cams(EnvConst* cams, const EnvConst* 
 
 // conservative footprint test (DESIGN.md §4 K1a): lambda1 <= a + c + sqrt(0.1)
 // and a + c <= s_max^2 |T|_F^2 + 0.6; generous margins absorb f32 rounding.
-__device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float smax2, const RenderParams& rp) {
+__device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float smax2, const RenderParams& rp,
+                                              uint32_t& zbits) {
   const float3 p = to_cam(c, g);
+  zbits = __float_as_uint(p.z);
   if (!(p.z > rp.near_p && p.z <= rp.far_p)) return false;   // exact (canonical p_z)
   const float rz = 1.f / p.z;
   const float u = c.fx * p.x * rz + c.cx;
@@ -129,11 +131,19 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
   }
   const int wi = blockIdx.y * (PROJ_BLOCK / 32) + warp;
   for (int k = 0; k < grp.cnt; ++k) {
-    const bool keep = i < n && maybe_visible(cams[k], g, smax2, rp);
+    uint32_t zb = 0;
+    const bool keep = i < n && maybe_visible(cams[k], g, smax2, rp, zb);
     const uint32_t word = __ballot_sync(0xffffffffu, keep);
+    // depth-key range of the kept records (= the env's record set): sort key offset
+    const uint32_t zmn = __reduce_min_sync(0xffffffffu, keep ? zb : 0xffffffffu);
+    const uint32_t zmx = __reduce_max_sync(0xffffffffu, keep ? zb : 0u);
     if (lane == 0) {
       ws.flags[(size_t)(grp.elo + k) * ws.nwords + wi] = word;
       wc[k][warp] = __popc(word);
+      if (word) {
+        atomicMin(&ws.zmin[grp.elo + k], zmn);
+        atomicMax(&ws.zmax[grp.elo + k], zmx);
+      }
     }
   }
   __syncthreads();

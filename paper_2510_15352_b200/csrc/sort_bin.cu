@@ -28,10 +28,14 @@
 
 namespace gg {
 
-constexpr int SB_THREADS = 1024;
+constexpr int SB_THREADS = 1024;                // placement kernels
 constexpr int SB_WARPS = 32;
-constexpr int SB_IPT = 8;
-constexpr int SB_BLK = SB_THREADS * SB_IPT;   // 8192 elements / records per block
+constexpr int SORT_BLK = 4096;                  // records per sort block (depth and placement)
+constexpr int DS_THREADS = 512;                 // depth passes: 16 warps x 8 elements
+constexpr int DS_WARPS = DS_THREADS / 32;
+constexpr int DS_IPT = SORT_BLK / DS_THREADS;
+constexpr int DS_BITS = 10;                     // digit width of the depth passes
+constexpr int DS_RADIX = 1 << DS_BITS;
 
 // blocks of the chunk: env of block b is the e with blk_base[e] <= b < blk_base[e+1]
 struct BlockTable {
@@ -58,13 +62,6 @@ __device__ __forceinline__ uint32_t peers_of(uint32_t v, int bits, uint32_t acti
   }
   return peers;
 }
-
-struct RankSmem {
-  uint32_t wcnt[SB_WARPS][256];   // per-warp digit counts -> offsets
-  uint32_t dstart[256];
-  uint32_t dcnt[256];
-  uint32_t wsum[SB_WARPS];
-};
 
 // exclusive scan over the block (all threads call); *total = block sum
 __device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* wsum, uint32_t* total) {
@@ -94,157 +91,163 @@ __device__ __forceinline__ uint32_t block_scan(uint32_t x, uint32_t* wsum, uint3
   return excl;
 }
 
-// Block-local stable ranking of up to 8192 elements: element (warp w, round
-// j, lane l) has block index 256 w + 32 j + l and digit d[j] < 2^bits.  On
-// return lpos[j] is its position in the block sorted stably by digit, and
-// rs.dstart / rs.dcnt hold digit starts / counts.  rs.wcnt is zero on entry
-// and on return.
-__device__ __forceinline__ void block_rank(const uint32_t (&d)[SB_IPT], uint32_t n, int bits,
-                                           uint32_t (&lpos)[SB_IPT], RankSmem& rs) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t lt = lanemask_lt();
-  uint32_t rk[SB_IPT];
-#pragma unroll
-  for (int j = 0; j < SB_IPT; ++j) {
-    const uint32_t e = warp * 32 * SB_IPT + j * 32 + lane;
-    const bool ok = e < n;
-    const uint32_t active = __ballot_sync(0xffffffffu, ok);
-    rk[j] = 0;
-    if (active) {
-      const uint32_t peers = peers_of(d[j], bits, active);
-      const uint32_t before = ok ? rs.wcnt[warp][d[j]] : 0u;
-      __syncwarp();
-      if (ok && lane == __ffs(peers) - 1) rs.wcnt[warp][d[j]] = before + __popc(peers);
-      __syncwarp();
-      rk[j] = before + __popc(peers & lt);
-    }
-  }
-  __syncthreads();
-  const int radix = 1 << bits;
-  uint32_t c = 0;
-  if (tid < radix) {
-#pragma unroll 8
-    for (int w = 0; w < SB_WARPS; ++w) {
-      const uint32_t x = rs.wcnt[w][tid];
-      rs.wcnt[w][tid] = c;
-      c += x;
-    }
-    rs.dcnt[tid] = c;
-  }
-  uint32_t total;
-  const uint32_t ex = block_scan(tid < radix ? c : 0u, rs.wsum, &total);
-  if (tid < radix) rs.dstart[tid] = ex;
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < SB_IPT; ++j) {
-    const uint32_t e = warp * 32 * SB_IPT + j * 32 + lane;
-    lpos[j] = e < n ? rs.dstart[d[j]] + rs.wcnt[warp][d[j]] + rk[j] : 0u;
-  }
-  __syncthreads();
-  if (tid < radix)
-#pragma unroll 8
-    for (int w = 0; w < SB_WARPS; ++w) rs.wcnt[w][tid] = 0u;
-}
-
 __device__ __forceinline__ void unpack_rect(uint2 r, uint32_t& x0, uint32_t& x1, uint32_t& y0, uint32_t& y1) {
   x0 = r.x & 0xffffu; x1 = r.x >> 16; y0 = r.y & 0xffffu; y1 = r.y >> 16;
 }
 
-// Input / output arrays of depth pass p (all indexed rec_base[e] + j).
+// Input / output arrays of depth pass p (all indexed rec_base[e] + j).  The
+// sort key is the f32 depth bits minus the env's minimum (a monotone map of
+// the positive f32 bits), so a typical ~27-bit span needs 3 passes of 10 bits.
 struct DepthIO {
-  const uint32_t* kin;   // keys in
+  const uint32_t* kin;   // keys in (f32 depth bits)
   const uint32_t* vin;   // values in (null = identity j)
   uint32_t* kout;        // keys out (null on the last pass)
   uint32_t* vout;
 };
 
-// ---- depth passes --------------------------------------------------------
-__global__ void __launch_bounds__(SB_THREADS)
-depth_upsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, uint32_t* ghist) {
-  __shared__ uint32_t h[256];
-  const uint32_t b = blockIdx.x;
-  const int e = block_env(bt, b);
-  const uint32_t j0 = (b - bt.blk_base[e]) * SB_BLK;
-  const uint32_t V = ws.vcnt[e];
-  const uint32_t n = min((uint32_t)SB_BLK, V - j0);
-  const uint64_t rb = ws.rec_base[e];
-  if (threadIdx.x < 256) h[threadIdx.x] = 0;
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n; i += SB_THREADS)
-    atomicAdd(&h[(io.kin[rb + j0 + i] >> shift) & 255u], 1u);
-  __syncthreads();
-  if (threadIdx.x < 256) ghist[(size_t)b * 256 + threadIdx.x] = h[threadIdx.x];
+__device__ __forceinline__ uint32_t depth_digit(uint32_t z, uint32_t zmin, int shift) {
+  return ((z - zmin) >> shift) & (DS_RADIX - 1);
 }
 
-// one CTA (256 threads = digits) per env: ghist[b][d] -> output offset of
-// (block b, digit d) relative to the env's segment
-__global__ void __launch_bounds__(256) depth_scan_kernel(BlockTable bt, uint32_t* ghist) {
-  __shared__ uint32_t wsum[8];
+// ---- depth passes --------------------------------------------------------
+__global__ void __launch_bounds__(DS_THREADS)
+depth_upsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, uint32_t* ghist) {
+  __shared__ uint32_t h[DS_RADIX];
+  const uint32_t b = blockIdx.x;
+  const int e = block_env(bt, b);
+  const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
+  const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
+  const uint64_t rb = ws.rec_base[e];
+  const uint32_t zmin = ws.zmin[e];
+  for (int i = threadIdx.x; i < DS_RADIX; i += DS_THREADS) h[i] = 0;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += DS_THREADS)
+    atomicAdd(&h[depth_digit(io.kin[rb + j0 + i], zmin, shift)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < DS_RADIX; i += DS_THREADS) ghist[(size_t)b * DS_RADIX + i] = h[i];
+}
+
+// one CTA (1024 threads = digits) per env: ghist[b][d] -> output offset of
+// (block b, digit d) relative to the env's segment (digit-major, block-minor)
+__global__ void __launch_bounds__(DS_RADIX) depth_scan_kernel(BlockTable bt, uint32_t* ghist) {
+  __shared__ uint32_t wsum[32];
   const int e = blockIdx.x;
   const uint32_t b0 = bt.blk_base[e], b1 = bt.blk_base[e + 1];
   const int d = threadIdx.x;
+  uint32_t* col = ghist + d;
   uint32_t run = 0;
-  for (uint32_t b = b0; b < b1; ++b) {
-    const uint32_t x = ghist[(size_t)b * 256 + d];
-    ghist[(size_t)b * 256 + d] = run;
-    run += x;
-  }
-  // digit-major exclusive scan of the totals (256 threads = 8 warps)
-  const int lane = d & 31, warp = d >> 5;
-  uint32_t s = run;
+  for (uint32_t b = b0; b < b1; b += 8) {          // 8 independent loads in flight
+    uint32_t x[8];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-    if (lane >= o) s += y;
+    for (int u = 0; u < 8; ++u) x[u] = b + u < b1 ? col[(size_t)(b + u) * DS_RADIX] : 0u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b + u < b1) { col[(size_t)(b + u) * DS_RADIX] = run; run += x[u]; }
   }
-  if (lane == 31) wsum[warp] = s;
-  __syncthreads();
-  uint32_t off = 0;
-  for (int w = 0; w < warp; ++w) off += wsum[w];
-  const uint32_t base = off + s - run;
-  for (uint32_t b = b0; b < b1; ++b) ghist[(size_t)b * 256 + d] += base;
+  uint32_t total;
+  const uint32_t base = block_scan(run, wsum, &total);
+  for (uint32_t b = b0; b < b1; ++b) col[(size_t)b * DS_RADIX] += base;
 }
 
 struct DownSmem {
-  RankSmem rs;
-  uint32_t sk[SB_BLK];
-  uint32_t sv[SB_BLK];
+  uint32_t wcnt[DS_WARPS][DS_RADIX];   // per-warp digit counts -> offsets (64 KB)
+  uint32_t dstart[DS_RADIX];
+  uint32_t wsum[32];
+  uint32_t sk[SORT_BLK];
+  uint32_t sv[SORT_BLK];
 };
 
-__global__ void __launch_bounds__(SB_THREADS)
+// Stable block-local ranking: element (warp w, round j, lane l) has block
+// index 256 w + 32 j + l and digit d[j].  lpos[j] = position in the block
+// sorted stably by digit; sm.dstart = digit starts.  wcnt zero on entry/exit.
+__device__ __forceinline__ void block_rank(const uint32_t (&d)[DS_IPT], uint32_t n, uint32_t (&lpos)[DS_IPT],
+                                           DownSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt = lanemask_lt();
+  uint32_t rk[DS_IPT];
+#pragma unroll
+  for (int j = 0; j < DS_IPT; ++j) {
+    const uint32_t e = warp * 32 * DS_IPT + j * 32 + lane;
+    const bool ok = e < n;
+    const uint32_t active = __ballot_sync(0xffffffffu, ok);
+    rk[j] = 0;
+    if (active) {
+      const uint32_t peers = peers_of(d[j], DS_BITS, active);
+      const uint32_t before = ok ? sm.wcnt[warp][d[j]] : 0u;
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) sm.wcnt[warp][d[j]] = before + __popc(peers);
+      __syncwarp();
+      rk[j] = before + __popc(peers & lt);
+    }
+  }
+  __syncthreads();
+  // per digit: prefix over warps; digit totals -> block-wide exclusive scan
+  uint32_t c[DS_RADIX / DS_THREADS];
+  uint32_t mine = 0;
+#pragma unroll
+  for (int k = 0; k < DS_RADIX / DS_THREADS; ++k) {
+    const int dd = tid * (DS_RADIX / DS_THREADS) + k;
+    uint32_t run = 0;
+#pragma unroll 4
+    for (int w = 0; w < DS_WARPS; ++w) {
+      const uint32_t x = sm.wcnt[w][dd];
+      sm.wcnt[w][dd] = run;
+      run += x;
+    }
+    c[k] = run;
+    mine += run;
+  }
+  uint32_t total;
+  uint32_t ex = block_scan(mine, sm.wsum, &total);
+#pragma unroll
+  for (int k = 0; k < DS_RADIX / DS_THREADS; ++k) {
+    sm.dstart[tid * (DS_RADIX / DS_THREADS) + k] = ex;
+    ex += c[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < DS_IPT; ++j) {
+    const uint32_t e = warp * 32 * DS_IPT + j * 32 + lane;
+    lpos[j] = e < n ? sm.dstart[d[j]] + sm.wcnt[warp][d[j]] + rk[j] : 0u;
+  }
+  __syncthreads();
+  for (int i = tid; i < DS_WARPS * DS_RADIX; i += DS_THREADS) (&sm.wcnt[0][0])[i] = 0u;
+}
+
+__global__ void __launch_bounds__(DS_THREADS, 2)
 depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const uint32_t* ghist) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   DownSmem& sm = *reinterpret_cast<DownSmem*>(smem_raw);
   const uint32_t b = blockIdx.x;
   const int e = block_env(bt, b);
-  const uint32_t j0 = (b - bt.blk_base[e]) * SB_BLK;
-  const uint32_t V = ws.vcnt[e];
-  const uint32_t n = min((uint32_t)SB_BLK, V - j0);
+  const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
+  const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
   const uint64_t rb = ws.rec_base[e];
+  const uint32_t zmin = ws.zmin[e];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < SB_WARPS * 256; i += SB_THREADS) (&sm.rs.wcnt[0][0])[i] = 0u;
-  __syncthreads();
-  uint32_t k[SB_IPT], v[SB_IPT], d[SB_IPT], lp[SB_IPT];
+  for (int i = tid; i < DS_WARPS * DS_RADIX; i += DS_THREADS) (&sm.wcnt[0][0])[i] = 0u;
+  uint32_t k[DS_IPT], v[DS_IPT], d[DS_IPT], lp[DS_IPT];
 #pragma unroll
-  for (int j = 0; j < SB_IPT; ++j) {
-    const uint32_t i = warp * 32 * SB_IPT + j * 32 + lane;
+  for (int j = 0; j < DS_IPT; ++j) {
+    const uint32_t i = warp * 32 * DS_IPT + j * 32 + lane;
     const bool ok = i < n;
     k[j] = ok ? io.kin[rb + j0 + i] : 0u;
     v[j] = ok ? (io.vin ? io.vin[rb + j0 + i] : j0 + i) : 0u;
-    d[j] = (k[j] >> shift) & 255u;
+    d[j] = depth_digit(k[j], zmin, shift);
   }
-  block_rank(d, n, 8, lp, sm.rs);
+  __syncthreads();
+  block_rank(d, n, lp, sm);
 #pragma unroll
-  for (int j = 0; j < SB_IPT; ++j) {
-    const uint32_t i = warp * 32 * SB_IPT + j * 32 + lane;
+  for (int j = 0; j < DS_IPT; ++j) {
+    const uint32_t i = warp * 32 * DS_IPT + j * 32 + lane;
     if (i < n) { sm.sk[lp[j]] = k[j]; sm.sv[lp[j]] = v[j]; }
   }
   __syncthreads();
-  const uint32_t* off = ghist + (size_t)b * 256;
-  for (uint32_t q = tid; q < n; q += SB_THREADS) {
+  const uint32_t* off = ghist + (size_t)b * DS_RADIX;
+  for (uint32_t q = tid; q < n; q += DS_THREADS) {
     const uint32_t kk = sm.sk[q];
-    const uint32_t dd = (kk >> shift) & 255u;
-    const uint64_t pos = rb + off[dd] + (q - sm.rs.dstart[dd]);
+    const uint32_t dd = depth_digit(kk, zmin, shift);
+    const uint64_t pos = rb + off[dd] + (q - sm.dstart[dd]);
     if (io.kout) io.kout[pos] = kk;
     io.vout[pos] = sm.sv[q];
   }
@@ -258,8 +261,8 @@ place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntile
   uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
   const uint32_t b = blockIdx.x;
   const int e = block_env(bt, b);
-  const uint32_t j0 = (b - bt.blk_base[e]) * SB_BLK;
-  const uint32_t n = min((uint32_t)SB_BLK, ws.vcnt[e] - j0);
+  const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
+  const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
   const uint64_t rb = ws.rec_base[e];
   for (int i = threadIdx.x; i < ntiles; i += SB_THREADS) h[i] = 0u;
   __syncthreads();
@@ -285,12 +288,17 @@ __global__ void __launch_bounds__(SB_THREADS) place_scan_kernel(BlockTable bt, C
   for (int base = 0; base < ntiles; base += SB_THREADS) {
     const int t = base + threadIdx.x;
     uint32_t run = 0;
-    if (t < ntiles)
-      for (uint32_t b = b0; b < b1; ++b) {
-        const uint32_t x = thist[(size_t)b * ntiles + t];
-        thist[(size_t)b * ntiles + t] = run;
-        run += x;
+    if (t < ntiles) {
+      uint32_t* col = thist + t;
+      for (uint32_t b = b0; b < b1; b += 8) {       // 8 independent loads in flight
+        uint32_t x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = b + u < b1 ? col[(size_t)(b + u) * ntiles] : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (b + u < b1) { col[(size_t)(b + u) * ntiles] = run; run += x[u]; }
       }
+    }
     uint32_t total;
     const uint32_t ex = carry + block_scan(t < ntiles ? run : 0u, wsum, &total);
     if (t < ntiles) {
@@ -318,8 +326,8 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
   uint32_t* wh = gb + nt;                                  // [S][nw2] packed u16 counters / cursors
   const uint32_t b = blockIdx.x;
   const int e = block_env(bt, b);
-  const uint32_t j0 = (b - bt.blk_base[e]) * SB_BLK;
-  const uint32_t nrec = min((uint32_t)SB_BLK, ws.vcnt[e] - j0);
+  const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
+  const uint32_t nrec = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
   const uint64_t rb = ws.rec_base[e];
   uint32_t* out = ws.sorted + ws.k_base[e];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -433,30 +441,39 @@ cudaError_t sort_bin_init() {
                               (int)(MAX_TILES * 4));
 }
 
-uint32_t sort_blocks(uint32_t V) { return (V + SB_BLK - 1) / SB_BLK; }
+uint32_t sort_blocks(uint32_t V) { return (V + SORT_BLK - 1) / SORT_BLK; }
+size_t sort_ghist_words() { return DS_RADIX; }
+
+// number of depth passes for a key span (max over the chunk's envs of zmax - zmin)
+int depth_passes(uint32_t span) {
+  int bits = 0;
+  while (bits < 32 && (span >> bits) != 0) ++bits;
+  const int p = (bits + DS_BITS - 1) / DS_BITS;
+  return p < 1 ? 1 : p;
+}
 
 // Enqueue K3-K5 for a chunk.  blk_base: device [ec+1] block prefix; nb total
-// blocks; ghist >= nb*256 u32; thist >= nb*ntiles u32.  Returns launches.
-int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, const RenderParams& rp, const ChunkWS& ws,
-                    uint32_t* ghist, uint32_t* thist, cudaStream_t s) {
+// blocks; ghist >= nb*DS_RADIX u32; thist >= nb*ntiles u32.  Returns launches.
+int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, const RenderParams& rp,
+                    const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s) {
   if (nb == 0) {
     cudaMemsetAsync(ws.ranges, 0, (size_t)ec * rp.ntiles * sizeof(uint2), s);
     return 0;
   }
   BlockTable bt{blk_base, ec};
   int launches = 0;
-  for (int p = 0; p < 4; ++p) {
+  for (int p = 0; p < passes; ++p) {
     DepthIO io;
     io.kin = p == 0 ? ws.zkey : ((p & 1) ? ws.dk0 : ws.dk1);
     io.vin = p == 0 ? nullptr : ((p & 1) ? ws.dv0 : ws.dv1);
-    io.kout = p == 3 ? nullptr : ((p & 1) ? ws.dk1 : ws.dk0);
+    io.kout = p == passes - 1 ? nullptr : ((p & 1) ? ws.dk1 : ws.dk0);
     io.vout = (p & 1) ? ws.dv1 : ws.dv0;
-    depth_upsweep_kernel<<<nb, SB_THREADS, 0, s>>>(bt, ws, io, 8 * p, ghist);
-    depth_scan_kernel<<<ec, 256, 0, s>>>(bt, ghist);
-    depth_downsweep_kernel<<<nb, SB_THREADS, depth_down_smem(), s>>>(bt, ws, io, 8 * p, ghist);
+    depth_upsweep_kernel<<<nb, DS_THREADS, 0, s>>>(bt, ws, io, DS_BITS * p, ghist);
+    depth_scan_kernel<<<ec, DS_RADIX, 0, s>>>(bt, ghist);
+    depth_downsweep_kernel<<<nb, DS_THREADS, depth_down_smem(), s>>>(bt, ws, io, DS_BITS * p, ghist);
     launches += 3;
   }
-  const uint32_t* order = ws.dv1;   // values of the last depth pass
+  const uint32_t* order = ((passes - 1) & 1) ? ws.dv1 : ws.dv0;   // values of the last depth pass
   place_upsweep_kernel<<<nb, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
   place_scan_kernel<<<ec, SB_THREADS, 0, s>>>(bt, ws, thist, rp.ntiles);
   place_downsweep_kernel<<<nb, SB_THREADS, place_down_smem(rp.ntiles), s>>>(bt, ws, order, rp, thist,
