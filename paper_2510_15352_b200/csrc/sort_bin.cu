@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(SB_THREADS) place_scan_kernel(BlockTable bt, C
 // warp walks its records in order, 32 (record, tile) pairs per step, ranks
 // equal tiles among the lanes with a ballot multisplit and writes each
 // record index at its final slot; no block barrier inside the walk.
+template <int TB>   // tile-id bits (compile time: the multisplit fully unrolls)
 __global__ void __launch_bounds__(SB_THREADS)
 place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderParams rp, const uint32_t* thist,
                        int S) {
@@ -366,8 +367,6 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
   // phase 3: ordered walk, 32 records per step, their pairs 32 at a time
   if (warp >= S) return;
   uint32_t* h = wh + (size_t)warp * nw2;
-  int tile_bits = 0;
-  while ((1 << tile_bits) < nt) ++tile_bits;
   const uint32_t lt = lanemask_lt();
   for (uint32_t base = s0; base < s1; base += 32) {
     const uint32_t j = base + lane;
@@ -405,10 +404,16 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
       if (ok) {
         // qq / o_w for small integers via the f32 reciprocal (exact: qq < 2^20, o_w < 2^16)
         const uint32_t qq = f - (o_incl - o_np);
-        const uint32_t row = (uint32_t)(((float)qq + 0.5f) * __frcp_rn((float)o_w));
+        const uint32_t row = (uint32_t)__fdividef((float)qq + 0.5f, (float)o_w);
         t = (o_y0 + row) * rp.TX + o_x0 + (qq - row * o_w);
       }
-      const uint32_t peers = peers_of(t, tile_bits, __ballot_sync(0xffffffffu, ok));
+      uint32_t peers = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+      for (int bb = 0; bb < TB; ++bb) {
+        const bool bit = (t >> bb) & 1u;
+        const uint32_t m = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? m : ~m;
+      }
       const uint32_t before = ok ? (h[t >> 1] >> (16 * (t & 1))) & 0xffffu : 0u;
       __syncwarp();
       if (ok && lane == __ffs(peers) - 1) atomicAdd(&h[t >> 1], __popc(peers) << (16 * (t & 1)));
@@ -434,7 +439,13 @@ cudaError_t sort_bin_init() {
   cudaError_t e = cudaFuncSetAttribute(depth_downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)depth_down_smem());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(place_downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(place_downsweep_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)place_down_smem(MAX_TILES));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(place_downsweep_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)place_down_smem(MAX_TILES));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(place_downsweep_kernel<13>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)place_down_smem(MAX_TILES));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(place_upsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -476,8 +487,14 @@ int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, c
   const uint32_t* order = ((passes - 1) & 1) ? ws.dv1 : ws.dv0;   // values of the last depth pass
   place_upsweep_kernel<<<nb, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
   place_scan_kernel<<<ec, SB_THREADS, 0, s>>>(bt, ws, thist, rp.ntiles);
-  place_downsweep_kernel<<<nb, SB_THREADS, place_down_smem(rp.ntiles), s>>>(bt, ws, order, rp, thist,
-                                                                            place_segments(rp.ntiles));
+  const size_t psm = place_down_smem(rp.ntiles);
+  const int S = place_segments(rp.ntiles);
+  if (rp.ntiles <= 256)
+    place_downsweep_kernel<8><<<nb, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+  else if (rp.ntiles <= 2048)
+    place_downsweep_kernel<11><<<nb, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+  else
+    place_downsweep_kernel<13><<<nb, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   return launches + 3;
 }
 
