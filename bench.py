@@ -112,6 +112,21 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the latest committed ncu --set full
+    capture (profiles/r*/ncu_summary.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_summary.json")))
+    if not files:
+        return None, None
+    try:
+        d = json.load(open(files[-1]))
+        r = d["full_captures"][kernel]
+        return r.get("dram_bytes_total"), os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -280,8 +295,10 @@ def main():
     bytes_proj = scene.n * 56 + n_vis * 64
     if names[dom] == "raster":
         ach = flops / (stage_ms[2] / 1000.0) / 1e12
-        roof = {"kernel": "raster_kernel (K6)", "bound": "alu", "achieved": ach, "peak": alu_peak,
-                "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": None,
+        tr, src = ncu_traffic("raster2_kernel")
+        roof = {"kernel": "raster2_kernel (K6)", "bound": "alu", "achieved": ach, "peak": alu_peak,
+                "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": tr,
+                "traffic_note": f"DRAM bytes per launch (one {args.chunk or 512}-env chunk) from {src}" if tr else None,
                 "peak_basis": f"148 SM x 128 FP32 lanes x 2 (FFMA) x {clock_mhz:.0f} MHz median SM clock under load",
                 "work": f"{n_eval:,} evaluated pairs x {FLOP_EVAL} + {n_contrib:,} blended x {FLOP_CONTRIB} flops"}
     elif names[dom] == "sort_bin":

@@ -1,0 +1,20 @@
+#!/bin/bash
+# GPU-box profiling pass for one round (run under gpurun from the repo root):
+#   1. the bench command without ncu (must exit 0 first)
+#   2. the ncu launch list of the same command (gpu__time_duration per launch)
+#   3. one `ncu --set full` capture of each hot kernel (steady-state launch)
+# Outputs land in gpurun_out/prof_<round>/ ; tools/ncu_summary.py turns them
+# into profiles/<round>/.
+set -e
+R=${1:-r01}
+O=gpurun_out/prof_$R
+mkdir -p $O
+CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu"
+$CMD > $O/bench_plain.json 2> $O/bench_plain.err
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > /dev/null 2>&1
+SMALL="python bench.py --envs 512 --steps 1 --warmup 1 --no-e2e --no-cpu"
+$SMALL > $O/small_plain.json 2>&1
+for k in raster2_kernel project_kernel cull_count_kernel depth_downsweep place_downsweep depth_upsweep place_upsweep; do
+  ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o $O/full_$k $SMALL > $O/ncu_$k.log 2>&1 || echo "ncu $k failed"
+done
+ls -la $O
