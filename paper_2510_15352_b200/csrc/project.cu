@@ -92,7 +92,7 @@ __device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float
   const float3 p = to_cam(c, g);
   zbits = __float_as_uint(p.z);
   if (!(p.z > rp.near_p && p.z <= rp.far_p)) return false;   // exact (canonical p_z)
-  const float rz = 1.f / p.z;
+  const float rz = __fdividef(1.f, p.z);      // approximate: the test has margins
   const float u = c.fx * p.x * rz + c.cx;
   const float v = c.fy * p.y * rz + c.cy;
   const float txz = fminf(c.lim_xp, fmaxf(-c.lim_xn, p.x * rz));
@@ -107,7 +107,7 @@ __device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float
     nT += t0 * t0 + t1 * t1;
   }
   const float lam_b = (smax2 * nT + 0.9163f) * 1.001f + 0.01f;
-  const float rb = 3.f * sqrtf(lam_b) * 1.001f + 2.f;
+  const float rb = 3.f * (lam_b * rsqrtf(lam_b)) * 1.002f + 2.f;
   return (u + rb > 0.f) && (u - rb < (float)(rp.TX * TILE)) && (v + rb > 0.f) && (v - rb < (float)(rp.TY * TILE));
 }
 
@@ -294,14 +294,18 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
       sm.cb[tid] = __ldg(&sc.cov_b[i]);
       sm.dcb[tid] = __ldg(&sc.aux[i]).x;
     }
-    if (deg > 0) {
-      // coalesced copy of [256][stride] -> transposed [K*3][SH_PITCH]
-      const int nf = K * 3;
-      const int nl = min(PROJ_BLOCK, c0.n - i0);
-      const float* src = sc.sh + (size_t)i0 * sc.sh_stride;
-      for (int x = tid; x < nl * sc.sh_stride; x += PROJ_BLOCK) {
-        const int l = x / sc.sh_stride, j = x - l * sc.sh_stride;
-        if (j < nf) sm.sh[j * SH_PITCH + l] = __ldg(&src[x]);
+    if (deg > 0 && i < c0.n) {
+      // this thread's Gaussian: 128-bit loads of its SH row, transposed into
+      // [coefficient][Gaussian] so the projection reads are conflict-free
+      const int nf4 = (K * 3 + 3) / 4;
+      const float4* src = reinterpret_cast<const float4*>(sc.sh + (size_t)i * sc.sh_stride);
+#pragma unroll 4
+      for (int q = 0; q < nf4; ++q) {
+        const float4 x = __ldg(&src[q]);
+        sm.sh[(4 * q + 0) * SH_PITCH + tid] = x.x;
+        sm.sh[(4 * q + 1) * SH_PITCH + tid] = x.y;
+        sm.sh[(4 * q + 2) * SH_PITCH + tid] = x.z;
+        sm.sh[(4 * q + 3) * SH_PITCH + tid] = x.w;
       }
     }
   }
