@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--cpu-envs", type=int, default=4, help="oracle sample size for cpu_baseline")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo only to exercise the multi-rank path on a single-GPU box")
     return p.parse_args()
 
 
@@ -137,6 +139,7 @@ def measured_peaks():
 def oracle_sample(scene, cams, envs, sh_degree):
     """Time the CPU oracle (as it stands) on `envs` of the pose set."""
     import oracle
+    oracle.use_all_cores()
     t0 = time.perf_counter()
     osc = oracle.OracleScene.from_inputs(scene)
     for e in envs:
@@ -154,6 +157,7 @@ def run_reference(args):
     scene = gi.config_scene(args.config, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])
     cams = gi.cameras(0, max(1, args.steps + args.warmup), c["width"], c["height"], scene)
     import oracle
+    oracle.use_all_cores()
     osc = oracle.OracleScene.from_inputs(scene)
     for w in range(args.warmup):
         oracle.render_env(osc, cams.viewmats[w], cams.intrinsics[w], cams.width, cams.height)
@@ -188,17 +192,22 @@ def main():
     from paper_2510_15352_b200.dist import dist_env, fold_digests, gather_stats, max_over_ranks
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    gpu = local % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")   # collective tensors
     c, name = workload(args)
     E, W, H = c["n_envs"], c["width"], c["height"]
     want_depth = c["depth"]
 
     # ---- inputs: scene replica + pre-generated pose sets, resident in HBM
     scene = gi.config_scene(args.config, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])
-    R = gg.Renderer(local)
+    R = gg.Renderer(gpu)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     sid = R.load_scene(t(scene.means), t(scene.scales), t(scene.quats), t(scene.opacities), t(scene.sh),
                        scene.sh_degree)
@@ -229,7 +238,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clk = ClockSampler(local)
+    clk = ClockSampler(gpu)
     clk.start()
     time.sleep(0.3)
     launches0 = gg.gg_launch_count(R.ctx)
@@ -253,7 +262,7 @@ def main():
     gg.gg_checksum(R.ctx, E, W, H, rgb, 0, depth, dig, stream)
     torch.cuda.synchronize()
     digest = fold_digests([int(x) & 0xFFFFFFFFFFFFFFFF for x in dig.cpu().tolist()])
-    frames_total, tmax_ns, digests = gather_stats(E * args.steps, digest, int(elapsed_ms * 1e6), dev)
+    frames_total, tmax_ns, digests = gather_stats(E * args.steps, digest, int(elapsed_ms * 1e6), cdev)
     tmax_ms = tmax_ns / 1e6
     value = frames_total / (tmax_ms / 1000.0)
     stage_ms = stage / args.steps          # per step, this rank
@@ -275,7 +284,7 @@ def main():
         for k in range(ke):
             gg.gg_render_host(R.ctx, E, h_ids, h_vm[k % len(h_vm)], h_in, W, H, None, h_rgb, h_depth, None, stream)
         torch.cuda.synchronize()
-        dt = max_over_ranks(time.perf_counter() - t0, dev)
+        dt = max_over_ranks(time.perf_counter() - t0, cdev)
         h2d = E * (4 + 64 + 16)
         d2h = E * W * H * (3 + (4 if want_depth else 0))
         e2e = {"value": E * world * ke / dt, "unit": UNIT, "h2d_bytes_per_step": h2d * world,

@@ -67,6 +67,7 @@ def lib():
         L.or_scene_cov3.argtypes = [vp, fp, dp]
         L.or_sh_basis.argtypes = [C.c_int32, dp, dp]
         L.or_num_threads.restype = C.c_int
+        L.or_set_threads.argtypes = [C.c_int]
         L.or_render_env.restype = vp
         L.or_render_env.argtypes = [vp, fp, fp, C.c_int32, C.c_int32, C.POINTER(_Opts)]
         L.or_result_len.restype = C.c_int64
@@ -174,3 +175,12 @@ def sh_basis(degree: int, direction) -> np.ndarray:
 
 def num_threads() -> int:
     return int(lib().or_num_threads())
+
+
+def use_all_cores() -> int:
+    """Run the oracle on every host core available to this process (torchrun
+    sets OMP_NUM_THREADS=1 per rank; the CPU baseline must not inherit that)."""
+    import os
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    lib().or_set_threads(n)
+    return num_threads()

@@ -348,6 +348,14 @@ void or_scene_cov3(const void* s, float* out32, double* out64) {
 
 void or_sh_basis(int32_t d, const double* dir, double* out) { sh_basis(d, dir[0], dir[1], dir[2], out); }
 
+void or_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int or_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();
