@@ -138,6 +138,28 @@ gg_status gg_render_host(gg_context* ctx, int32_t n_envs, const int32_t* scene_i
                          const gg_render_opts* opts, void* rgb, float* depth, float* alpha,
                          void* stream);
 
+/* Motion blur (§3.3 "rendering a small set of frames offset
+ * along the camera's velocity direction and alpha-blending them into a
+ * single image"; SPEC.md:221-229 render_with_motion_blur).  Readings
+ * (R32-R34): sample times t_i = shutter*((i+0.5)/K - 0.5),
+ * i = 0..K-1; sample pose i rotates the camera about its centre by the
+ * axis-angle vector ang_vel*t_i (world frame) and moves the centre by
+ * lin_vel*t_i (world frame, m/s); the K renders are averaged in linear f32
+ * colour before quantisation as m = x_0 + (sum_{i>=1} (x_i - x_0)) / K (so K=1
+ * and zero velocity reproduce the static render bit-exactly); alpha is
+ * averaged the same way; depth is taken from sample floor(K/2).
+ *   lin_vel, ang_vel  DEVICE f32 [E,3]; shutter >= 0 seconds; K in 1..64
+ * Other arguments and outputs as gg_render. */
+gg_status gg_render_blur(gg_context* ctx, int32_t n_envs, const int32_t* scene_ids, const float* viewmats,
+                         const float* intrinsics, const float* lin_vel, const float* ang_vel, float shutter,
+                         int32_t K, int32_t width, int32_t height, const gg_render_opts* opts, void* rgb,
+                         float* depth, float* alpha, void* stream);
+
+/* The K sample view matrices gg_render_blur renders: DEVICE f32 [E,K,4,4]
+ * (bottom row 0,0,0,1).  Exposed for tests. */
+gg_status gg_blur_poses(gg_context* ctx, int32_t n_envs, const float* viewmats, const float* lin_vel,
+                        const float* ang_vel, float shutter, int32_t K, float* out_viewmats, void* stream);
+
 /* Deterministic 64-bit digest per env of the outputs just rendered
  * (rgb bytes and depth bits), written to DEVICE uint64 [E] on stream.
  * Used for cross-GPU / batch-composition determinism checks. */

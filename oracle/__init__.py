@@ -184,3 +184,62 @@ def use_all_cores() -> int:
     n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     lib().or_set_threads(n)
     return num_threads()
+
+
+# ---------------------------------------------------------------- motion blur
+# SPEC.md:221-229 render_with_motion_blur; §3.3.  Readings
+# R32-R34: t_i = shutter ((i + 0.5)/K - 0.5); sample pose i
+# rotates the camera about its centre by the world-frame axis-angle vector
+# w t_i and moves the centre by v t_i; uniform 1/K average of the linear
+# colours (and alphas); depth from sample floor(K/2).
+
+def _rodrigues(rv):
+    rv = np.asarray(rv, np.float64)
+    th = float(np.linalg.norm(rv))
+    if th == 0.0:
+        return np.eye(3)
+    k = rv / th
+    Kx = np.array([[0.0, -k[2], k[1]], [k[2], 0.0, -k[0]], [-k[1], k[0], 0.0]])
+    return np.eye(3) + np.sin(th) * Kx + (1.0 - np.cos(th)) * (Kx @ Kx)
+
+
+def blur_poses(viewmat, lin_vel, ang_vel, shutter: float, K: int) -> np.ndarray:
+    """The K sample view matrices [K,4,4] (f64) of one camera."""
+    V = np.asarray(viewmat, np.float64).reshape(4, 4)
+    Rcw, t = V[:3, :3], V[:3, 3]
+    C = -Rcw.T @ t
+    v = np.asarray(lin_vel, np.float64)
+    w = np.asarray(ang_vel, np.float64)
+    out = np.zeros((K, 4, 4))
+    for i in range(K):
+        ti = float(np.float32(shutter)) * ((i + 0.5) / K - 0.5)
+        Rwc = _rodrigues(w * ti) @ Rcw.T
+        Ci = C + v * ti
+        out[i, :3, :3] = Rwc.T
+        out[i, :3, 3] = -Rwc.T @ Ci
+        out[i, 3, 3] = 1.0
+    return out
+
+
+@dataclass
+class BlurResult:
+    rgb: np.ndarray      # [H,W,3] f64 uniform average of the samples' linear colours
+    rgb8: np.ndarray     # [H,W,3] u8
+    depth: np.ndarray    # [H,W] depth of sample floor(K/2)
+    alpha: np.ndarray    # [H,W] average alpha
+    exempt: np.ndarray   # [H,W] any sample's near-miss flag
+    depth_alpha: np.ndarray   # [H,W] alpha of the depth's sample
+    samples: list
+
+
+def render_blur_env(scene: OracleScene, viewmat, intr, width: int, height: int, lin_vel, ang_vel,
+                    shutter: float, K: int, **kw) -> BlurResult:
+    if K < 1:
+        raise ValueError("K must be >= 1 (SPEC.md:226)")
+    poses = blur_poses(viewmat, lin_vel, ang_vel, shutter, K)
+    samples = [render_env(scene, np.float32(p), intr, width, height, **kw) for p in poses]
+    rgb = np.mean([s.rgb for s in samples], axis=0)
+    alpha = np.mean([s.alpha for s in samples], axis=0)
+    rgb8 = np.rint(np.clip(rgb, 0.0, 1.0) * 255.0).astype(np.uint8)   # numpy rint = half-to-even
+    exempt = np.any([s.exempt for s in samples], axis=0)
+    return BlurResult(rgb, rgb8, samples[K // 2].depth, alpha, exempt, samples[K // 2].alpha, samples)

@@ -28,7 +28,7 @@ GG_COUNTERS = 2
 
 # every symbol include/gg.h declares
 EXPORTS = ["gg_default_opts", "gg_create", "gg_destroy", "gg_load_scene", "gg_unload_scene", "gg_reserve",
-           "gg_render", "gg_render_host", "gg_checksum", "gg_check_errors", "gg_debug_dump", "gg_get_counters",
+           "gg_render", "gg_render_host", "gg_render_blur", "gg_blur_poses", "gg_checksum", "gg_check_errors", "gg_debug_dump", "gg_get_counters",
            "gg_launch_count", "gg_set_timing", "gg_get_stage_ms", "gg_last_error", "gg_status_string"]
 
 
@@ -75,6 +75,9 @@ def load_library(path: str = LIB_PATH):
     L.gg_reserve.argtypes = [vp, i32, i32, i32, i32]
     L.gg_render.argtypes = [vp, i32, vp, vp, vp, i32, i32, C.POINTER(gg_render_opts), vp, vp, vp, vp]
     L.gg_render_host.argtypes = [vp, i32, vp, vp, vp, i32, i32, C.POINTER(gg_render_opts), vp, vp, vp, vp]
+    L.gg_render_blur.argtypes = [vp, i32, vp, vp, vp, vp, vp, C.c_float, i32, i32, i32, C.POINTER(gg_render_opts),
+                                 vp, vp, vp, vp]
+    L.gg_blur_poses.argtypes = [vp, i32, vp, vp, vp, C.c_float, i32, vp, vp]
     L.gg_checksum.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp, vp]
     L.gg_check_errors.argtypes = [vp, vp]
     L.gg_debug_dump.argtypes = [vp, i32, vp, i64, C.POINTER(i64)]
@@ -201,6 +204,20 @@ def gg_render_host(ctx, n_envs, scene_ids, viewmats, intrinsics, width, height, 
     _check(ctx, load_library().gg_render_host(ctx, int(n_envs), _ptr(scene_ids), _ptr(viewmats), _ptr(intrinsics),
                                               int(width), int(height), C.byref(o), _ptr(rgb), _ptr(depth),
                                               _ptr(alpha), _stream_handle(stream)))
+
+
+def gg_render_blur(ctx, n_envs, scene_ids, viewmats, intrinsics, lin_vel, ang_vel, shutter, K, width, height,
+                   opts=None, rgb=None, depth=None, alpha=None, stream=None):
+    o = opts if opts is not None else default_opts()
+    _check(ctx, load_library().gg_render_blur(ctx, int(n_envs), _ptr(scene_ids), _ptr(viewmats), _ptr(intrinsics),
+                                              _ptr(lin_vel), _ptr(ang_vel), float(shutter), int(K), int(width),
+                                              int(height), C.byref(o), _ptr(rgb), _ptr(depth), _ptr(alpha),
+                                              _stream_handle(stream)))
+
+
+def gg_blur_poses(ctx, n_envs, viewmats, lin_vel, ang_vel, shutter, K, out, stream=None):
+    _check(ctx, load_library().gg_blur_poses(ctx, int(n_envs), _ptr(viewmats), _ptr(lin_vel), _ptr(ang_vel),
+                                             float(shutter), int(K), _ptr(out), _stream_handle(stream)))
 
 
 def gg_checksum(ctx, n_envs, width, height, rgb, rgb_format, depth, out, stream=None):

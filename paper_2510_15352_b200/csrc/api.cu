@@ -37,6 +37,12 @@ int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, c
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s);
+void launch_blur_poses(int E, int K, const float* viewmats, const float* lin, const float* ang, float shutter,
+                       float* out, cudaStream_t s);
+void launch_blur_average(int ec, int e0, int K, size_t P, const float* srgb, const float* sdepth,
+                         const float* salpha, int rgb_format, void* rgb, float* depth, float* alpha, cudaStream_t s);
+void launch_blur_expand(int ec, int K, const int32_t* ids, const float* intr, int32_t* ids_k, float* intr_k,
+                        cudaStream_t s);
 void launch_checksum(int E, int W, int H, const uint8_t* rgb8, const float* rgbf, const float* depth,
                      unsigned long long* out, cudaStream_t s);
 void launch_debug_records(uint32_t V, uint64_t rb, const ChunkWS& ws, int32_t* tile_counts, float* proj,
@@ -81,6 +87,7 @@ struct gg_context {
   DevBuf sorted, ranges, counters, valid_out, perm, groups, blkbase, ghist, thist;
   DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval, dconic;
   DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
+  DevBuf blur_vm, blur_ids, blur_intr, blur_rgb, blur_depth, blur_alpha;   // gg_render_blur
   // pinned host mirrors
   uint32_t* h_vcnt = nullptr;
   uint32_t* h_kcnt = nullptr;
@@ -279,7 +286,8 @@ gg_status gg_destroy(gg_context* ctx) {
                    &ctx->blkbase, &ctx->ghist, &ctx->thist,
                    &ctx->sorted, &ctx->ranges, &ctx->counters, &ctx->valid_out,
                    &ctx->dbg_tc, &ctx->dbg_proj, &ctx->dbg_stile, &ctx->dbg_sz, &ctx->dbg_sgid,
-                   &ctx->dbg_neval, &ctx->dconic, &ctx->h_in};
+                   &ctx->dbg_neval, &ctx->dconic, &ctx->h_in, &ctx->blur_vm, &ctx->blur_ids,
+                   &ctx->blur_intr, &ctx->blur_rgb, &ctx->blur_depth, &ctx->blur_alpha};
   for (DevBuf* b : all) dev_free(ctx, *b, s);
   cudaStreamSynchronize(s);
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
@@ -760,6 +768,65 @@ gg_status gg_render_host(gg_context* ctx, int32_t E, const int32_t* scene_ids, c
   if (st != GG_OK) return st;
   CK(cudaStreamSynchronize(ctx->own));
   CK(cudaStreamSynchronize(s));
+  return GG_OK;
+}
+
+gg_status gg_blur_poses(gg_context* ctx, int32_t E, const float* viewmats, const float* lin, const float* ang,
+                        float shutter, int32_t K, float* out, void* stream) {
+  if (!ctx) return GG_E_INVALID;
+  if (E <= 0 || K < 1 || K > 64 || !(shutter >= 0.f) || !viewmats || !lin || !ang || !out)
+    return fail(ctx, GG_E_INVALID, "gg_blur_poses: bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  launch_blur_poses(E, K, viewmats, lin, ang, shutter, out, (cudaStream_t)stream);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return GG_OK;
+}
+
+gg_status gg_render_blur(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
+                         const float* intr, const float* lin, const float* ang, float shutter, int32_t K,
+                         int32_t W, int32_t H, const gg_render_opts* opts_in, void* rgb, float* depth, float* alpha,
+                         void* stream) {
+  if (!ctx) return GG_E_INVALID;
+  if (E <= 0 || W <= 0 || H <= 0 || K < 1 || K > 64 || !(shutter >= 0.f))
+    return fail(ctx, GG_E_INVALID, "gg_render_blur: bad sizes, K or shutter");
+  if (!scene_ids || !viewmats || !intr || !lin || !ang)
+    return fail(ctx, GG_E_INVALID, "gg_render_blur: null input pointer");
+  gg_render_opts opts;
+  if (opts_in) opts = *opts_in; else gg_default_opts(&opts);
+  if (opts.rgb_format != 0 && opts.rgb_format != 1) return fail(ctx, GG_E_INVALID, "gg_render_blur: rgb_format");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t npx = (size_t)W * H;
+  const int ecb = std::max(1, std::min(E, ctx->chunk / K));
+  const size_t nk = (size_t)ecb * K;
+  if (!ensure(ctx, ctx->blur_vm, nk * 64, s) || !ensure(ctx, ctx->blur_ids, nk * 4, s) ||
+      !ensure(ctx, ctx->blur_intr, nk * 16, s) || (rgb && !ensure(ctx, ctx->blur_rgb, nk * npx * 12, s)) ||
+      (depth && !ensure(ctx, ctx->blur_depth, nk * npx * 4, s)) || (alpha && !ensure(ctx, ctx->blur_alpha, nk * npx * 4, s)))
+    return fail(ctx, GG_E_OOM, "gg_render_blur: sample buffers");
+  gg_render_opts sub = opts;
+  sub.rgb_format = 1;   // linear f32 samples, averaged before quantisation
+  sub.flags = 0;
+  sub.debug_env = -1;
+  for (int e0 = 0; e0 < E; e0 += ecb) {
+    const int ec = std::min(ecb, E - e0);
+    launch_blur_poses(ec, K, viewmats + (size_t)e0 * 16, lin + (size_t)e0 * 3, ang + (size_t)e0 * 3, shutter,
+                      P<float>(ctx->blur_vm), s);
+    launch_blur_expand(ec, K, scene_ids + e0, intr + (size_t)e0 * 4, P<int32_t>(ctx->blur_ids),
+                       P<float>(ctx->blur_intr), s);
+    ctx->launches += 2;
+    CK(cudaGetLastError());
+    gg_status st = render_impl(ctx, ec * K, P<int32_t>(ctx->blur_ids), P<float>(ctx->blur_vm),
+                               P<float>(ctx->blur_intr), W, H, &sub, rgb ? ctx->blur_rgb.p : nullptr,
+                               depth ? P<float>(ctx->blur_depth) : nullptr, alpha ? P<float>(ctx->blur_alpha) : nullptr,
+                               s, nullptr, nullptr);
+    if (st != GG_OK) return st;
+    launch_blur_average(ec, e0, K, npx, rgb ? P<float>(ctx->blur_rgb) : nullptr,
+                        depth ? P<float>(ctx->blur_depth) : nullptr, alpha ? P<float>(ctx->blur_alpha) : nullptr,
+                        opts.rgb_format, rgb, depth, alpha, s);
+    ctx->launches++;
+    CK(cudaGetLastError());
+  }
   return GG_OK;
 }
 

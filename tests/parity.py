@@ -29,7 +29,8 @@ def pixel_failures(rgb_gpu, depth_gpu, alpha_gpu, o, rgb_is_u8=True):
         bad = np.zeros(o.alpha.shape, bool)
     if depth_gpu is not None:
         d = depth_gpu.astype(np.float64)
-        pos = o.alpha > 0
+        # the depth's own accumulated alpha (motion blur: the centre sample's)
+        pos = getattr(o, "depth_alpha", o.alpha) > 0
         rel = np.where(pos, np.abs(d - o.depth) / np.where(pos, o.depth, 1.0), 0.0)
         bad |= pos & (rel > DEPTH_RTOL)
         bad |= (~pos) & (d != 0.0)
@@ -56,7 +57,7 @@ class Tally:
             g = rgb_gpu.astype(np.float64) / 255.0 if rgb_is_u8 else rgb_gpu.astype(np.float64)
             self.max_rgb = max(self.max_rgb, float(np.abs(g - np.clip(o.rgb, 0, 1)).max(axis=-1)[ok].max()))
         if depth_gpu is not None:
-            pos = (o.alpha > 0) & ok
+            pos = (getattr(o, "depth_alpha", o.alpha) > 0) & ok
             if pos.any():
                 rel = np.abs(depth_gpu.astype(np.float64)[pos] - o.depth[pos]) / o.depth[pos]
                 self.max_depth_rel = max(self.max_depth_rel, float(rel.max()))
