@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--cpu-envs", type=int, default=4, help="oracle sample size for cpu_baseline")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--blur", type=int, default=0, help="motion blur with K samples (gg_render_blur); 0 = off")
+    p.add_argument("--shutter", type=float, default=0.01, help="shutter time (s) for --blur")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo only to exercise the multi-rank path on a single-GPU box")
     return p.parse_args()
@@ -70,6 +72,8 @@ def workload(args):
         c["sh_degree"] = args.sh
     name = (f"{args.config}: 1 scene x {c['n_gauss']:,} Gaussians SH{c['sh_degree']}, {c['n_envs']} envs/GPU, "
             f"{c['width']}x{c['height']} {'RGB+D' if c['depth'] else 'RGB'}")
+    if getattr(args, "blur", 0):
+        name += f", motion blur K={args.blur} shutter {args.shutter}s"
     return c, name
 
 
@@ -222,8 +226,17 @@ def main():
     depth = torch.empty((E, H, W), dtype=torch.float32, device=dev) if want_depth else None
     stream = torch.cuda.current_stream()
 
+    if args.blur:
+        g = gi.rng(gi.KIND_CAMERAS, 777 + rank)
+        lin_d = t(np.float32(g.normal(0.0, 0.5, (E, 3))))       # m/s (robot base speeds)
+        ang_d = t(np.float32(g.normal(0.0, 1.0, (E, 3))))       # rad/s (stair jolts)
+
     def step(s, **kw):
-        gg.gg_render(R.ctx, E, ids, vm_d[s], intr, W, H, gg.default_opts(**kw), rgb, depth, None, stream)
+        if args.blur:
+            gg.gg_render_blur(R.ctx, E, ids, vm_d[s], intr, lin_d, ang_d, args.shutter, args.blur, W, H,
+                              gg.default_opts(**kw), rgb, depth, None, stream)
+        else:
+            gg.gg_render(R.ctx, E, ids, vm_d[s], intr, W, H, gg.default_opts(**kw), rgb, depth, None, stream)
 
     # ---- counters pass (untimed): n_eval / n_contrib / V / K of pose set 0
     step(0, flags=gg.GG_COUNTERS)
