@@ -239,9 +239,11 @@ def main():
             gg.gg_render(R.ctx, E, ids, vm_d[s], intr, W, H, gg.default_opts(**kw), rgb, depth, None, stream)
 
     # ---- counters pass (untimed): n_eval / n_contrib / V / K of pose set 0
-    step(0, flags=gg.GG_COUNTERS)
+    gg.gg_render(R.ctx, E, ids, vm_d[0], intr, W, H, gg.default_opts(flags=gg.GG_COUNTERS), rgb, depth, None,
+                 stream)
     cnt = gg.gg_get_counters(R.ctx, E)
-    n_eval, n_contrib, n_vis, n_keys = (int(x) for x in cnt.sum(axis=0))
+    kb = max(1, args.blur)     # blur renders K sample frames per env (work scaled by K, static-pose counts)
+    n_eval, n_contrib, n_vis, n_keys = (int(x) * kb for x in cnt.sum(axis=0))
 
     # ---- warm-up + timed region
     gg.gg_set_timing(R.ctx, True)
