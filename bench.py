@@ -322,7 +322,7 @@ def main():
         tr, src = ncu_traffic("raster2_kernel")
         roof = {"kernel": "raster2_kernel (K6)", "bound": "alu", "achieved": ach, "peak": alu_peak,
                 "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": tr,
-                "traffic_note": f"DRAM bytes per launch (one {args.chunk or 512}-env chunk) from {src}" if tr else None,
+                "traffic_note": f"DRAM bytes per launch (one {args.chunk or 1024}-env chunk) from {src}" if tr else None,
                 "peak_basis": f"148 SM x 128 FP32 lanes x 2 (FFMA) x {clock_mhz:.0f} MHz median SM clock under load",
                 "work": f"{n_eval:,} evaluated pairs x {FLOP_EVAL} + {n_contrib:,} blended x {FLOP_CONTRIB} flops"}
     elif names[dom] == "sort_bin":
@@ -354,7 +354,7 @@ def main():
                           "sh_degree": scene.sh_degree, "width": W, "height": H, "depth": want_depth,
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
-                          "chunk_envs": args.chunk or 512},
+                          "chunk_envs": args.chunk or 1024},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clocks,
                "counters": {"n_eval": n_eval, "n_contrib": n_contrib, "visible": n_vis, "keys": n_keys,

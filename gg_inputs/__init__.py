@@ -434,3 +434,31 @@ def config_scene(cfg: str, scene_index: int = 0, n_gauss: int | None = None, sh_
 def config_cameras(cfg: str, scene: Scene, n_envs: int | None = None, index: int = 0) -> Cameras:
     c = CONFIGS[cfg]
     return cameras(index, c["n_envs"] if n_envs is None else n_envs, c["width"], c["height"], scene)
+
+
+# ---------------------------------------------------------------------------
+# 3DGS PLY writer (input construction for the PLY-reader tests): stores the
+# *raw* parameters the 3DGS format holds (log scales, opacity logits,
+# channel-major f_rest).
+# ---------------------------------------------------------------------------
+
+def write_3dgs_ply(path: str, scene: Scene) -> None:
+    import struct
+    n, d = scene.n, scene.sh_degree
+    K = (d + 1) ** 2
+    names = ["x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2"]
+    names += [f"f_rest_{i}" for i in range(3 * (K - 1))]
+    names += ["opacity", "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"]
+    op = np.clip(scene.opacities.astype(np.float64), 1e-7, 1 - 1e-7)
+    cols = [scene.means.astype(np.float64), np.zeros((n, 3)), scene.sh[:, 0, :].astype(np.float64)]
+    rest = scene.sh[:, 1:, :].astype(np.float64).transpose(0, 2, 1).reshape(n, -1)   # channel-major
+    cols += [rest, np.log(op / (1 - op))[:, None], np.log(scene.scales.astype(np.float64)),
+             scene.quats.astype(np.float64)]
+    data = np.concatenate(cols, axis=1).astype("<f4")
+    assert data.shape[1] == len(names)
+    with open(path, "wb") as f:
+        hdr = "ply\nformat binary_little_endian 1.0\nelement vertex %d\n" % n
+        hdr += "".join(f"property float {nm}\n" for nm in names) + "end_header\n"
+        f.write(hdr.encode())
+        f.write(data.tobytes())
+    del struct

@@ -167,6 +167,20 @@ gg_status gg_checksum(gg_context* ctx, int32_t n_envs, int32_t width, int32_t he
                       const void* rgb, int32_t rgb_format, const float* depth, uint64_t* out,
                       void* stream);
 
+/* 3DGS binary PLY scenes (SPEC.md:51-59 load_splat_ply).
+ * gg_read_ply parses `path` into ACTIVATED host arrays (scale = exp,
+ * opacity = sigmoid, quaternion = rot_0..3 as (w,x,y,z), SH reordered from
+ * the file's channel-major f_rest to [n,(d+1)^2,3]).  Call once with null
+ * array pointers to get n and the SH degree, then with caller-allocated
+ * host buffers of those sizes.  Errors: missing property (named), NaN/Inf
+ * (record index), empty or truncated file -> GG_E_INVALID with the reason in
+ * gg_ply_error().  No context or GPU needed.  gg_load_ply = gg_read_ply +
+ * gg_load_scene. */
+gg_status gg_read_ply(const char* path, int64_t* n, int32_t* sh_degree, float* means, float* scales,
+                      float* quats, float* opacities, float* sh);
+gg_status gg_load_ply(gg_context* ctx, const char* path, int32_t* out_scene_id);
+const char* gg_ply_error(void);
+
 /* Synchronise `stream` and return any sticky device-side error. */
 gg_status gg_check_errors(gg_context* ctx, void* stream);
 

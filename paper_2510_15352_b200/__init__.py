@@ -29,7 +29,8 @@ GG_COUNTERS = 2
 # every symbol include/gg.h declares
 EXPORTS = ["gg_default_opts", "gg_create", "gg_destroy", "gg_load_scene", "gg_unload_scene", "gg_reserve",
            "gg_render", "gg_render_host", "gg_render_blur", "gg_blur_poses", "gg_checksum", "gg_check_errors", "gg_debug_dump", "gg_get_counters",
-           "gg_launch_count", "gg_set_timing", "gg_get_stage_ms", "gg_last_error", "gg_status_string"]
+           "gg_launch_count", "gg_set_timing", "gg_get_stage_ms", "gg_last_error", "gg_status_string",
+           "gg_read_ply", "gg_load_ply", "gg_ply_error"]
 
 
 class GGError(RuntimeError):
@@ -90,8 +91,12 @@ def load_library(path: str = LIB_PATH):
     L.gg_last_error.restype = C.c_char_p
     L.gg_status_string.argtypes = [C.c_int]
     L.gg_status_string.restype = C.c_char_p
+    L.gg_read_ply.argtypes = [C.c_char_p, C.POINTER(i64), C.POINTER(i32), vp, vp, vp, vp, vp]
+    L.gg_load_ply.argtypes = [vp, C.c_char_p, C.POINTER(i32)]
+    L.gg_ply_error.argtypes = []
+    L.gg_ply_error.restype = C.c_char_p
     for name in EXPORTS:
-        if name not in ("gg_default_opts", "gg_launch_count", "gg_last_error", "gg_status_string"):
+        if name not in ("gg_default_opts", "gg_launch_count", "gg_last_error", "gg_status_string", "gg_ply_error"):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -258,6 +263,36 @@ def gg_get_stage_ms(ctx) -> tuple[float, float, float]:
     a = (C.c_float * 3)()
     _check(ctx, load_library().gg_get_stage_ms(ctx, a))
     return tuple(a)
+
+
+def gg_read_ply(path: str):
+    """Parse a 3DGS PLY into activated numpy arrays (means, scales, quats, opacities, sh, degree)."""
+    L = load_library()
+    n, d = C.c_int64(0), C.c_int32(0)
+    st = L.gg_read_ply(path.encode(), C.byref(n), C.byref(d), None, None, None, None, None)
+    if st != GG_OK:
+        raise GGError(st, L.gg_ply_error().decode())
+    N, K = n.value, (d.value + 1) ** 2
+    m, s, q = np.zeros((N, 3), np.float32), np.zeros((N, 3), np.float32), np.zeros((N, 4), np.float32)
+    o, sh = np.zeros(N, np.float32), np.zeros((N, K, 3), np.float32)
+    st = L.gg_read_ply(path.encode(), C.byref(n), C.byref(d), m.ctypes.data, s.ctypes.data, q.ctypes.data,
+                       o.ctypes.data, sh.ctypes.data)
+    if st != GG_OK:
+        raise GGError(st, L.gg_ply_error().decode())
+    return m, s, q, o, sh, d.value
+
+
+def gg_load_ply(ctx, path: str) -> int:
+    out = C.c_int32(-1)
+    st = load_library().gg_load_ply(ctx, path.encode(), C.byref(out))
+    if st != GG_OK:
+        msg = load_library().gg_ply_error().decode() or load_library().gg_last_error(ctx).decode()
+        raise GGError(st, msg)
+    return out.value
+
+
+def gg_ply_error() -> str:
+    return load_library().gg_ply_error().decode()
 
 
 def gg_last_error(ctx) -> str:

@@ -66,7 +66,7 @@ struct SceneSlot {
   bool live = false;
 };
 
-constexpr int DEFAULT_CHUNK = 512;
+constexpr int DEFAULT_CHUNK = 1024;
 
 }  // namespace
 

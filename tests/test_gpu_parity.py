@@ -241,3 +241,19 @@ def test_counters_match_oracle(gg, R):
         assert cnt[e, 3] == len(o.sorted_gid)
         assert abs(cnt[e, 0] - o.n_eval.sum()) <= 0.001 * o.n_eval.sum()
         assert abs(cnt[e, 1] - o.n_contrib.sum()) <= 0.001 * o.n_contrib.sum()
+
+
+def test_ply_scene_renders_like_arrays(gg, R, tmp_path):
+    """gg_load_ply (native PLY reader + load) renders bit-identically to
+    loading the reader's activated arrays through gg_load_scene."""
+    sc = gi.random_cloud(900, 200, sh_degree=2)
+    p = tmp_path / "s.ply"
+    gi.write_3dgs_ply(str(p), sc)
+    sid_ply = gg.gg_load_ply(R.ctx, str(p))
+    m, s, q, o, sh, d = gg.gg_read_ply(str(p))
+    sid_arr = gg.gg_load_scene(R.ctx, m.shape[0], d, m, s, q, o, sh)
+    cams = gi.cloud_cameras(900, 2)
+    a = render(gg, R, [sid_ply, sid_ply], cams)
+    b = render(gg, R, [sid_arr, sid_arr], cams)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
