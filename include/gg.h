@@ -51,7 +51,8 @@ typedef struct {
 
 enum {
   GG_KEEP_INTERMEDIATES = 1u, /* keep opts.debug_env's integer artefacts for gg_debug_dump */
-  GG_COUNTERS = 2u            /* accumulate per-env n_eval / n_contrib totals */
+  GG_COUNTERS = 2u,           /* accumulate per-env n_eval / n_contrib totals */
+  GG_ASYNC = 4u               /* sync-free, CUDA-graph-capturable render (needs gg_reserve_async) */
 };
 
 typedef struct {
@@ -104,6 +105,18 @@ gg_status gg_unload_scene(gg_context* ctx, int32_t scene_id);
  * 0 = default).  Optional: gg_render grows the workspace on demand. */
 gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t width, int32_t height,
                      int32_t chunk_envs);
+
+/* Reserve the fixed workspace of the sync-free render mode (opts.flags |=
+ * GG_ASYNC).  Call after loading every scene.  Renders
+ * of up to max_envs envs at exactly width x height then run without any host
+ * synchronisation or allocation, so they can be captured in a CUDA graph.
+ * Capacities per env chunk: records = chunk * max_scene_n * max_visible_frac,
+ * keys = records * keys_per_visible.  Envs are processed in caller order in
+ * groups of 16 (sort envs by scene id for best projection efficiency).  On
+ * overflow that chunk's frames are background and gg_check_errors returns
+ * GG_E_CAPACITY.  Counters (GG_COUNTERS) are supported; intermediates are not. */
+gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t width, int32_t height, int32_t chunk_envs,
+                           float max_visible_frac, float keys_per_visible);
 
 /* Render one frame for each of n_envs environments (SPEC.md:154-162
  * render_batch): env e uses scene scene_ids[e] and the pinhole camera

@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libgg.so")
 GG_OK, GG_E_INVALID, GG_E_NONFINITE, GG_E_OOM, GG_E_CUDA, GG_E_BAD_SCENE, GG_E_CAPACITY, GG_E_UNSUPPORTED = range(8)
 GG_KEEP_INTERMEDIATES = 1
 GG_COUNTERS = 2
+GG_ASYNC = 4
 (GG_DUMP_TILE_COUNTS, GG_DUMP_SORTED_TILE, GG_DUMP_SORTED_ZBITS, GG_DUMP_SORTED_GIDS, GG_DUMP_RANGES,
  GG_DUMP_COUNTERS, GG_DUMP_N_EVAL, GG_DUMP_PROJ) = range(8)
 
@@ -30,7 +31,7 @@ GG_COUNTERS = 2
 EXPORTS = ["gg_default_opts", "gg_create", "gg_destroy", "gg_load_scene", "gg_unload_scene", "gg_reserve",
            "gg_render", "gg_render_host", "gg_render_blur", "gg_blur_poses", "gg_checksum", "gg_check_errors", "gg_debug_dump", "gg_get_counters",
            "gg_launch_count", "gg_set_timing", "gg_get_stage_ms", "gg_last_error", "gg_status_string",
-           "gg_read_ply", "gg_load_ply", "gg_ply_error"]
+           "gg_read_ply", "gg_load_ply", "gg_ply_error", "gg_reserve_async"]
 
 
 class GGError(RuntimeError):
@@ -74,6 +75,7 @@ def load_library(path: str = LIB_PATH):
     L.gg_load_scene.argtypes = [vp, i64, i32, fp, fp, fp, fp, fp, C.POINTER(i32)]
     L.gg_unload_scene.argtypes = [vp, i32]
     L.gg_reserve.argtypes = [vp, i32, i32, i32, i32]
+    L.gg_reserve_async.argtypes = [vp, i32, i32, i32, i32, C.c_float, C.c_float]
     L.gg_render.argtypes = [vp, i32, vp, vp, vp, i32, i32, C.POINTER(gg_render_opts), vp, vp, vp, vp]
     L.gg_render_host.argtypes = [vp, i32, vp, vp, vp, i32, i32, C.POINTER(gg_render_opts), vp, vp, vp, vp]
     L.gg_render_blur.argtypes = [vp, i32, vp, vp, vp, vp, vp, C.c_float, i32, i32, i32, C.POINTER(gg_render_opts),
@@ -193,6 +195,12 @@ def gg_unload_scene(ctx, scene_id: int):
 
 def gg_reserve(ctx, max_envs: int, width: int, height: int, chunk_envs: int = 0):
     _check(ctx, load_library().gg_reserve(ctx, max_envs, width, height, chunk_envs))
+
+
+def gg_reserve_async(ctx, max_envs: int, width: int, height: int, chunk_envs: int = 0,
+                     max_visible_frac: float = 0.6, keys_per_visible: float = 4.0):
+    _check(ctx, load_library().gg_reserve_async(ctx, max_envs, width, height, chunk_envs, max_visible_frac,
+                                                keys_per_visible))
 
 
 def gg_render(ctx, n_envs, scene_ids, viewmats, intrinsics, width, height, opts=None, rgb=None, depth=None,

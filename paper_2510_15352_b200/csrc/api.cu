@@ -30,6 +30,7 @@ void launch_project(int e0, int ngroups, int nblk, int max_degree, const EnvGrou
 cudaError_t project_init();
 cudaError_t sort_bin_init();
 uint32_t sort_blocks(uint32_t V);
+int sort_block_size();
 size_t sort_ghist_words();
 int depth_passes(uint32_t span);
 int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, const RenderParams& rp,
@@ -43,6 +44,10 @@ void launch_blur_average(int ec, int e0, int K, size_t P, const float* srgb, con
                          const float* salpha, int rgb_format, void* rgb, float* depth, float* alpha, cudaStream_t s);
 void launch_blur_expand(int ec, int K, const int32_t* ids, const float* intr, int32_t* ids_k, float* intr_k,
                         cudaStream_t s);
+void launch_tables_v(int ec, const uint32_t* vcnt, uint64_t* rbase, uint64_t vcap, uint32_t* ok, uint32_t* err,
+                     cudaStream_t s);
+void launch_tables_k(int ec, const uint32_t* vcnt, const uint32_t* kcnt, uint64_t* kbase, uint32_t* blkbase,
+                     int sort_blk, uint64_t kcap, uint64_t nbcap, uint32_t* ok, uint32_t* err, cudaStream_t s);
 void launch_checksum(int E, int W, int H, const uint8_t* rgb8, const float* rgbf, const float* depth,
                      unsigned long long* out, cudaStream_t s);
 void launch_debug_records(uint32_t V, uint64_t rb, const ChunkWS& ws, int32_t* tile_counts, float* proj,
@@ -111,6 +116,13 @@ struct gg_context {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_copy = nullptr;
   int last_E = 0;
+  // sync-free mode (gg_reserve_async)
+  bool async_ready = false;
+  int a_max_envs = 0, a_W = 0, a_H = 0, a_chunk = 0, a_nblk = 0, a_maxdeg = 0;
+  uint64_t a_vcap = 0, a_kcap = 0, a_nbcap = 0;
+  DevBuf okflag;
+  std::vector<cudaEvent_t> a_ev;   // per-chunk stage events (timing only)
+  int a_nchunks = 0;
 };
 
 namespace {
@@ -280,7 +292,8 @@ gg_status gg_destroy(gg_context* ctx) {
     dev_free(ctx, sc.pos_op, s); dev_free(ctx, sc.cov_a, s); dev_free(ctx, sc.cov_b, s);
     dev_free(ctx, sc.aux, s); dev_free(ctx, sc.sh, s);
   }
-  DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->zmm, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
+  for (auto& e : ctx->a_ev) cudaEventDestroy(e);
+  DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->zmm, &ctx->okflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
                    &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect,
                    &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->perm, &ctx->groups,
                    &ctx->blkbase, &ctx->ghist, &ctx->thist,
@@ -449,6 +462,18 @@ gg_status gg_set_timing(gg_context* ctx, int32_t en) {
 
 gg_status gg_get_stage_ms(gg_context* ctx, float* out3) {
   if (!ctx || !out3) return GG_E_INVALID;
+  if (ctx->a_nchunks > 0) {   // async-mode events: resolve now (synchronises)
+    float ms[3] = {0, 0, 0};
+    CK(cudaEventSynchronize(ctx->a_ev[ctx->a_nchunks * 4 - 1]));
+    for (int c = 0; c < ctx->a_nchunks; ++c)
+      for (int k = 0; k < 3; ++k) {
+        float x = 0;
+        cudaEventElapsedTime(&x, ctx->a_ev[c * 4 + k], ctx->a_ev[c * 4 + k + 1]);
+        ms[k] += x;
+      }
+    for (int k = 0; k < 3; ++k) ctx->stage_ms[k] = ms[k];
+    ctx->a_nchunks = 0;
+  }
   for (int i = 0; i < 3; ++i) out3[i] = ctx->stage_ms[i];
   return GG_OK;
 }
@@ -557,6 +582,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ws.zmax = P<uint32_t>(ctx->zmm) + chunk;
     ws.nwords = nwords;
     ws.nblk = nblk;
+    ws.ec = ec;
     const EnvGroup* groups = P<EnvGroup>(ctx->groups);
     CK(cudaMemsetAsync(ws.zmin, 0xff, ec * 4, s));
     CK(cudaMemsetAsync(ws.zmax, 0, ec * 4, s));
@@ -699,10 +725,158 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   return GG_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Sync-free mode (GG_ASYNC): fixed, pre-reserved workspace; every offset
+// table is built on the device (async.cu), grids have fixed sizes, envs are
+// taken in caller order in fixed groups of 16 (mixed scenes allowed), the
+// number of depth passes follows from [near, far].  No host synchronisation
+// and no allocation: the call can be captured in a CUDA graph.  Capacity
+// overflow marks the chunk invalid and raises a sticky GG_E_CAPACITY.
+static int depth_passes_for(float near_p, float far_p) {
+  uint32_t a, b;
+  memcpy(&a, &near_p, 4);
+  memcpy(&b, &far_p, 4);
+  return depth_passes(b - a);
+}
+
+static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
+                              const float* intr, int32_t W, int32_t H, const gg_render_opts& opts, void* rgb,
+                              float* depth, float* alpha, cudaStream_t s) {
+  if (!ctx->async_ready) return fail(ctx, GG_E_INVALID, "GG_ASYNC: call gg_reserve_async first");
+  if (E > ctx->a_max_envs || W != ctx->a_W || H != ctx->a_H)
+    return fail(ctx, GG_E_CAPACITY, "GG_ASYNC: render (%d envs, %dx%d) exceeds the reservation (%d, %dx%d)", E, W, H,
+                ctx->a_max_envs, ctx->a_W, ctx->a_H);
+  if (opts.flags & GG_KEEP_INTERMEDIATES) return fail(ctx, GG_E_UNSUPPORTED, "GG_ASYNC: no intermediates");
+  if ((opts.flags & GG_COUNTERS) && ctx->counters.bytes < (size_t)E * 32)
+    return fail(ctx, GG_E_CAPACITY, "GG_ASYNC: counters not reserved");
+  const int TX = (W + TILE - 1) / TILE, TY = (H + TILE - 1) / TILE;
+  RenderParams rp;
+  rp.W = W; rp.H = H; rp.TX = TX; rp.TY = TY; rp.ntiles = TX * TY;
+  rp.near_p = opts.near_plane; rp.far_p = opts.far_plane;
+  rp.bg[0] = opts.background[0]; rp.bg[1] = opts.background[1]; rp.bg[2] = opts.background[2];
+  rp.rgb_format = opts.rgb_format;
+  const bool counters = (opts.flags & GG_COUNTERS) != 0;
+  const int chunk = ctx->a_chunk, nblk = ctx->a_nblk, nwords = nblk * (PROJ_BLOCK / 32);
+  if (nblk < (max_scene_n(ctx) + PROJ_BLOCK - 1) / PROJ_BLOCK)
+    return fail(ctx, GG_E_CAPACITY, "GG_ASYNC: a scene larger than at gg_reserve_async time was loaded");
+  const int passes = depth_passes_for(opts.near_plane, opts.far_plane);
+  uint32_t* err = P<uint32_t>(ctx->errflag);
+  uint32_t* ok = P<uint32_t>(ctx->okflag);
+  if (counters) CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)E * 32, s));
+  launch_setup_envs(E, nullptr, scene_ids, viewmats, intr, P<DevScene>(ctx->scene_table), (int)ctx->scenes.size(), W,
+                    H, opts.sh_degree, P<EnvConst>(ctx->envc), err, s);
+  ctx->launches++;
+  const int nchunks = (E + chunk - 1) / chunk;
+  if (ctx->timing) {
+    while ((int)ctx->a_ev.size() < nchunks * 4) {
+      cudaEvent_t ev;
+      CK(cudaEventCreate(&ev));
+      ctx->a_ev.push_back(ev);
+    }
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    const int e0 = c * chunk, ec = std::min(chunk, E - e0);
+    const int ngroups = (ec + ENV_GROUP - 1) / ENV_GROUP;
+    ChunkWS ws{};
+    ws.flags = P<uint32_t>(ctx->flags);
+    ws.blkcnt = P<uint32_t>(ctx->blkcnt);
+    ws.vcnt = P<uint32_t>(ctx->vcnt);
+    ws.kcnt = P<uint32_t>(ctx->kcnt);
+    ws.rec_base = P<uint64_t>(ctx->rbase);
+    ws.k_base = P<uint64_t>(ctx->kbase);
+    ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
+    ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
+    ws.zmin = P<uint32_t>(ctx->zmm); ws.zmax = P<uint32_t>(ctx->zmm) + chunk;
+    ws.dk0 = P<uint32_t>(ctx->dk0); ws.dv0 = P<uint32_t>(ctx->dv0);
+    ws.dk1 = P<uint32_t>(ctx->dk1); ws.dv1 = P<uint32_t>(ctx->dv1);
+    ws.sorted = P<uint32_t>(ctx->sorted);
+    ws.ranges = P<uint2>(ctx->ranges);
+    ws.ok = ok;
+    ws.nwords = nwords;
+    ws.nblk = nblk;
+    ws.ec = ec;
+    if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 0], s));
+    CK(cudaMemsetAsync(ws.kcnt, 0, ec * 4, s));
+    CK(cudaMemsetAsync(ws.zmin, 0xff, ec * 4, s));
+    CK(cudaMemsetAsync(ws.zmax, 0, ec * 4, s));
+    CK(cudaMemsetAsync(ok, 0x01, 4, s));
+    launch_cull_count(e0, ngroups, nblk, nullptr, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
+    launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
+    launch_tables_v(ec, ws.vcnt, P<uint64_t>(ctx->rbase), ctx->a_vcap, ok, err, s);
+    launch_project(e0, ngroups, nblk, ctx->a_maxdeg, nullptr, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table),
+                   rp, ws, s);
+    launch_tables_k(ec, ws.vcnt, ws.kcnt, P<uint64_t>(ctx->kbase), P<uint32_t>(ctx->blkbase), sort_block_size(),
+                    ctx->a_kcap, ctx->a_nbcap, ok, err, s);
+    ctx->launches += 5;
+    if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 1], s));
+    ctx->launches += launch_sort_bin(ec, (uint32_t)ctx->a_nbcap, P<uint32_t>(ctx->blkbase), passes, rp, ws,
+                                     P<uint32_t>(ctx->ghist), P<uint32_t>(ctx->thist), s);
+    if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 2], s));
+    launch_raster(e0, ec, P<EnvConst>(ctx->envc), rp, ws, rgb, depth, alpha, counters,
+                  counters ? P<unsigned long long>(ctx->counters) : nullptr, nullptr, -1, s);
+    ctx->launches++;
+    if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 3], s));
+    CK(cudaGetLastError());
+  }
+  ctx->a_nchunks = ctx->timing ? nchunks : 0;
+  ctx->last_E = E;
+  return GG_OK;
+}
+
+gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t H, int32_t chunk,
+                           float max_visible_frac, float keys_per_visible) {
+  if (!ctx) return GG_E_INVALID;
+  if (max_envs <= 0 || W <= 0 || H <= 0 || chunk < 0 || !(max_visible_frac > 0.f) || max_visible_frac > 1.f ||
+      !(keys_per_visible > 0.f))
+    return fail(ctx, GG_E_INVALID, "gg_reserve_async: bad arguments");
+  if (ctx->scenes.empty()) return fail(ctx, GG_E_INVALID, "gg_reserve_async: load the scenes first");
+  const int TX = (W + TILE - 1) / TILE, TY = (H + TILE - 1) / TILE, ntiles = TX * TY;
+  if (ntiles > MAX_TILES) return fail(ctx, GG_E_UNSUPPORTED, "gg_reserve_async: image too large");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->own;
+  const int ch = std::min(max_envs, chunk > 0 ? chunk : ctx->chunk);
+  const int nmax = std::max(max_scene_n(ctx), 1);
+  const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
+  int maxdeg = 0;
+  for (const auto& sc : ctx->scenes)
+    if (sc.live) maxdeg = std::max(maxdeg, sc.d.degree);
+  const uint64_t vcap = (uint64_t)((double)ch * nmax * max_visible_frac) + 1;
+  const uint64_t kcap = (uint64_t)((double)vcap * keys_per_visible) + 1;
+  const uint64_t nbcap = vcap / (uint64_t)sort_block_size() + ch + 1;
+  bool okb = ensure(ctx, ctx->envc, sizeof(EnvConst) * max_envs, s) &&
+             ensure(ctx, ctx->flags, (size_t)ch * nblk * 8 * 4, s) && ensure(ctx, ctx->blkcnt, (size_t)ch * nblk * 4, s) &&
+             ensure(ctx, ctx->vcnt, ch * 4, s) && ensure(ctx, ctx->kcnt, ch * 4, s) && ensure(ctx, ctx->rbase, ch * 8, s) &&
+             ensure(ctx, ctx->kbase, ch * 8, s) && ensure(ctx, ctx->zmm, (size_t)ch * 8, s) &&
+             ensure(ctx, ctx->ranges, (size_t)ch * ntiles * 8, s) && ensure(ctx, ctx->okflag, 16, s) &&
+             ensure(ctx, ctx->counters, (size_t)max_envs * 32, s) && ensure(ctx, ctx->rec0, vcap * 16, s) &&
+             ensure(ctx, ctx->rec1, vcap * 16, s) && ensure(ctx, ctx->rec2, vcap * 16, s) &&
+             ensure(ctx, ctx->rect, vcap * 8, s) && ensure(ctx, ctx->zkey, vcap * 4, s) &&
+             ensure(ctx, ctx->dk0, vcap * 4, s) && ensure(ctx, ctx->dv0, vcap * 4, s) &&
+             ensure(ctx, ctx->dk1, vcap * 4, s) && ensure(ctx, ctx->dv1, vcap * 4, s) &&
+             ensure(ctx, ctx->sorted, kcap * 4, s) && ensure(ctx, ctx->blkbase, (size_t)(ch + 1) * 4, s) &&
+             ensure(ctx, ctx->ghist, nbcap * sort_ghist_words() * 4, s) &&
+             ensure(ctx, ctx->thist, nbcap * ntiles * 4, s);
+  CK(cudaStreamSynchronize(s));
+  if (!okb) return fail(ctx, GG_E_OOM, "gg_reserve_async: allocation failed (%llu records, %llu keys)",
+                        (unsigned long long)vcap, (unsigned long long)kcap);
+  ctx->a_max_envs = max_envs; ctx->a_W = W; ctx->a_H = H; ctx->a_chunk = ch; ctx->a_nblk = nblk;
+  ctx->a_maxdeg = maxdeg; ctx->a_vcap = vcap; ctx->a_kcap = kcap; ctx->a_nbcap = nbcap;
+  ctx->async_ready = true;
+  return GG_OK;
+}
+
 gg_status gg_render(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
                     const float* intr, int32_t W, int32_t H, const gg_render_opts* opts, void* rgb,
                     float* depth, float* alpha, void* stream) {
   if (!ctx) return GG_E_INVALID;
+  if (opts && (opts->flags & GG_ASYNC)) {
+    if (E <= 0 || !scene_ids || !viewmats || !intr || (opts->rgb_format != 0 && opts->rgb_format != 1) ||
+        !(opts->near_plane > 0.f) || !(opts->far_plane > opts->near_plane) || opts->sh_degree > 3)
+      return fail(ctx, GG_E_INVALID, "gg_render: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    return render_async(ctx, E, scene_ids, viewmats, intr, W, H, *opts, rgb, depth, alpha, (cudaStream_t)stream);
+  }
   return render_impl(ctx, E, scene_ids, viewmats, intr, W, H, opts, rgb, depth, alpha,
                      (cudaStream_t)stream, nullptr, nullptr);
 }

@@ -77,8 +77,24 @@ struct ChunkWS {
   uint32_t* dk0; uint32_t* dv0; uint32_t* dk1; uint32_t* dv1;
   uint32_t* sorted;     // [K] final record-local indices, tile-major
   uint2* ranges;        // [Ec][ntiles] [start,end) relative to k_base[e]
+  const uint32_t* ok;   // chunk validity (async mode: 0 after a capacity overflow); null = always valid
   int nwords, nblk;
+  int ec;               // envs in this chunk
 };
+
+// A group of envs for the Gaussian-major projection kernels: explicit table
+// (sync mode, scene-sorted) or, when the table is null, the fixed groups
+// [16 g, 16 g + 16) of the chunk (async mode).  Envs of one group may be
+// bound to different scenes; the kernels reload a Gaussian per scene change.
+__device__ __forceinline__ EnvGroup group_of(const EnvGroup* groups, int g, int ec) {
+  if (groups) return groups[g];
+  EnvGroup r;
+  r.elo = g * ENV_GROUP;
+  r.cnt = min(ENV_GROUP, ec - r.elo);
+  return r;
+}
+
+__device__ __forceinline__ bool chunk_ok(const uint32_t* ok) { return ok == nullptr || *ok != 0u; }
 
 // gg_load_scene validation: first offending record per class (atomicMin)
 struct ValidateOut {

@@ -116,23 +116,28 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
                   const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
   __shared__ EnvConst cams[ENV_GROUP];
   __shared__ uint32_t wc[ENV_GROUP][PROJ_BLOCK / 32];
-  const EnvGroup grp = groups[blockIdx.x];
+  const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
+  if (grp.cnt <= 0) return;
   load_group_cams(cams, envs, e0, grp);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.y * PROJ_BLOCK + threadIdx.x;
-  const int n = cams[0].n;
+  int cur = -2;                       // scene whose Gaussian i is in registers
   float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
   float smax2 = 0.f;
-  if (i < n) {
-    const DevScene& sc = scenes[cams[0].scene];
-    g = __ldg(&sc.pos_op[i]);
-    smax2 = __ldg(&sc.aux[i]).y;
-  }
   const int wi = blockIdx.y * (PROJ_BLOCK / 32) + warp;
   for (int k = 0; k < grp.cnt; ++k) {
+    const EnvConst& c = cams[k];
+    if (c.scene != cur) {             // uniform across the CTA
+      cur = c.scene;
+      if (i < c.n) {
+        const DevScene& sc = scenes[c.scene];
+        g = __ldg(&sc.pos_op[i]);
+        smax2 = __ldg(&sc.aux[i]).y;
+      }
+    }
     uint32_t zb = 0;
-    const bool keep = i < n && maybe_visible(cams[k], g, smax2, rp, zb);
+    const bool keep = i < c.n && maybe_visible(c, g, smax2, rp, zb);
     const uint32_t word = __ballot_sync(0xffffffffu, keep);
     // depth-key range of the kept records (= the env's record set): sort key offset
     const uint32_t zmn = __reduce_min_sync(0xffffffffu, keep ? zb : 0xffffffffu);
@@ -236,7 +241,8 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
                const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ProjSmem& sm = *reinterpret_cast<ProjSmem*>(smem_raw);
-  const EnvGroup grp = groups[blockIdx.x];
+  const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
+  if (grp.cnt <= 0 || !chunk_ok(ws.ok)) return;
   const int tid = threadIdx.x;
   const int gblk = blockIdx.y;
   const int i0 = gblk * PROJ_BLOCK;
@@ -282,11 +288,16 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     }
   }
   // stage the block's Gaussians (visible in at least one env of the group)
-  const EnvConst& c0 = sm.cams[0];
-  const DevScene& sc = scenes[c0.scene];
+  // stage the block's Gaussians of the group's first valid scene; envs of
+  // another scene (mixed groups, async mode) read theirs from global memory
+  int st_k = 0;
+  while (st_k < grp.cnt - 1 && sm.cams[st_k].scene < 0) ++st_k;
+  const EnvConst& c0 = sm.cams[st_k];
+  const int st_scene = c0.scene;
+  const DevScene& sc = scenes[st_scene < 0 ? 0 : st_scene];
   const int deg = c0.degree;
   const int K = (deg + 1) * (deg + 1);
-  {
+  if (st_scene >= 0) {
     const int i = i0 + tid;
     if (i < c0.n) {
       sm.pos[tid] = __ldg(&sc.pos_op[i]);
@@ -318,9 +329,12 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     const int eloc = grp.elo + k;
     const uint32_t rank = s - sm.cnt[k * 8];
     const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + rank;
-    const float4 g = sm.pos[l];
-    const float4 ca = sm.ca[l];
-    const float4 cb = sm.cb[l];
+    const bool staged = c.scene == st_scene;
+    const DevScene& scn = scenes[c.scene];
+    const int gi = i0 + l;
+    const float4 g = staged ? sm.pos[l] : __ldg(&scn.pos_op[gi]);
+    const float4 ca = staged ? sm.ca[l] : __ldg(&scn.cov_a[gi]);
+    const float4 cb = staged ? sm.cb[l] : __ldg(&scn.cov_b[gi]);
     // O2.1 p = R mu + t, 1/z (canonical)
     const float3 p = to_cam(c, g);
     const float rz = fd(1.f, p.z);
@@ -373,21 +387,32 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     const uint32_t ntiles = (x1 - x0) * (y1 - y0);
     // O2.8 colour
     float col[3];
-    if (deg == 0) {
-      col[0] = cb.z; col[1] = cb.w; col[2] = sm.dcb[l];
+    const int cdeg = c.degree;
+    if (cdeg == 0) {
+      col[0] = cb.z; col[1] = cb.w; col[2] = staged ? sm.dcb[l] : __ldg(&scn.aux[gi]).x;
     } else {
       float dx = g.x - c.C[0], dy = g.y - c.C[1], dz = g.z - c.C[2];
       const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
       dx *= inv; dy *= inv; dz *= inv;
       float Y[16];
-      sh_eval(deg, dx, dy, dz, Y);
+      sh_eval(cdeg, dx, dy, dz, Y);
+      const int Kc = (cdeg + 1) * (cdeg + 1);
       float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+      if (staged) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        if (q < K) {
-          s0 += Y[q] * sm.sh[(q * 3 + 0) * SH_PITCH + l];
-          s1 += Y[q] * sm.sh[(q * 3 + 1) * SH_PITCH + l];
-          s2 += Y[q] * sm.sh[(q * 3 + 2) * SH_PITCH + l];
+        for (int q = 0; q < 16; ++q) {
+          if (q < Kc) {
+            s0 += Y[q] * sm.sh[(q * 3 + 0) * SH_PITCH + l];
+            s1 += Y[q] * sm.sh[(q * 3 + 1) * SH_PITCH + l];
+            s2 += Y[q] * sm.sh[(q * 3 + 2) * SH_PITCH + l];
+          }
+        }
+      } else {
+        const float* f = scn.sh + (size_t)gi * scn.sh_stride;
+        for (int q = 0; q < Kc; ++q) {
+          s0 += Y[q] * __ldg(&f[q * 3 + 0]);
+          s1 += Y[q] * __ldg(&f[q * 3 + 1]);
+          s2 += Y[q] * __ldg(&f[q * 3 + 2]);
         }
       }
       col[0] = fminf(1.f, fmaxf(0.f, s0 + 0.5f));

@@ -88,7 +88,7 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
   // pixel-centre extents of the tile's warp blocks (columns: 2 x 8 px, rows: 4 x 4 px)
   const float tx0 = (float)(tx * TILE) + 0.5f, ty0 = (float)(ty * TILE) + 0.5f;
 
-  const uint2 rg = ws.ranges[(size_t)eloc * rp.ntiles + tile];
+  const uint2 rg = chunk_ok(ws.ok) ? ws.ranges[(size_t)eloc * rp.ntiles + tile] : make_uint2(0u, 0u);
   const uint64_t kb = ws.k_base[eloc];
   const uint64_t rb = ws.rec_base[eloc];
   const uint32_t* __restrict__ list = ws.sorted + kb;
@@ -220,7 +220,7 @@ raster2_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, Chunk
   const f2 FPX = pk(fpx, fpx), FPY = pk((float)py0 + 0.5f, (float)py1 + 0.5f);
   const float tx0 = (float)(tx * TILE) + 0.5f, ty0 = (float)(ty * TILE) + 0.5f;
 
-  const uint2 rg = ws.ranges[(size_t)eloc * rp.ntiles + tile];
+  const uint2 rg = chunk_ok(ws.ok) ? ws.ranges[(size_t)eloc * rp.ntiles + tile] : make_uint2(0u, 0u);
   const uint64_t rb = ws.rec_base[eloc];
   const uint32_t* __restrict__ list = ws.sorted + ws.k_base[eloc];
 

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(DS_THREADS)
 depth_upsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, uint32_t* ghist) {
   __shared__ uint32_t h[DS_RADIX];
   const uint32_t b = blockIdx.x;
+  if (!chunk_ok(ws.ok) || b >= bt.blk_base[bt.ec]) return;   // async mode: fixed grid, capacity guard
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
@@ -129,8 +130,9 @@ depth_upsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, uint32_t*
 
 // one CTA (1024 threads = digits) per env: ghist[b][d] -> output offset of
 // (block b, digit d) relative to the env's segment (digit-major, block-minor)
-__global__ void __launch_bounds__(DS_RADIX) depth_scan_kernel(BlockTable bt, uint32_t* ghist) {
+__global__ void __launch_bounds__(DS_RADIX) depth_scan_kernel(BlockTable bt, uint32_t* ghist, const uint32_t* ok) {
   __shared__ uint32_t wsum[32];
+  if (!chunk_ok(ok)) return;
   const int e = blockIdx.x;
   const uint32_t b0 = bt.blk_base[e], b1 = bt.blk_base[e + 1];
   const int d = threadIdx.x;
@@ -219,6 +221,7 @@ depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const u
   extern __shared__ __align__(16) unsigned char smem_raw[];
   DownSmem& sm = *reinterpret_cast<DownSmem*>(smem_raw);
   const uint32_t b = blockIdx.x;
+  if (!chunk_ok(ws.ok) || b >= bt.blk_base[bt.ec]) return;   // async mode: fixed grid, capacity guard
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
@@ -260,6 +263,7 @@ place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntile
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
   const uint32_t b = blockIdx.x;
+  if (!chunk_ok(ws.ok) || b >= bt.blk_base[bt.ec]) return;   // async mode: fixed grid, capacity guard
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
@@ -282,6 +286,7 @@ place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntile
 __global__ void __launch_bounds__(SB_THREADS) place_scan_kernel(BlockTable bt, ChunkWS ws, uint32_t* thist,
                                                                 int ntiles) {
   __shared__ uint32_t wsum[SB_WARPS];
+  if (!chunk_ok(ws.ok)) return;
   const int e = blockIdx.x;
   const uint32_t b0 = bt.blk_base[e], b1 = bt.blk_base[e + 1];
   uint32_t carry = 0;
@@ -326,6 +331,7 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
   uint32_t* gb = reinterpret_cast<uint32_t*>(smem_raw);   // [nt] block offsets (rel. to k_base)
   uint32_t* wh = gb + nt;                                  // [S][nw2] packed u16 counters / cursors
   const uint32_t b = blockIdx.x;
+  if (!chunk_ok(ws.ok) || b >= bt.blk_base[bt.ec]) return;   // async mode: fixed grid, capacity guard
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t nrec = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
@@ -453,6 +459,7 @@ cudaError_t sort_bin_init() {
 }
 
 uint32_t sort_blocks(uint32_t V) { return (V + SORT_BLK - 1) / SORT_BLK; }
+int sort_block_size() { return SORT_BLK; }
 size_t sort_ghist_words() { return DS_RADIX; }
 
 // number of depth passes for a key span (max over the chunk's envs of zmax - zmin)
@@ -480,7 +487,7 @@ int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, c
     io.kout = p == passes - 1 ? nullptr : ((p & 1) ? ws.dk1 : ws.dk0);
     io.vout = (p & 1) ? ws.dv1 : ws.dv0;
     depth_upsweep_kernel<<<nb, DS_THREADS, 0, s>>>(bt, ws, io, DS_BITS * p, ghist);
-    depth_scan_kernel<<<ec, DS_RADIX, 0, s>>>(bt, ghist);
+    depth_scan_kernel<<<ec, DS_RADIX, 0, s>>>(bt, ghist, ws.ok);
     depth_downsweep_kernel<<<nb, DS_THREADS, depth_down_smem(), s>>>(bt, ws, io, DS_BITS * p, ghist);
     launches += 3;
   }
