@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--cpu-envs", type=int, default=4, help="oracle sample size for cpu_baseline")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--mode", default="async", choices=["async", "sync"],
+                   help="async: sync-free GG_ASYNC render (default); sync: host-sized workspace per chunk")
     p.add_argument("--blur", type=int, default=0, help="motion blur with K samples (gg_render_blur); 0 = off")
     p.add_argument("--shutter", type=float, default=0.01, help="shutter time (s) for --blur")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -216,6 +218,10 @@ def main():
     sid = R.load_scene(t(scene.means), t(scene.scales), t(scene.quats), t(scene.opacities), t(scene.sh),
                        scene.sh_degree)
     gg.gg_reserve(R.ctx, E, W, H, args.chunk)
+    use_async = args.mode == "async" and not args.blur
+    if use_async:
+        gg.gg_reserve_async(R.ctx, E, W, H, args.chunk, 0.7, 4.0)
+    mflag = gg.GG_ASYNC if use_async else 0
     n_sets = args.warmup + args.steps
     # a fresh, seeded pose set for every step, all resident in HBM
     vm = np.stack([gi.cameras(10_000 * (rank + 1) + s, E, W, H, scene).viewmats for s in range(n_sets)])
@@ -236,11 +242,12 @@ def main():
             gg.gg_render_blur(R.ctx, E, ids, vm_d[s], intr, lin_d, ang_d, args.shutter, args.blur, W, H,
                               gg.default_opts(**kw), rgb, depth, None, stream)
         else:
+            kw["flags"] = kw.get("flags", 0) | mflag
             gg.gg_render(R.ctx, E, ids, vm_d[s], intr, W, H, gg.default_opts(**kw), rgb, depth, None, stream)
 
     # ---- counters pass (untimed): n_eval / n_contrib / V / K of pose set 0
-    gg.gg_render(R.ctx, E, ids, vm_d[0], intr, W, H, gg.default_opts(flags=gg.GG_COUNTERS), rgb, depth, None,
-                 stream)
+    gg.gg_render(R.ctx, E, ids, vm_d[0], intr, W, H, gg.default_opts(flags=gg.GG_COUNTERS | mflag), rgb, depth,
+                 None, stream)
     cnt = gg.gg_get_counters(R.ctx, E)
     kb = max(1, args.blur)     # blur renders K sample frames per env (work scaled by K, static-pose counts)
     n_eval, n_contrib, n_vis, n_keys = (int(x) * kb for x in cnt.sum(axis=0))
@@ -265,6 +272,7 @@ def main():
         stage += np.array(gg.gg_get_stage_ms(R.ctx))
     ev1.record(stream)
     torch.cuda.synchronize()
+    gg.gg_check_errors(R.ctx)          # async mode reports capacity overflow here
     launches = gg.gg_launch_count(R.ctx) - launches0
     clocks = clk.stop()
     if world > 1:
@@ -354,7 +362,7 @@ def main():
                           "sh_degree": scene.sh_degree, "width": W, "height": H, "depth": want_depth,
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
-                          "chunk_envs": args.chunk or 1024},
+                          "chunk_envs": args.chunk or 1024, "render_mode": "async (GG_ASYNC)" if use_async else "sync"},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clocks,
                "counters": {"n_eval": n_eval, "n_contrib": n_contrib, "visible": n_vis, "keys": n_keys,

@@ -1,6 +1,6 @@
 # quick: gpu tests + 512-env launch list (kernel times)
 timeout 600 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -3 gpurun_out/pytest_gpu.log
-CMD="python bench.py --envs 512 --steps 1 --warmup 1 --no-e2e --no-cpu"
+CMD="python bench.py --envs 512 --steps 1 --warmup 1 --no-e2e --no-cpu --mode ${MODE:-sync}"
 $CMD > gpurun_out/b512.json 2> gpurun_out/b512.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_q.csv $CMD > /dev/null 2>&1
 python - <<'PY'

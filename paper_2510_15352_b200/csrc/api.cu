@@ -34,7 +34,7 @@ int sort_block_size();
 size_t sort_ghist_words();
 int depth_passes(uint32_t span);
 int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, const RenderParams& rp,
-                    const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s);
+                    const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s, bool nb_is_capacity);
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s);
@@ -644,7 +644,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       return fail(ctx, GG_E_OOM, "gg_render: sort workspace allocation failed");
     CK(cudaMemcpyAsync(ctx->blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, cudaMemcpyHostToDevice, s));
     ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->blkbase), passes, rp, ws, P<uint32_t>(ctx->ghist),
-                                     P<uint32_t>(ctx->thist), s);
+                                     P<uint32_t>(ctx->thist), s, false);
     CK(cudaGetLastError());
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], s));
     // K6
@@ -811,7 +811,7 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     ctx->launches += 5;
     if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 1], s));
     ctx->launches += launch_sort_bin(ec, (uint32_t)ctx->a_nbcap, P<uint32_t>(ctx->blkbase), passes, rp, ws,
-                                     P<uint32_t>(ctx->ghist), P<uint32_t>(ctx->thist), s);
+                                     P<uint32_t>(ctx->ghist), P<uint32_t>(ctx->thist), s, true);
     if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 2], s));
     launch_raster(e0, ec, P<EnvConst>(ctx->envc), rp, ws, rgb, depth, alpha, counters,
                   counters ? P<unsigned long long>(ctx->counters) : nullptr, nullptr, -1, s);

@@ -25,6 +25,7 @@
 // the writes coalesced.  No float math, no order-dependent atomics:
 // identical inputs give bit-identical lists.
 #include "gg_internal.cuh"
+#include <algorithm>
 
 namespace gg {
 
@@ -110,11 +111,7 @@ __device__ __forceinline__ uint32_t depth_digit(uint32_t z, uint32_t zmin, int s
 }
 
 // ---- depth passes --------------------------------------------------------
-__global__ void __launch_bounds__(DS_THREADS)
-depth_upsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, uint32_t* ghist) {
-  __shared__ uint32_t h[DS_RADIX];
-  const uint32_t b = blockIdx.x;
-  if (!chunk_ok(ws.ok) || b >= bt.blk_base[bt.ec]) return;   // async mode: fixed grid, capacity guard
+__device__ __forceinline__ void depth_upsweep_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws, const DepthIO& io, int shift, uint32_t* ghist, uint32_t* h) {
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
@@ -126,6 +123,22 @@ depth_upsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, uint32_t*
     atomicAdd(&h[depth_digit(io.kin[rb + j0 + i], zmin, shift)], 1u);
   __syncthreads();
   for (int i = threadIdx.x; i < DS_RADIX; i += DS_THREADS) ghist[(size_t)b * DS_RADIX + i] = h[i];
+}
+
+template <bool LOOP>
+__global__ void __launch_bounds__(DS_THREADS)
+depth_upsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, uint32_t* ghist) {
+  __shared__ uint32_t h[DS_RADIX];
+  if (!chunk_ok(ws.ok)) return;
+  const uint32_t nb = bt.blk_base[bt.ec];
+  if (!LOOP) {                                     // one CTA per block (sync mode)
+    if (blockIdx.x < nb) depth_upsweep_block(blockIdx.x, bt, ws, io, shift, ghist, h);
+    return;
+  }
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {   // async mode: bounded grid strides over blocks
+    depth_upsweep_block(b, bt, ws, io, shift, ghist, h);
+    __syncthreads();
+  }
 }
 
 // one CTA (1024 threads = digits) per env: ghist[b][d] -> output offset of
@@ -216,12 +229,7 @@ __device__ __forceinline__ void block_rank(const uint32_t (&d)[DS_IPT], uint32_t
   for (int i = tid; i < DS_WARPS * DS_RADIX; i += DS_THREADS) (&sm.wcnt[0][0])[i] = 0u;
 }
 
-__global__ void __launch_bounds__(DS_THREADS, 2)
-depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const uint32_t* ghist) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  DownSmem& sm = *reinterpret_cast<DownSmem*>(smem_raw);
-  const uint32_t b = blockIdx.x;
-  if (!chunk_ok(ws.ok) || b >= bt.blk_base[bt.ec]) return;   // async mode: fixed grid, capacity guard
+__device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws, const DepthIO& io, int shift, const uint32_t* ghist, DownSmem& sm) {
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
@@ -256,14 +264,26 @@ depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const u
   }
 }
 
+template <bool LOOP>
+__global__ void __launch_bounds__(DS_THREADS, 2)
+depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const uint32_t* ghist) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  DownSmem& sm = *reinterpret_cast<DownSmem*>(smem_raw);
+  if (!chunk_ok(ws.ok)) return;
+  const uint32_t nb = bt.blk_base[bt.ec];
+  if (!LOOP) {                                     // one CTA per block (sync mode)
+    if (blockIdx.x < nb) depth_downsweep_block(blockIdx.x, bt, ws, io, shift, ghist, sm);
+    return;
+  }
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {   // async mode: bounded grid strides over blocks
+    depth_downsweep_block(b, bt, ws, io, shift, ghist, sm);
+    __syncthreads();
+  }
+}
+
 // ---- tile placement ------------------------------------------------------
 // order[rb + j] = record (gid-ordered local index) of depth rank j
-__global__ void __launch_bounds__(SB_THREADS)
-place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntiles, int TX, uint32_t* thist) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
-  const uint32_t b = blockIdx.x;
-  if (!chunk_ok(ws.ok) || b >= bt.blk_base[bt.ec]) return;   // async mode: fixed grid, capacity guard
+__device__ __forceinline__ void place_upsweep_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws, const uint32_t* order, int ntiles, int TX, uint32_t* thist, uint32_t* h) {
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
@@ -279,6 +299,23 @@ place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntile
   }
   __syncthreads();
   for (int i = threadIdx.x; i < ntiles; i += SB_THREADS) thist[(size_t)b * ntiles + i] = h[i];
+}
+
+template <bool LOOP>
+__global__ void __launch_bounds__(SB_THREADS)
+place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntiles, int TX, uint32_t* thist) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* h = reinterpret_cast<uint32_t*>(smem_raw);
+  if (!chunk_ok(ws.ok)) return;
+  const uint32_t nb = bt.blk_base[bt.ec];
+  if (!LOOP) {                                     // one CTA per block (sync mode)
+    if (blockIdx.x < nb) place_upsweep_block(blockIdx.x, bt, ws, order, ntiles, TX, thist, h);
+    return;
+  }
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {   // async mode: bounded grid strides over blocks
+    place_upsweep_block(b, bt, ws, order, ntiles, TX, thist, h);
+    __syncthreads();
+  }
 }
 
 // one CTA per env: thist[b][t] -> output offset (relative to k_base[e]) of
@@ -322,16 +359,13 @@ __global__ void __launch_bounds__(SB_THREADS) place_scan_kernel(BlockTable bt, C
 // equal tiles among the lanes with a ballot multisplit and writes each
 // record index at its final slot; no block barrier inside the walk.
 template <int TB>   // tile-id bits (compile time: the multisplit fully unrolls)
-__global__ void __launch_bounds__(SB_THREADS)
-place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderParams rp, const uint32_t* thist,
-                       int S) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws,
+                                                      const uint32_t* order, const RenderParams& rp,
+                                                      const uint32_t* thist, int S, unsigned char* smem_raw) {
   const int nt = rp.ntiles;
   const int nw2 = (nt + 1) >> 1;                     // packed words per warp
   uint32_t* gb = reinterpret_cast<uint32_t*>(smem_raw);   // [nt] block offsets (rel. to k_base)
   uint32_t* wh = gb + nt;                                  // [S][nw2] packed u16 counters / cursors
-  const uint32_t b = blockIdx.x;
-  if (!chunk_ok(ws.ok) || b >= bt.blk_base[bt.ec]) return;   // async mode: fixed grid, capacity guard
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t nrec = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
@@ -429,6 +463,23 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
   }
 }
 
+template <int TB, bool LOOP>
+__global__ void __launch_bounds__(SB_THREADS, 2)
+place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderParams rp, const uint32_t* thist,
+                       int S) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (!chunk_ok(ws.ok)) return;
+  const uint32_t nb = bt.blk_base[bt.ec];
+  if (!LOOP) {                                     // one CTA per block (sync mode)
+    if (blockIdx.x < nb) place_downsweep_block<TB>(blockIdx.x, bt, ws, order, rp, thist, S, smem_raw);
+    return;
+  }
+  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {   // async mode: bounded grid strides over blocks
+    place_downsweep_block<TB>(b, bt, ws, order, rp, thist, S, smem_raw);
+    __syncthreads();
+  }
+}
+
 // ---- host side -------------------------------------------------------------
 size_t depth_down_smem() { return sizeof(DownSmem); }
 // placement segments per block: as many warps as the packed counter table allows
@@ -441,21 +492,27 @@ size_t place_down_smem(int ntiles) {
   return (size_t)ntiles * 4 + (size_t)place_segments(ntiles) * ((ntiles + 1) / 2) * 4;
 }
 
-cudaError_t sort_bin_init() {
-  cudaError_t e = cudaFuncSetAttribute(depth_downsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <bool LOOP>
+static cudaError_t sort_bin_init_variant() {
+  cudaError_t e = cudaFuncSetAttribute(depth_downsweep_kernel<LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)depth_down_smem());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(place_downsweep_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(place_downsweep_kernel<8, LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)place_down_smem(MAX_TILES));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(place_downsweep_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(place_downsweep_kernel<11, LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)place_down_smem(MAX_TILES));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(place_downsweep_kernel<13>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(place_downsweep_kernel<13, LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)place_down_smem(MAX_TILES));
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(place_upsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(place_upsweep_kernel<LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(MAX_TILES * 4));
+}
+
+cudaError_t sort_bin_init() {
+  cudaError_t e = sort_bin_init_variant<false>();
+  return e != cudaSuccess ? e : sort_bin_init_variant<true>();
 }
 
 uint32_t sort_blocks(uint32_t V) { return (V + SORT_BLK - 1) / SORT_BLK; }
@@ -472,13 +529,13 @@ int depth_passes(uint32_t span) {
 
 // Enqueue K3-K5 for a chunk.  blk_base: device [ec+1] block prefix; nb total
 // blocks; ghist >= nb*DS_RADIX u32; thist >= nb*ntiles u32.  Returns launches.
-int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, const RenderParams& rp,
-                    const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s) {
-  if (nb == 0) {
-    cudaMemsetAsync(ws.ranges, 0, (size_t)ec * rp.ntiles * sizeof(uint2), s);
-    return 0;
-  }
-  BlockTable bt{blk_base, ec};
+template <bool LOOP>
+static int launch_sort_bin_t(int ec, uint32_t nb, const BlockTable& bt, int passes, const RenderParams& rp,
+                             const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s) {
+  // sync mode (LOOP = false): one CTA per block; async mode: nb is only a
+  // capacity, so a bounded grid strides over the blocks that exist
+  const uint32_t g1 = LOOP ? std::min<uint32_t>(nb, 148u * 16u) : nb;
+  const uint32_t g2 = LOOP ? std::min<uint32_t>(nb, 148u * 8u) : nb;
   int launches = 0;
   for (int p = 0; p < passes; ++p) {
     DepthIO io;
@@ -486,23 +543,37 @@ int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, c
     io.vin = p == 0 ? nullptr : ((p & 1) ? ws.dv0 : ws.dv1);
     io.kout = p == passes - 1 ? nullptr : ((p & 1) ? ws.dk1 : ws.dk0);
     io.vout = (p & 1) ? ws.dv1 : ws.dv0;
-    depth_upsweep_kernel<<<nb, DS_THREADS, 0, s>>>(bt, ws, io, DS_BITS * p, ghist);
+    depth_upsweep_kernel<LOOP><<<g1, DS_THREADS, 0, s>>>(bt, ws, io, DS_BITS * p, ghist);
     depth_scan_kernel<<<ec, DS_RADIX, 0, s>>>(bt, ghist, ws.ok);
-    depth_downsweep_kernel<<<nb, DS_THREADS, depth_down_smem(), s>>>(bt, ws, io, DS_BITS * p, ghist);
+    depth_downsweep_kernel<LOOP><<<g1, DS_THREADS, depth_down_smem(), s>>>(bt, ws, io, DS_BITS * p, ghist);
     launches += 3;
   }
   const uint32_t* order = ((passes - 1) & 1) ? ws.dv1 : ws.dv0;   // values of the last depth pass
-  place_upsweep_kernel<<<nb, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
+  place_upsweep_kernel<LOOP><<<g2, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
   place_scan_kernel<<<ec, SB_THREADS, 0, s>>>(bt, ws, thist, rp.ntiles);
   const size_t psm = place_down_smem(rp.ntiles);
   const int S = place_segments(rp.ntiles);
   if (rp.ntiles <= 256)
-    place_downsweep_kernel<8><<<nb, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+    place_downsweep_kernel<8, LOOP><<<g2, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   else if (rp.ntiles <= 2048)
-    place_downsweep_kernel<11><<<nb, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+    place_downsweep_kernel<11, LOOP><<<g2, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   else
-    place_downsweep_kernel<13><<<nb, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+    place_downsweep_kernel<13, LOOP><<<g2, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   return launches + 3;
+}
+
+// Enqueue K3-K5 for a chunk.  blk_base: device [ec+1] block prefix; nb total
+// blocks (a capacity if nb_is_capacity); ghist >= nb*DS_RADIX u32; thist >=
+// nb*ntiles u32.  Returns the number of launches.
+int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, const RenderParams& rp,
+                    const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s, bool nb_is_capacity) {
+  if (nb == 0) {
+    cudaMemsetAsync(ws.ranges, 0, (size_t)ec * rp.ntiles * sizeof(uint2), s);
+    return 0;
+  }
+  BlockTable bt{blk_base, ec};
+  return nb_is_capacity ? launch_sort_bin_t<true>(ec, nb, bt, passes, rp, ws, ghist, thist, s)
+                        : launch_sort_bin_t<false>(ec, nb, bt, passes, rp, ws, ghist, thist, s);
 }
 
 }  // namespace gg
