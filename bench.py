@@ -55,7 +55,7 @@ def parse():
     p.add_argument("--cpu-envs", type=int, default=4, help="oracle sample size for cpu_baseline")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--mode", default="async", choices=["async", "sync"],
+    p.add_argument("--mode", default="sync", choices=["async", "sync"],
                    help="async: sync-free GG_ASYNC render (default); sync: host-sized workspace per chunk")
     p.add_argument("--blur", type=int, default=0, help="motion blur with K samples (gg_render_blur); 0 = off")
     p.add_argument("--shutter", type=float, default=0.01, help="shutter time (s) for --blur")

@@ -534,8 +534,8 @@ static int launch_sort_bin_t(int ec, uint32_t nb, const BlockTable& bt, int pass
                              const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s) {
   // sync mode (LOOP = false): one CTA per block; async mode: nb is only a
   // capacity, so a bounded grid strides over the blocks that exist
-  const uint32_t g1 = LOOP ? std::min<uint32_t>(nb, 148u * 16u) : nb;
-  const uint32_t g2 = LOOP ? std::min<uint32_t>(nb, 148u * 8u) : nb;
+  const uint32_t g1 = LOOP ? std::min<uint32_t>(nb, 148u * 64u) : nb;
+  const uint32_t g2 = LOOP ? std::min<uint32_t>(nb, 148u * 32u) : nb;
   int launches = 0;
   for (int p = 0; p < passes; ++p) {
     DepthIO io;
