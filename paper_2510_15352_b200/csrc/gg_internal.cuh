@@ -14,7 +14,7 @@ constexpr int MAX_TILES = 8192;        // tile table limit (e.g. 1024x2048 px)
 // Scene store (SoA, 16-B aligned; DESIGN.md §4 "HBM layout").  O1 results
 // (Sigma3, DC colour) are precomputed at load (K0 scene_pack).
 struct DevScene {
-  const float4* pos_op;  // (x, y, z, opacity)
+  const float4* pos_op;  // (x, y, z, log2 opacity)
   const float4* cov_a;   // (Sxx, Sxy, Sxz, Syy)
   const float4* cov_b;   // (Syz, Szz, dc_r, dc_g)
   const float2* aux;     // (dc_b, max_j s_j^2)
@@ -27,7 +27,7 @@ struct DevScene {
 
 // Per-env camera constants (setup_envs).  f32 values follow the canonical
 // order of DESIGN.md §2.1 (they feed integer decisions).
-struct EnvConst {
+struct __align__(16) EnvConst {
   float R[9];          // world->camera rotation, row-major
   float t[3];
   float fx, fy, cx, cy;
@@ -38,6 +38,16 @@ struct EnvConst {
   int32_t degree;      // SH degree used at render
   int32_t out_index;   // caller's env index (outputs, counters); envs are processed scene-sorted
 };
+
+// 128-bit loads of a camera from shared memory (7 x LDS.128 instead of 28 LDS)
+__device__ __forceinline__ EnvConst load_cam(const EnvConst* p) {
+  EnvConst c;
+  const float4* s = reinterpret_cast<const float4*>(p);
+  float4* d = reinterpret_cast<float4*>(&c);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(EnvConst) / 16); ++i) d[i] = s[i];
+  return c;
+}
 
 // A run of <= ENV_GROUP chunk-local envs bound to the same scene; the
 // projection kernels load each Gaussian once and test it against the group.

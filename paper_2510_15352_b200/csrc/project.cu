@@ -127,7 +127,7 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
   float smax2 = 0.f;
   const int wi = blockIdx.y * (PROJ_BLOCK / 32) + warp;
   for (int k = 0; k < grp.cnt; ++k) {
-    const EnvConst& c = cams[k];
+    const EnvConst c = load_cam(&cams[k]);
     if (c.scene != cur) {             // uniform across the CTA
       cur = c.scene;
       if (i < c.n) {
@@ -223,7 +223,7 @@ __device__ __forceinline__ void sh_eval(int deg, float x, float y, float z, floa
 }
 
 constexpr int SH_MAX = 48;              // floats per Gaussian at degree 3
-constexpr int SH_PITCH = PROJ_BLOCK + 1;
+constexpr int SH_PITCH = PROJ_BLOCK + 1;   // transposed [coefficient][Gaussian], conflict-free
 
 struct ProjSmem {
   EnvConst cams[ENV_GROUP];
@@ -233,7 +233,7 @@ struct ProjSmem {
   uint32_t kacc[ENV_GROUP];
   uint32_t total;
   uint16_t list[ENV_GROUP * PROJ_BLOCK];   // (k << 8) | local
-  float sh[1];                       // [SH_MAX][SH_PITCH] when degree > 0 (dynamic tail)
+  __align__(16) float sh[4];         // [SH_MAX][SH_PITCH] when degree > 0 (dynamic tail)
 };
 
 __global__ void __launch_bounds__(PROJ_BLOCK)
@@ -308,6 +308,8 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     if (deg > 0 && i < c0.n) {
       // this thread's Gaussian: 128-bit loads of its SH row, transposed into
       // [coefficient][Gaussian] so the projection reads are conflict-free
+      // this thread's Gaussian: 128-bit loads of its SH row, transposed into
+      // [coefficient][Gaussian] so the projection reads are conflict-free
       const int nf4 = (K * 3 + 3) / 4;
       const float4* src = reinterpret_cast<const float4*>(sc.sh + (size_t)i * sc.sh_stride);
 #pragma unroll 4
@@ -325,7 +327,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   for (uint32_t s = tid; s < total; s += PROJ_BLOCK) {
     const uint32_t ent = sm.list[s];
     const int k = ent >> 8, l = ent & 255;
-    const EnvConst& c = sm.cams[k];
+    const EnvConst c = load_cam(&sm.cams[k]);
     const int eloc = grp.elo + k;
     const uint32_t rank = s - sm.cnt[k * 8];
     const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + rank;
@@ -422,23 +424,25 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     // blend-side culling extents: alpha >= 1/255 needs q <= 2 ln(255 o); the
     // ellipse's half extents are sqrt(qmax Sigma2_xx), sqrt(qmax Sigma2_yy)
     // (+ margins, so the skip never changes a blend decision).
-    const float o = g.w;
+    const float L = g.w;                       // log2 opacity (scene store)
     float ex = -1.f, ey = -1.f;
-    if (o * 255.f > 1.f) {
-      const float qmax = 2.f * logf(255.f * o);
-      ex = sqrtf(qmax * a) * 1.002f + 0.02f;
-      ey = sqrtf(qmax * cc) * 1.002f + 0.02f;
+    if (L > -7.99435343685885793f) {           // o > 1/255
+      // q <= qmax = 2 ln 2 (log2 o + log2 255); half extents sqrt(qmax Sxx), sqrt(qmax Syy)
+      const float qmax = 1.3862943611198906f * (L + 7.99435343685885793f);
+      const float qa = qmax * a, qc = qmax * cc;
+      ex = qa * rsqrtf(qa) * 1.002f + 0.02f;
+      ey = qc * rsqrtf(qc) * 1.002f + 0.02f;
     }
     // record for the blend (DESIGN.md §4 K6): alpha = min(.99, 2^(A'dx^2 + B'dxdy + C'dy^2 + log2 o))
     const float kq = -0.72134752044448170f;   // -0.5 log2(e)
-    ws.rec0[r] = make_float4(u, v, log2f(o), p.z);
+    ws.rec0[r] = make_float4(u, v, L, p.z);
     ws.rec1[r] = make_float4(cA * kq, 2.f * cB * kq, cC * kq, ex);
     ws.rec2[r] = make_float4(col[0], col[1], col[2], ey);
     ws.rect[r] = make_uint2(x0 | (x1 << 16), y0 | (y1 << 16));
     ws.zkey[r] = __float_as_uint(p.z);
     if (ws.gid) {
       ws.gid[r] = (uint32_t)(i0 + l);
-      ws.dconic[r] = make_float4(cA, cB, cC, o);
+      ws.dconic[r] = make_float4(cA, cB, cC, exp2f(L));
     }
     if (ntiles) atomicAdd(&sm.kacc[k], ntiles);
   }

@@ -73,7 +73,8 @@ __global__ void pack_kernel(int64_t n, int K, int sh_stride, const float* __rest
 #pragma unroll
     for (int c = 0; c < 3; ++c) dc[c] = fminf(1.f, fmaxf(0.f, SH_C0 * sh[i * K * 3 + c] + 0.5f));
     const float smax = fmaxf(s0, fmaxf(s1, s2));
-    pos_op[i] = make_float4(means[i * 3], means[i * 3 + 1], means[i * 3 + 2], opac[i]);
+    // log2(o) once per Gaussian: the blend works in the log2 domain (R30)
+    pos_op[i] = make_float4(means[i * 3], means[i * 3 + 1], means[i * 3 + 2], log2f(opac[i]));
     cov_a[i] = make_float4(Sxx, Sxy, Sxz, Syy);
     cov_b[i] = make_float4(Syz, Szz, dc[0], dc[1]);
     aux[i] = make_float2(dc[2], smax * smax);
