@@ -50,6 +50,7 @@ void launch_tables_k(int ec, const uint32_t* vcnt, const uint32_t* kcnt, uint64_
                      int sort_blk, uint64_t kcap, uint64_t nbcap, uint32_t* ok, uint32_t* err, cudaStream_t s);
 void launch_checksum(int E, int W, int H, const uint8_t* rgb8, const float* rgbf, const float* depth,
                      unsigned long long* out, cudaStream_t s);
+int launch_copy_words(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void launch_debug_records(uint32_t V, uint64_t rb, const ChunkWS& ws, int32_t* tile_counts, float* proj,
                           cudaStream_t s);
 void launch_debug_sorted(int ntiles, const uint2* ranges, uint64_t kb, uint64_t rb, const ChunkWS& ws,
@@ -529,7 +530,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   // contiguous, so the projection kernels can share each Gaussian load
   // across a group of envs.  Outputs are still written at the caller's
   // env index (EnvConst.out_index).
-  CK(cudaMemcpyAsync(ctx->h_ids, scene_ids, (size_t)E * 4, cudaMemcpyDeviceToHost, s));
+  ctx->launches += launch_copy_words(ctx->h_ids, scene_ids, (size_t)E * 4, s);
   CK(cudaStreamSynchronize(s));
   const int nsc = (int)ctx->scenes.size();
   auto key = [&](int e) {
@@ -544,7 +545,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ctx->h_perm[p] = order[p];
     if (keep && order[p] == opts.debug_env) dbg_pos = p;
   }
-  CK(cudaMemcpyAsync(ctx->perm.p, ctx->h_perm, (size_t)E * 4, cudaMemcpyHostToDevice, s));
+  ctx->launches += launch_copy_words(ctx->perm.p, ctx->h_perm, (size_t)E * 4, s);
   launch_setup_envs(E, P<int32_t>(ctx->perm), scene_ids, viewmats, intr, P<DevScene>(ctx->scene_table), nsc, W, H,
                     opts.sh_degree, P<EnvConst>(ctx->envc), P<uint32_t>(ctx->errflag), s);
   ctx->launches++;
@@ -569,7 +570,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       }
       i = j;
     }
-    CK(cudaMemcpyAsync(ctx->groups.p, ctx->h_groups, sizeof(EnvGroup) * ngroups, cudaMemcpyHostToDevice, s));
+    ctx->launches += launch_copy_words(ctx->groups.p, ctx->h_groups, sizeof(EnvGroup) * ngroups, s);
     ChunkWS ws{};
     ws.flags = P<uint32_t>(ctx->flags);
     ws.blkcnt = P<uint32_t>(ctx->blkcnt);
@@ -592,7 +593,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
     ctx->launches += 2;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(ctx->h_vcnt, ws.vcnt, ec * 4, cudaMemcpyDeviceToHost, s));
+    ctx->launches += launch_copy_words(ctx->h_vcnt, ws.vcnt, ec * 4, s);
     CK(cudaStreamSynchronize(s));
     uint64_t V = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_rbase[i] = V; V += ctx->h_vcnt[i]; }
@@ -604,7 +605,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
         !ensure(ctx, ctx->dk1, V * 4, s) || !ensure(ctx, ctx->dv1, V * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: record workspace (%llu records) allocation failed",
                   (unsigned long long)V);
-    CK(cudaMemcpyAsync(P<uint64_t>(ctx->rbase), ctx->h_rbase, ec * 8, cudaMemcpyHostToDevice, s));
+    ctx->launches += launch_copy_words(ctx->rbase.p, ctx->h_rbase, ec * 8, s);
     CK(cudaMemsetAsync(ws.kcnt, 0, ec * 4, s));
     ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
     ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
@@ -617,9 +618,9 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
                    ws, s);
     ctx->launches++;
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(ctx->h_kcnt, ws.kcnt, ec * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ctx->h_zmm, ws.zmin, ec * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(ctx->h_zmm + ctx->h_cap, ws.zmax, ec * 4, cudaMemcpyDeviceToHost, s));
+    ctx->launches += launch_copy_words(ctx->h_kcnt, ws.kcnt, ec * 4, s);
+    ctx->launches += launch_copy_words(ctx->h_zmm, ws.zmin, ec * 4, s);
+    ctx->launches += launch_copy_words(ctx->h_zmm + ctx->h_cap, ws.zmax, ec * 4, s);
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], s));
     CK(cudaStreamSynchronize(s));
     uint64_t K = 0;
@@ -628,7 +629,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       if (ctx->h_kcnt[i] >= 0xfffffff0u) return fail(ctx, GG_E_CAPACITY, "gg_render: env key overflow");
     if (!ensure(ctx, ctx->sorted, K * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: key workspace (%llu keys) allocation failed", (unsigned long long)K);
-    CK(cudaMemcpyAsync(P<uint64_t>(ctx->kbase), ctx->h_kbase, ec * 8, cudaMemcpyHostToDevice, s));
+    ctx->launches += launch_copy_words(ctx->kbase.p, ctx->h_kbase, ec * 8, s);
     ws.sorted = P<uint32_t>(ctx->sorted);
     // K3-K5: sort blocks of 8192 records, never straddling an env
     uint32_t nb = 0;
@@ -642,7 +643,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
         !ensure(ctx, ctx->ghist, (size_t)nb * sort_ghist_words() * 4, s) ||
         !ensure(ctx, ctx->thist, (size_t)nb * ntiles * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: sort workspace allocation failed");
-    CK(cudaMemcpyAsync(ctx->blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, cudaMemcpyHostToDevice, s));
+    ctx->launches += launch_copy_words(ctx->blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, s);
     ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->blkbase), passes, rp, ws, P<uint32_t>(ctx->ghist),
                                      P<uint32_t>(ctx->thist), s, false);
     CK(cudaGetLastError());
@@ -719,7 +720,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   }
   if (ctx->timing) for (int i = 0; i < 3; ++i) ctx->stage_ms[i] = ms[i];
   ctx->last_E = E;
-  CK(cudaMemcpyAsync(ctx->h_err, ctx->errflag.p, 4, cudaMemcpyDeviceToHost, s));
+  ctx->launches += launch_copy_words(ctx->h_err, ctx->errflag.p, 4, s);
   CK(cudaStreamSynchronize(s));
   if (*ctx->h_err & ERR_BAD_SCENE) return fail(ctx, GG_E_BAD_SCENE, "gg_render: an env is bound to an unknown scene id");
   return GG_OK;

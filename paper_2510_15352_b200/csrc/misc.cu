@@ -1,3 +1,4 @@
+#include <algorithm>
 // misc.cu — K7 checksum and K8 debug extraction kernels.
 #include "gg_internal.cuh"
 
@@ -80,6 +81,24 @@ void launch_debug_records(uint32_t V, uint64_t rb, const ChunkWS& ws, int32_t* t
 void launch_debug_sorted(int ntiles, const uint2* ranges, uint64_t kb, uint64_t rb, const ChunkWS& ws,
                          int32_t* s_tile, uint32_t* s_z, int32_t* s_gid, cudaStream_t s) {
   debug_sorted_kernel<<<min(ntiles, 1024), 256, 0, s>>>(ntiles, ranges, kb, rb, ws, s_tile, s_z, s_gid);
+}
+
+
+// Small host<->device table transfers for the sync-mode host loop.  Pinned
+// host memory is UVA-mapped, so a one-block kernel moves the words over the
+// bus without touching a copy engine: the per-chunk readbacks never queue
+// behind large frame copies (gg_render_host) issued on other streams.
+__global__ void copy_words_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, size_t n) {
+  for (size_t i = threadIdx.x + (size_t)blockIdx.x * blockDim.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+int launch_copy_words(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  const size_t n = bytes / 4;
+  if (!n) return 0;
+  const int grid = (int)std::min<size_t>((n + 255) / 256, 64);
+  copy_words_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<uint32_t*>(dst), reinterpret_cast<const uint32_t*>(src), n);
+  return 1;
 }
 
 }  // namespace gg
