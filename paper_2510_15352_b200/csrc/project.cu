@@ -229,7 +229,9 @@ struct ProjSmem {
   EnvConst cams[ENV_GROUP];
   float4 pos[PROJ_BLOCK], ca[PROJ_BLOCK], cb[PROJ_BLOCK];
   float dcb[PROJ_BLOCK];
-  uint32_t cnt[ENV_GROUP * 8];       // popc per (env, word), then exclusive prefix
+  uint32_t fw[ENV_GROUP * 8];        // visibility words (env, word)
+  uint32_t cnt[ENV_GROUP * 8];       // popc per (env, word), then exclusive prefix within the env
+  uint32_t wsum[PROJ_BLOCK / 32];
   uint32_t kacc[ENV_GROUP];
   uint32_t total;
   uint16_t list[ENV_GROUP * PROJ_BLOCK];   // (k << 8) | local
@@ -247,46 +249,68 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   const int gblk = blockIdx.y;
   const int i0 = gblk * PROJ_BLOCK;
   load_group_cams(sm.cams, envs, e0, grp);
-  // visibility words of the group -> (env, Gaussian) list in (env, gid) order
+  // visibility words of the group -> (Gaussian, env) pair list in (gid, env)
+  // order: lanes that share a Gaussian broadcast its shared-memory SH/geometry
+  // and the few distinct Gaussians of a warp are adjacent (no bank
+  // conflicts).  A record's index is its rank within its env (gid order),
+  // which does not depend on which thread computes it.
   if (tid < ENV_GROUP * 8) {
     const int k = tid >> 3, w = tid & 7;
     uint32_t word = 0;
     if (k < grp.cnt) word = ws.flags[(size_t)(grp.elo + k) * ws.nwords + gblk * 8 + w];
+    sm.fw[tid] = word;
     sm.cnt[tid] = __popc(word);
   }
   if (tid < ENV_GROUP) sm.kacc[tid] = 0;
   __syncthreads();
-  if (tid < 32) {   // exclusive scan of 128 counts (4 per lane)
-    uint32_t c0 = sm.cnt[tid * 4], c1 = sm.cnt[tid * 4 + 1], c2 = sm.cnt[tid * 4 + 2], c3 = sm.cnt[tid * 4 + 3];
-    const uint32_t loc = c0 + c1 + c2 + c3;
-    uint32_t s = loc;
+  if (tid < ENV_GROUP) {   // per env: exclusive prefix of its 8 word counts
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t c = sm.cnt[tid * 8 + w];
+      sm.cnt[tid * 8 + w] = run;
+      run += c;
+    }
+  }
+  // this thread's Gaussian: mask of the group's envs that see it
+  uint32_t emask = 0;
+  {
+    const int w = tid >> 5, b = tid & 31;
+#pragma unroll
+    for (int k = 0; k < ENV_GROUP; ++k) emask |= ((sm.fw[k * 8 + w] >> b) & 1u) << k;
+  }
+  const uint32_t ecnt = __popc(emask);
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    uint32_t incl = ecnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-      if (tid >= o) s += y;
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    uint32_t ex = s - loc;
-    sm.cnt[tid * 4] = ex; ex += c0;
-    sm.cnt[tid * 4 + 1] = ex; ex += c1;
-    sm.cnt[tid * 4 + 2] = ex; ex += c2;
-    sm.cnt[tid * 4 + 3] = ex;
-    if (tid == 31) sm.total = s;
+    if (lane == 31) sm.wsum[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t run = 0;
+#pragma unroll
+      for (int q = 0; q < PROJ_BLOCK / 32; ++q) {
+        const uint32_t c = sm.wsum[q];
+        sm.wsum[q] = run;
+        run += c;
+      }
+      sm.total = run;
+    }
+    __syncthreads();
+    uint32_t o = sm.wsum[warp] + incl - ecnt;
+    uint32_t m = emask;
+    while (m) {
+      const int k = __ffs(m) - 1;
+      m &= m - 1;
+      sm.list[o++] = (uint16_t)((k << 8) | tid);
+    }
   }
-  __syncthreads();
   const uint32_t total = sm.total;
   if (total == 0) return;
-  if (tid < ENV_GROUP * 8) {
-    const int k = tid >> 3, w = tid & 7;
-    if (k < grp.cnt) {
-      uint32_t word = ws.flags[(size_t)(grp.elo + k) * ws.nwords + gblk * 8 + w];
-      uint32_t o = sm.cnt[tid];
-      while (word) {
-        const int b = __ffs(word) - 1;
-        word &= word - 1;
-        sm.list[o++] = (uint16_t)((k << 8) | (w * 32 + b));
-      }
-    }
-  }
   // stage the block's Gaussians (visible in at least one env of the group)
   // stage the block's Gaussians of the group's first valid scene; envs of
   // another scene (mixed groups, async mode) read theirs from global memory
@@ -297,7 +321,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   const DevScene& sc = scenes[st_scene < 0 ? 0 : st_scene];
   const int deg = c0.degree;
   const int K = (deg + 1) * (deg + 1);
-  if (st_scene >= 0) {
+  if (st_scene >= 0 && emask) {   // only Gaussians some env of the group sees
     const int i = i0 + tid;
     if (i < c0.n) {
       sm.pos[tid] = __ldg(&sc.pos_op[i]);
@@ -306,8 +330,6 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
       sm.dcb[tid] = __ldg(&sc.aux[i]).x;
     }
     if (deg > 0 && i < c0.n) {
-      // this thread's Gaussian: 128-bit loads of its SH row, transposed into
-      // [coefficient][Gaussian] so the projection reads are conflict-free
       // this thread's Gaussian: 128-bit loads of its SH row, transposed into
       // [coefficient][Gaussian] so the projection reads are conflict-free
       const int nf4 = (K * 3 + 3) / 4;
@@ -329,7 +351,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     const int k = ent >> 8, l = ent & 255;
     const EnvConst c = load_cam(&sm.cams[k]);
     const int eloc = grp.elo + k;
-    const uint32_t rank = s - sm.cnt[k * 8];
+    const uint32_t rank = sm.cnt[k * 8 + (l >> 5)] + __popc(sm.fw[k * 8 + (l >> 5)] & ((1u << (l & 31)) - 1u));
     const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + rank;
     const bool staged = c.scene == st_scene;
     const DevScene& scn = scenes[c.scene];

@@ -31,6 +31,8 @@ namespace gg {
 
 constexpr int SB_THREADS = 1024;                // placement kernels
 constexpr int SB_WARPS = 32;
+constexpr int PD_THREADS = 512;                 // placement downsweep: 16 warps = up to 16 segments
+constexpr int PD_WARPS = PD_THREADS / 32;
 constexpr int SORT_BLK = 4096;                  // records per sort block (depth and placement)
 constexpr int DS_THREADS = 512;                 // depth passes: 16 warps x 8 elements
 constexpr int DS_WARPS = DS_THREADS / 32;
@@ -362,18 +364,23 @@ template <int TB>   // tile-id bits (compile time: the multisplit fully unrolls)
 __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws,
                                                       const uint32_t* order, const RenderParams& rp,
                                                       const uint32_t* thist, int S, unsigned char* smem_raw) {
+  constexpr bool STAMP = TB <= 11;                   // warp-private tile stamps fit in shared memory
   const int nt = rp.ntiles;
   const int nw2 = (nt + 1) >> 1;                     // packed words per warp
   uint32_t* gb = reinterpret_cast<uint32_t*>(smem_raw);   // [nt] block offsets (rel. to k_base)
   uint32_t* wh = gb + nt;                                  // [S][nw2] packed u16 counters / cursors
+  uint32_t* pmask = wh + (size_t)S * nw2;                  // [S][32] peer masks by representative lane
+  uint8_t* stamps = reinterpret_cast<uint8_t*>(pmask + (STAMP ? S * 32 : 0));   // [S][nt] last lane per tile
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t nrec = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
   const uint64_t rb = ws.rec_base[e];
   uint32_t* out = ws.sorted + ws.k_base[e];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < nt; i += SB_THREADS) gb[i] = thist[(size_t)b * nt + i];
-  for (int i = tid; i < S * nw2; i += SB_THREADS) wh[i] = 0u;
+  for (int i = tid; i < nt; i += PD_THREADS) gb[i] = thist[(size_t)b * nt + i];
+  for (int i = tid; i < S * nw2; i += PD_THREADS) wh[i] = 0u;
+  if (STAMP)
+    for (int i = tid; i < S * 32; i += PD_THREADS) pmask[i] = 0u;
   // segment of warp w: records [w*Ls, (w+1)*Ls) of the block, Ls multiple of 32
   const uint32_t Ls = ((nrec + S * 32 - 1) / (S * 32)) * 32;
   const uint32_t s0 = warp < S ? min(nrec, warp * Ls) : nrec;
@@ -394,7 +401,7 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
   }
   __syncthreads();
   // phase 2: per-warp cursors relative to the block's run of each tile
-  for (int q = tid; q < nw2; q += SB_THREADS) {
+  for (int q = tid; q < nw2; q += PD_THREADS) {
     uint32_t run0 = 0, run1 = 0;
     for (int w = 0; w < S; ++w) {
       const uint32_t c = wh[(size_t)w * nw2 + q];
@@ -407,6 +414,8 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
   // phase 3: ordered walk, 32 records per step, their pairs 32 at a time
   if (warp >= S) return;
   uint32_t* h = wh + (size_t)warp * nw2;
+  uint8_t* st = stamps + (size_t)warp * nt;
+  uint32_t* pm = pmask + warp * 32;
   const uint32_t lt = lanemask_lt();
   for (uint32_t base = s0; base < s1; base += 32) {
     const uint32_t j = base + lane;
@@ -425,6 +434,8 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
       if (lane >= o) incl += y;
     }
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - np;
+    const uint32_t xy0 = x0 | (y0 << 16);
     for (uint32_t f0 = 0; f0 < tot; f0 += 32) {
       const uint32_t f = f0 + lane;
       const bool ok = f < tot;
@@ -434,25 +445,37 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
         const uint32_t v = __shfl_sync(0xffffffffu, incl, src + step - 1);
         if (v <= f) src += step;
       }
-      const uint32_t o_incl = __shfl_sync(0xffffffffu, incl, src);
-      const uint32_t o_np = __shfl_sync(0xffffffffu, np, src);
+      const uint32_t o_ex = __shfl_sync(0xffffffffu, excl, src);
       const uint32_t o_w = __shfl_sync(0xffffffffu, w, src);
-      const uint32_t o_x0 = __shfl_sync(0xffffffffu, x0, src);
-      const uint32_t o_y0 = __shfl_sync(0xffffffffu, y0, src);
+      const uint32_t o_xy = __shfl_sync(0xffffffffu, xy0, src);
       const uint32_t o_idx = __shfl_sync(0xffffffffu, idx, src);
       uint32_t t = 0;
       if (ok) {
         // qq / o_w for small integers via the f32 reciprocal (exact: qq < 2^20, o_w < 2^16)
-        const uint32_t qq = f - (o_incl - o_np);
+        const uint32_t qq = f - o_ex;
         const uint32_t row = (uint32_t)__fdividef((float)qq + 0.5f, (float)o_w);
-        t = (o_y0 + row) * rp.TX + o_x0 + (qq - row * o_w);
+        t = ((o_xy >> 16) + row) * rp.TX + (o_xy & 0xffffu) + (qq - row * o_w);
       }
-      uint32_t peers = __ballot_sync(0xffffffffu, ok);
+      uint32_t peers;
+      if (STAMP) {
+        // lanes sharing a tile agree on a representative (the last lane that
+        // stamped it); one shared-memory OR per lane then yields the peer mask
+        if (ok) st[t] = (uint8_t)lane;
+        __syncwarp();
+        const uint32_t rep = ok ? st[t] : 0u;
+        if (ok) atomicOr(&pm[rep], 1u << lane);
+        __syncwarp();
+        peers = ok ? pm[rep] : 0u;
+        __syncwarp();
+        if (ok && lane == (int)rep) pm[rep] = 0u;
+      } else {
+        peers = __ballot_sync(0xffffffffu, ok);
 #pragma unroll
-      for (int bb = 0; bb < TB; ++bb) {
-        const bool bit = (t >> bb) & 1u;
-        const uint32_t m = __ballot_sync(0xffffffffu, bit);
-        peers &= bit ? m : ~m;
+        for (int bb = 0; bb < TB; ++bb) {
+          const bool bit = (t >> bb) & 1u;
+          const uint32_t m = __ballot_sync(0xffffffffu, bit);
+          peers &= bit ? m : ~m;
+        }
       }
       const uint32_t before = ok ? (h[t >> 1] >> (16 * (t & 1))) & 0xffffu : 0u;
       __syncwarp();
@@ -464,7 +487,7 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
 }
 
 template <int TB, bool LOOP>
-__global__ void __launch_bounds__(SB_THREADS, 2)
+__global__ void __launch_bounds__(PD_THREADS, 3)
 place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderParams rp, const uint32_t* thist,
                        int S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -482,14 +505,20 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
 
 // ---- host side -------------------------------------------------------------
 size_t depth_down_smem() { return sizeof(DownSmem); }
-// placement segments per block: as many warps as the packed counter table allows
+// placement segments per block: as many warps as the shared-memory budget
+// allows (per segment: packed u16 counters, and for <= 2048 tiles the u8
+// stamps and 32 peer masks of the warp-private ranking)
+static size_t place_seg_bytes(int ntiles) {
+  const size_t w = ((size_t)ntiles + 1) / 2 * 4;
+  return ntiles <= 2048 ? w + 128 + (size_t)ntiles : w;
+}
 int place_segments(int ntiles) {
-  const size_t budget = 200 * 1024 - (size_t)ntiles * 4;
-  const int s = (int)(budget / (((size_t)ntiles + 1) / 2 * 4));
-  return s < 1 ? 1 : (s > SB_WARPS ? SB_WARPS : s);
+  const size_t budget = 72 * 1024 - (size_t)ntiles * 4;
+  const int s = (int)(budget / place_seg_bytes(ntiles));
+  return s < 1 ? 1 : (s > PD_WARPS ? PD_WARPS : s);
 }
 size_t place_down_smem(int ntiles) {
-  return (size_t)ntiles * 4 + (size_t)place_segments(ntiles) * ((ntiles + 1) / 2) * 4;
+  return (size_t)ntiles * 4 + (size_t)place_segments(ntiles) * place_seg_bytes(ntiles);
 }
 
 template <bool LOOP>
@@ -498,13 +527,13 @@ static cudaError_t sort_bin_init_variant() {
                                        (int)depth_down_smem());
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(place_downsweep_kernel<8, LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)place_down_smem(MAX_TILES));
+                           72 * 1024);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(place_downsweep_kernel<11, LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)place_down_smem(MAX_TILES));
+                           72 * 1024);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(place_downsweep_kernel<13, LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)place_down_smem(MAX_TILES));
+                           72 * 1024);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(place_upsweep_kernel<LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(MAX_TILES * 4));
@@ -554,11 +583,11 @@ static int launch_sort_bin_t(int ec, uint32_t nb, const BlockTable& bt, int pass
   const size_t psm = place_down_smem(rp.ntiles);
   const int S = place_segments(rp.ntiles);
   if (rp.ntiles <= 256)
-    place_downsweep_kernel<8, LOOP><<<g2, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+    place_downsweep_kernel<8, LOOP><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   else if (rp.ntiles <= 2048)
-    place_downsweep_kernel<11, LOOP><<<g2, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+    place_downsweep_kernel<11, LOOP><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   else
-    place_downsweep_kernel<13, LOOP><<<g2, SB_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+    place_downsweep_kernel<13, LOOP><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   return launches + 3;
 }
 
