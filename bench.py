@@ -327,8 +327,8 @@ def main():
     bytes_proj = scene.n * 56 + n_vis * 64
     if names[dom] == "raster":
         ach = flops / (stage_ms[2] / 1000.0) / 1e12
-        tr, src = ncu_traffic("raster2_kernel")
-        roof = {"kernel": "raster2_kernel (K6)", "bound": "alu", "achieved": ach, "peak": alu_peak,
+        tr, src = ncu_traffic("raster_warp_kernel")
+        roof = {"kernel": "raster_warp_kernel (K6)", "bound": "alu", "achieved": ach, "peak": alu_peak,
                 "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": tr,
                 "traffic_note": f"DRAM bytes per launch (one {args.chunk or 1024}-env chunk) from {src}" if tr else None,
                 "peak_basis": f"148 SM x 128 FP32 lanes x 2 (FFMA) x {clock_mhz:.0f} MHz median SM clock under load",

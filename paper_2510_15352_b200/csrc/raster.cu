@@ -23,8 +23,6 @@
 // holds into a per-warp list (ballot + popc, order preserved) and walks only
 // that list, so work is spent only where the cutoff can be passed — this never changes a blend decision.  Early-out:
 // warp vote ends a warp's walk; __syncthreads_count ends the tile.
-#include <cstdlib>
-
 #include "gg_internal.cuh"
 #include "f32x2.cuh"
 
@@ -195,147 +193,11 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
 }
 
 // ---------------------------------------------------------------------------
-// Timed-path variant: 2 pixels per thread with packed f32x2 arithmetic
-// (FFMA2/FADD2/FMUL2).  128 threads per tile; warp w covers an 8x8 block,
-// lane (lx, ly) owns pixels (lx, ly) and (lx, ly + 4) of it.  The per-pixel
-// operation sequence is identical to blend_step (same fma order), so the
-// images are bit-identical to the 256-thread reference walk.
-constexpr int R2_THREADS = 128;
-
-__global__ void __launch_bounds__(R2_THREADS, 10)
-raster2_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
-               float* __restrict__ depth, float* __restrict__ alpha_out) {
-  constexpr int BATCH = 256;
-  __shared__ float4 srec[BATCH * 3];            // rec0 (u,v,L,z), rec1 (A',B',C',ex), rec2 (r,g,b,ey)
-  __shared__ uint8_t smask[BATCH];
-  __shared__ uint8_t wlist[R2_THREADS / 32][BATCH];
-  const int eloc = blockIdx.y;
-  const int tile = blockIdx.x;
-  const int e = envs[e0 + eloc].out_index;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tx = tile % rp.TX, ty = tile / rp.TX;
-  const int bx = warp & 1, by = warp >> 1;
-  const int px = tx * TILE + bx * 8 + (lane & 7);
-  const int py0 = ty * TILE + by * 8 + (lane >> 3), py1 = py0 + 4;
-  const bool in0 = px < rp.W && py0 < rp.H, in1 = px < rp.W && py1 < rp.H;
-  const float fpx = (float)px + 0.5f;
-  const f2 FPX = pk(fpx, fpx), FPY = pk((float)py0 + 0.5f, (float)py1 + 0.5f);
-  const float tx0 = (float)(tx * TILE) + 0.5f, ty0 = (float)(ty * TILE) + 0.5f;
-
-  const uint2 rg = chunk_ok(ws.ok) ? ws.ranges[(size_t)eloc * rp.ntiles + tile] : make_uint2(0u, 0u);
-  const uint64_t rb = ws.rec_base[eloc];
-  const uint32_t* __restrict__ list = ws.sorted + ws.k_base[eloc];
-
-  f2 T = pk(1.f, 1.f), Cr = pk(0.f, 0.f), Cg = Cr, Cb = Cr, Dn = Cr, Aw = Cr;
-  bool done0 = !in0, done1 = !in1;
-
-  for (uint32_t b = rg.x; b < rg.y; b += BATCH) {
-    const uint32_t n = min((uint32_t)BATCH, rg.y - b);
-    __syncthreads();
-    for (uint32_t i = tid; i < n; i += R2_THREADS) {
-      const uint64_t r = rb + __ldg(&list[b + i]);
-      const float4 a0 = __ldg(&ws.rec0[r]);
-      const float4 a1 = __ldg(&ws.rec1[r]);
-      const float4 a2 = __ldg(&ws.rec2[r]);
-      srec[3 * i] = a0;
-      srec[3 * i + 1] = a1;
-      srec[3 * i + 2] = a2;
-      uint32_t m = 0;
-      if (a1.w >= 0.f) {
-        const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const float cx0 = tx0 + 8.f * (w & 1), cy0 = ty0 + 8.f * (w >> 1);
-          if (xh >= cx0 && xl <= cx0 + 7.f && yh >= cy0 && yl <= cy0 + 7.f) m |= 1u << w;
-        }
-      }
-      smask[i] = (uint8_t)m;
-    }
-    __syncthreads();
-    if (!__all_sync(0xffffffffu, done0 && done1)) {
-      uint32_t cnt = 0;
-      const uint32_t lt = (1u << lane) - 1u;
-      for (uint32_t g = 0; g < n; g += 32) {
-        const uint32_t j = g + lane;
-        const bool mine = j < n && ((smask[j] >> warp) & 1u);
-        const uint32_t m = __ballot_sync(0xffffffffu, mine);
-        if (mine) wlist[warp][cnt + __popc(m & lt)] = (uint8_t)j;
-        cnt += __popc(m);
-      }
-      __syncwarp();
-      for (uint32_t i = 0; i < cnt; ++i) {
-        // scalar record fields broadcast to both lanes (FFMA2 .F32 operands)
-        const float4* q = &srec[3 * wlist[warp][i]];
-        const float4 r0 = q[0], r1 = q[1];
-        const float L = r0.z;
-        const f2 dx = sub2(pk(r0.x, r0.x), FPX), dy = sub2(pk(r0.y, r0.y), FPY);
-        const f2 t = fma2(pk(r1.x, r1.x), dx, mul2(pk(r1.y, r1.y), dy));
-        const f2 s = fma2(mul2(pk(r1.z, r1.z), dy), dy, pk(L, L));
-        float x0, x1;
-        upk(fma2(dx, t, s), x0, x1);
-        x0 = fminf(x0, L);
-        x1 = fminf(x1, L);
-        const bool p0 = !done0 && x0 >= LOG2_CUTOFF;
-        const bool p1 = !done1 && x1 >= LOG2_CUTOFF;
-        if (p0 || p1) {
-          const float a0 = p0 ? fminf(0.99f, ex2_approx(x0)) : 0.f;
-          const float a1 = p1 ? fminf(0.99f, ex2_approx(x1)) : 0.f;
-          f2 W = mul2(pk(a0, a1), T);
-          f2 TN = sub2(T, W);
-          float tn0, tn1;
-          upk(TN, tn0, tn1);
-          const bool s0 = p0 && tn0 < 1e-4f, s1 = p1 && tn1 < 1e-4f;
-          if (s0 || s1) {   // stopping pixel: not blended, transmittance kept
-            float w0, w1, t0, t1;
-            upk(W, w0, w1);
-            upk(T, t0, t1);
-            done0 |= s0;
-            done1 |= s1;
-            W = pk(s0 ? 0.f : w0, s1 ? 0.f : w1);
-            TN = pk(s0 ? t0 : tn0, s1 ? t1 : tn1);
-          }
-          const float4 r2 = q[2];
-          Cr = fma2(W, pk(r2.x, r2.x), Cr);
-          Cg = fma2(W, pk(r2.y, r2.y), Cg);
-          Cb = fma2(W, pk(r2.z, r2.z), Cb);
-          Dn = fma2(W, pk(r0.w, r0.w), Dn);
-          Aw = add2(Aw, W);
-          T = TN;
-        }
-        if ((i & 15) == 15 && __all_sync(0xffffffffu, done0 && done1)) break;
-      }
-    }
-    if (__syncthreads_count(done0 && done1) == R2_THREADS) break;
-  }
-
-  float t[2], cr[2], cg[2], cb[2], dn[2], aw[2];
-  upk(T, t[0], t[1]); upk(Cr, cr[0], cr[1]); upk(Cg, cg[0], cg[1]); upk(Cb, cb[0], cb[1]);
-  upk(Dn, dn[0], dn[1]); upk(Aw, aw[0], aw[1]);
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    if (!(k == 0 ? in0 : in1)) continue;
-    const int py = k == 0 ? py0 : py1;
-    const size_t p = ((size_t)e * rp.H + py) * rp.W + px;
-    const float r = fmaf(t[k], rp.bg[0], cr[k]), g = fmaf(t[k], rp.bg[1], cg[k]), bl = fmaf(t[k], rp.bg[2], cb[k]);
-    if (rgb) {
-      if (rp.rgb_format == 0) {
-        uint8_t* o = reinterpret_cast<uint8_t*>(rgb) + p * 3;
-        o[0] = (uint8_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 255.f);
-        o[1] = (uint8_t)__float2uint_rn(fminf(fmaxf(g, 0.f), 1.f) * 255.f);
-        o[2] = (uint8_t)__float2uint_rn(fminf(fmaxf(bl, 0.f), 1.f) * 255.f);
-      } else {
-        float* o = reinterpret_cast<float*>(rgb) + p * 3;
-        o[0] = r; o[1] = g; o[2] = bl;
-      }
-    }
-    if (depth) depth[p] = aw[k] > 0.f ? dn[k] / aw[k] : 0.f;
-    if (alpha_out) alpha_out[p] = aw[k];
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-independent variant (timed path).  Same pixel mapping and per-pixel
-// arithmetic as raster2, but no CTA-wide batches: each warp streams the
+// Timed path: 128 threads per (tile, env); warp w covers an 8x8 block and
+// lane (lx, ly) owns its pixels (lx, ly) and (lx, ly + 4), both evaluated
+// with packed f32x2 arithmetic (FFMA2/FADD2/FMUL2) in the same per-pixel
+// operation order as blend_step, so the images are bit-identical to the
+// 256-thread walk above.  No CTA-wide batches: each warp streams the
 // tile's sorted list 32 records at a time for its own 8x8 block, keeps the
 // records whose alpha >= 1/255 region can reach the block (compacted in list
 // order into a per-warp shared buffer), walks them, and leaves the tile as
@@ -349,7 +211,7 @@ raster2_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, Chunk
 // dy = -B'e / (2C') clamped to the edge (and symmetrically for dy = e).  The
 // record is kept if the maximum over the four edges reaches the cutoff minus
 // a rounding margin that covers the f32 evaluation of every pixel.
-constexpr int R3_THREADS = 128;
+constexpr int RW_THREADS = 128;
 
 __device__ __forceinline__ float edge_max(float a, float b, float c, float e, float lo, float hi) {
   // max over t in [lo, hi] of a e^2 + b e t + c t^2  (c < 0)
@@ -369,11 +231,10 @@ __device__ __forceinline__ bool block_hit(const float4 a0, const float4 a1, floa
   return m + a0.z >= LOG2_CUTOFF - (0.01f + mag * 1.2e-5f);
 }
 
-template <int MINB>
-__global__ void __launch_bounds__(R3_THREADS, MINB)
-raster3_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
+__global__ void __launch_bounds__(RW_THREADS, 8)
+raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
                float* __restrict__ depth, float* __restrict__ alpha_out) {
-  __shared__ float4 srec[R3_THREADS / 32][32 * 3];
+  __shared__ float4 srec[RW_THREADS / 32][32 * 3];
   const int eloc = blockIdx.y;
   const int tile = blockIdx.x;
   const int e = envs[e0 + eloc].out_index;
@@ -489,24 +350,6 @@ raster3_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, Chunk
   }
 }
 
-static int raster_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("GG_RASTER");
-    v = (s && s[0] == '2') ? 2 : 3;
-  }
-  return v;
-}
-
-static int raster3_minb() {
-  static int v = -1;
-  if (v < 0) {
-    const char* s = getenv("GG_R3MB");
-    v = s ? atoi(s) : 8;
-  }
-  return v;
-}
-
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s) {
@@ -514,14 +357,8 @@ void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp,
   dim3 grid(rp.ntiles, ec);
   if (counters)
     raster_kernel<true><<<grid, TILE_PX, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha, co);
-  else if (raster_variant() == 2)
-    raster2_kernel<<<grid, R2_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
-  else if (raster3_minb() == 12)
-    raster3_kernel<12><<<grid, R3_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
-  else if (raster3_minb() == 10)
-    raster3_kernel<10><<<grid, R3_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
   else
-    raster3_kernel<8><<<grid, R3_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
+    raster_warp_kernel<<<grid, RW_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
 }
 
 }  // namespace gg

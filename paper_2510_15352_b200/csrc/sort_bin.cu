@@ -167,68 +167,78 @@ __global__ void __launch_bounds__(DS_RADIX) depth_scan_kernel(BlockTable bt, uin
 }
 
 struct DownSmem {
-  uint32_t wcnt[DS_WARPS][DS_RADIX];   // per-warp digit counts -> offsets (64 KB)
+  union {
+    struct {                                   // ranking
+      uint32_t wcnt[DS_WARPS][DS_RADIX / 2];   // per-warp digit counts -> offsets, packed u16 pairs (32 KB)
+      uint32_t pm[DS_WARPS][32];               // peer masks by representative lane
+      uint8_t st[DS_WARPS][DS_RADIX];          // last lane that stamped each digit (warp-private)
+    } r;
+    struct {                                   // staging in digit order (after ranking)
+      uint32_t sk[SORT_BLK];
+      uint32_t sv[SORT_BLK];
+    } o;
+  } u;
   uint32_t dstart[DS_RADIX];
   uint32_t wsum[32];
-  uint32_t sk[SORT_BLK];
-  uint32_t sv[SORT_BLK];
 };
 
 // Stable block-local ranking: element (warp w, round j, lane l) has block
 // index 256 w + 32 j + l and digit d[j].  lpos[j] = position in the block
-// sorted stably by digit; sm.dstart = digit starts.  wcnt zero on entry/exit.
+// sorted stably by digit; sm.dstart = digit starts.  Equal digits among a
+// warp's 32 lanes are found through a warp-private stamp per digit (the last
+// lane to stamp it is the digits' representative) and one shared-memory OR
+// into the representative's peer mask.  u.r is zero on entry; on exit it is
+// free (the caller stages into u.o).
 __device__ __forceinline__ void block_rank(const uint32_t (&d)[DS_IPT], uint32_t n, uint32_t (&lpos)[DS_IPT],
                                            DownSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = lanemask_lt();
+  uint32_t* wc = sm.u.r.wcnt[warp];
+  uint32_t* pm = sm.u.r.pm[warp];
+  uint8_t* st = sm.u.r.st[warp];
   uint32_t rk[DS_IPT];
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t e = warp * 32 * DS_IPT + j * 32 + lane;
     const bool ok = e < n;
-    const uint32_t active = __ballot_sync(0xffffffffu, ok);
-    rk[j] = 0;
-    if (active) {
-      const uint32_t peers = peers_of(d[j], DS_BITS, active);
-      const uint32_t before = ok ? sm.wcnt[warp][d[j]] : 0u;
-      __syncwarp();
-      if (ok && lane == __ffs(peers) - 1) sm.wcnt[warp][d[j]] = before + __popc(peers);
-      __syncwarp();
-      rk[j] = before + __popc(peers & lt);
-    }
+    const uint32_t dd = d[j];
+    if (ok) st[dd] = (uint8_t)lane;
+    __syncwarp();
+    const uint32_t rep = ok ? st[dd] : 0u;
+    if (ok) atomicOr(&pm[rep], 1u << lane);
+    __syncwarp();
+    const uint32_t peers = ok ? pm[rep] : 0u;
+    const uint32_t before = ok ? (wc[dd >> 1] >> (16 * (dd & 1))) & 0xffffu : 0u;
+    __syncwarp();
+    if (ok && lane == (int)rep) pm[rep] = 0u;
+    if (ok && lane == __ffs(peers) - 1) atomicAdd(&wc[dd >> 1], __popc(peers) << (16 * (dd & 1)));
+    __syncwarp();
+    rk[j] = before + __popc(peers & lt);
   }
   __syncthreads();
-  // per digit: prefix over warps; digit totals -> block-wide exclusive scan
-  uint32_t c[DS_RADIX / DS_THREADS];
-  uint32_t mine = 0;
-#pragma unroll
-  for (int k = 0; k < DS_RADIX / DS_THREADS; ++k) {
-    const int dd = tid * (DS_RADIX / DS_THREADS) + k;
-    uint32_t run = 0;
+  // per digit pair (one packed word per thread): prefix over warps; digit
+  // totals -> block-wide exclusive scan
+  static_assert(DS_RADIX == 2 * DS_THREADS, "one packed digit pair per thread");
+  uint32_t run = 0;
 #pragma unroll 4
-    for (int w = 0; w < DS_WARPS; ++w) {
-      const uint32_t x = sm.wcnt[w][dd];
-      sm.wcnt[w][dd] = run;
-      run += x;
-    }
-    c[k] = run;
-    mine += run;
+  for (int w = 0; w < DS_WARPS; ++w) {
+    const uint32_t x = sm.u.r.wcnt[w][tid];
+    sm.u.r.wcnt[w][tid] = run;
+    run += x;
   }
+  const uint32_t c0 = run & 0xffffu, c1 = run >> 16;
   uint32_t total;
-  uint32_t ex = block_scan(mine, sm.wsum, &total);
-#pragma unroll
-  for (int k = 0; k < DS_RADIX / DS_THREADS; ++k) {
-    sm.dstart[tid * (DS_RADIX / DS_THREADS) + k] = ex;
-    ex += c[k];
-  }
+  const uint32_t ex = block_scan(c0 + c1, sm.wsum, &total);
+  sm.dstart[2 * tid] = ex;
+  sm.dstart[2 * tid + 1] = ex + c0;
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t e = warp * 32 * DS_IPT + j * 32 + lane;
-    lpos[j] = e < n ? sm.dstart[d[j]] + sm.wcnt[warp][d[j]] + rk[j] : 0u;
+    const uint32_t dd = d[j];
+    lpos[j] = e < n ? sm.dstart[dd] + ((wc[dd >> 1] >> (16 * (dd & 1))) & 0xffffu) + rk[j] : 0u;
   }
   __syncthreads();
-  for (int i = tid; i < DS_WARPS * DS_RADIX; i += DS_THREADS) (&sm.wcnt[0][0])[i] = 0u;
 }
 
 __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws, const DepthIO& io, int shift, const uint32_t* ghist, DownSmem& sm) {
@@ -238,7 +248,8 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
   const uint64_t rb = ws.rec_base[e];
   const uint32_t zmin = ws.zmin[e];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < DS_WARPS * DS_RADIX; i += DS_THREADS) (&sm.wcnt[0][0])[i] = 0u;
+  for (int i = tid; i < DS_WARPS * DS_RADIX / 2; i += DS_THREADS) (&sm.u.r.wcnt[0][0])[i] = 0u;
+  for (int i = tid; i < DS_WARPS * 32; i += DS_THREADS) (&sm.u.r.pm[0][0])[i] = 0u;
   uint32_t k[DS_IPT], v[DS_IPT], d[DS_IPT], lp[DS_IPT];
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
@@ -253,21 +264,21 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t i = warp * 32 * DS_IPT + j * 32 + lane;
-    if (i < n) { sm.sk[lp[j]] = k[j]; sm.sv[lp[j]] = v[j]; }
+    if (i < n) { sm.u.o.sk[lp[j]] = k[j]; sm.u.o.sv[lp[j]] = v[j]; }
   }
   __syncthreads();
   const uint32_t* off = ghist + (size_t)b * DS_RADIX;
   for (uint32_t q = tid; q < n; q += DS_THREADS) {
-    const uint32_t kk = sm.sk[q];
+    const uint32_t kk = sm.u.o.sk[q];
     const uint32_t dd = depth_digit(kk, zmin, shift);
     const uint64_t pos = rb + off[dd] + (q - sm.dstart[dd]);
     if (io.kout) io.kout[pos] = kk;
-    io.vout[pos] = sm.sv[q];
+    io.vout[pos] = sm.u.o.sv[q];
   }
 }
 
 template <bool LOOP>
-__global__ void __launch_bounds__(DS_THREADS, 2)
+__global__ void __launch_bounds__(DS_THREADS, 4)
 depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const uint32_t* ghist) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   DownSmem& sm = *reinterpret_cast<DownSmem*>(smem_raw);

@@ -78,7 +78,7 @@ def full(kernel):
 
 agg, tot, nl = launches()
 kern = {}
-for k in ["raster2_kernel", "project_kernel", "cull_count_kernel", "depth_downsweep", "place_downsweep",
+for k in ["raster_warp_kernel", "project_kernel", "cull_count_kernel", "depth_downsweep", "place_downsweep",
           "depth_upsweep", "place_upsweep"]:
     r = full(k)
     if r:
