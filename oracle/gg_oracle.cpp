@@ -213,6 +213,39 @@ bool project_geom(const float* mu, const T cov[6], const Cam& cam, T near_p, T f
   return true;
 }
 
+// Work-reduction variant (reading R35): the
+// paper rect intersected with the tiles whose pixel centres can lie in the
+// axis-aligned box of the alpha >= 1/255 ellipse.  alpha = o exp(-q/2) >=
+// 1/255  <=>  q <= qmax = 2 ln(255 o); the ellipse {d : q(d) <= qm} of the
+// f32 conic [[A,B],[B,C]] has half extents sqrt(qm C / D), sqrt(qm A / D),
+// D = AC - B^2.  qm adds a margin over qmax that covers the f32 evaluation
+// of every pixel, so a dropped tile never holds a pixel that blends the
+// Gaussian: images are unchanged, only the lists get shorter.  qmax is
+// rounded to f32 once per Gaussian; the rest is f64, each op rounded once.
+void tight_rect(Proj& P, float o, int TX, int TY) {
+  (void)TX; (void)TY;
+  const float qmax32 = (float)(2.0 * std::log(255.0 * (double)o));
+  const double qmax = (double)qmax32;
+  if (!(qmax >= 0.0)) { P.x0 = P.x1 = P.y0 = P.y1 = 0; return; }   // o < 1/255: no pixel blends
+  const double A = (double)P.A32, B = (double)P.B32, C = (double)P.C32;
+  const double D = A * C - B * B;            // exact products of f32 values, one rounding
+  if (!(D > 0.0)) return;                     // degenerate conic: keep the paper rect
+  const double ex0 = std::sqrt(qmax * C / D), ey0 = std::sqrt(qmax * A / D);
+  const double mag = (std::fabs(A) * ex0) * ex0 + ((2.0 * std::fabs(B)) * ex0) * ey0 + (std::fabs(C) * ey0) * ey0;
+  const double qm = (qmax + 1e-3) + 1e-5 * mag;
+  const double ex = std::sqrt(qm * C / D) + 1e-3, ey = std::sqrt(qm * A / D) + 1e-3;
+  const double u = (double)P.u32, v = (double)P.v32;
+  // tile t holds pixel centres 16 t + 0.5 .. 16 t + 15.5
+  const double lx = std::ceil((u - ex - 15.5) * 0.0625), hx = std::floor((u + ex - 0.5) * 0.0625) + 1.0;
+  const double ly = std::ceil((v - ey - 15.5) * 0.0625), hy = std::floor((v + ey - 0.5) * 0.0625) + 1.0;
+  const int x0 = (int)std::max((double)P.x0, std::min((double)P.x1, lx));
+  const int x1 = (int)std::max((double)P.x0, std::min((double)P.x1, hx));
+  const int y0 = (int)std::max((double)P.y0, std::min((double)P.y1, ly));
+  const int y1 = (int)std::max((double)P.y0, std::min((double)P.y1, hy));
+  if (x0 >= x1 || y0 >= y1) { P.x0 = P.x1 = P.y0 = P.y1 = 0; return; }
+  P.x0 = x0; P.x1 = x1; P.y0 = y0; P.y1 = y1;
+}
+
 // O2.8 colour (f64): degree 0 from O1, else SH at dir = (mu - C)/|mu - C|.
 void colour_of(const Scene& S, int64_t i, int dr, const Cam& cam, double out[3]) {
   const int K = (S.d + 1) * (S.d + 1);
@@ -257,7 +290,7 @@ struct Result {
   std::vector<float> proj;     // [n*16]
 };
 
-enum { F_NO_EARLY_OUT = 1, F_UNTRUNCATED = 2, F_PLAIN = 4 };
+enum { F_NO_EARLY_OUT = 1, F_UNTRUNCATED = 2, F_PLAIN = 4, F_TIGHT = 8 };
 
 // O4 + O5 for one pixel over an ordered sequence of records.
 struct PixelOut {
@@ -314,7 +347,7 @@ struct OrOpts {
   double background[3];
   int32_t sh_degree;   // -1: scene degree
   int32_t mode;        // 0 = A (f32 canonical projection), 1 = B (f64 projection)
-  int32_t flags;       // F_NO_EARLY_OUT | F_UNTRUNCATED | F_PLAIN
+  int32_t flags;       // F_NO_EARLY_OUT | F_UNTRUNCATED | F_PLAIN | F_TIGHT
 };
 
 void* or_scene_create(int64_t n, int32_t d, const float* means, const float* scales,
@@ -400,9 +433,11 @@ void* or_render_env(const void* scene, const float* view, const float* intr, int
     if (!vis) continue;
     g.o = (double)S.opac[i];
     colour_of(S, i, dr, cam, g.col);
+    if (opt->flags & F_TIGHT) tight_rect(g, S.opac[i], cam.TX, cam.TY);
     R->tile_counts[i] = (g.x1 - g.x0) * (g.y1 - g.y0);
     float* d = &R->proj[i * 16];
-    d[0] = 1.0f; d[1] = g.u32; d[2] = g.v32; d[3] = g.A32; d[4] = g.B32; d[5] = g.C32; d[6] = g.z32;
+    // dump column 0: "has at least one tile"
+    d[0] = R->tile_counts[i] > 0 ? 1.0f : 0.0f; d[1] = g.u32; d[2] = g.v32; d[3] = g.A32; d[4] = g.B32; d[5] = g.C32; d[6] = g.z32;
     d[7] = (float)g.r; d[8] = (float)g.x0; d[9] = (float)g.x1; d[10] = (float)g.y0; d[11] = (float)g.y1;
     d[12] = (float)g.col[0]; d[13] = (float)g.col[1]; d[14] = (float)g.col[2]; d[15] = (float)g.o;
   }
