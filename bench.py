@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--mode", default="sync", choices=["async", "sync"],
                    help="async: sync-free GG_ASYNC render (default); sync: host-sized workspace per chunk")
+    p.add_argument("--tiles", default="tight", choices=["paper", "tight"],
+                   help="tile rects: the paper's 3-sigma circle, or opacity-aware (GG_TIGHT_TILES, identical images)")
     p.add_argument("--blur", type=int, default=0, help="motion blur with K samples (gg_render_blur); 0 = off")
     p.add_argument("--shutter", type=float, default=0.01, help="shutter time (s) for --blur")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -221,7 +223,7 @@ def main():
     use_async = args.mode == "async" and not args.blur
     if use_async:
         gg.gg_reserve_async(R.ctx, E, W, H, args.chunk, 0.7, 4.0)
-    mflag = gg.GG_ASYNC if use_async else 0
+    mflag = (gg.GG_ASYNC if use_async else 0) | (gg.GG_TIGHT_TILES if args.tiles == "tight" else 0)
     n_sets = args.warmup + args.steps
     # a fresh, seeded pose set for every step, all resident in HBM
     vm = np.stack([gi.cameras(10_000 * (rank + 1) + s, E, W, H, scene).viewmats for s in range(n_sets)])
@@ -239,6 +241,7 @@ def main():
 
     def step(s, **kw):
         if args.blur:
+            kw["flags"] = kw.get("flags", 0) | (mflag & gg.GG_TIGHT_TILES)
             gg.gg_render_blur(R.ctx, E, ids, vm_d[s], intr, lin_d, ang_d, args.shutter, args.blur, W, H,
                               gg.default_opts(**kw), rgb, depth, None, stream)
         else:
@@ -298,14 +301,15 @@ def main():
         h_in = np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1))
         h_rgb = torch.empty((E, H, W, 3), dtype=torch.uint8).pin_memory()
         h_depth = torch.empty((E, H, W), dtype=torch.float32).pin_memory() if want_depth else None
-        gg.gg_render_host(R.ctx, E, h_ids, h_vm[0], h_in, W, H, None, h_rgb, h_depth, None, stream)
+        hopts = gg.default_opts(flags=gg.GG_TIGHT_TILES if args.tiles == "tight" else 0)
+        gg.gg_render_host(R.ctx, E, h_ids, h_vm[0], h_in, W, H, hopts, h_rgb, h_depth, None, stream)
         ke = max(2, min(args.steps, 5))
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for k in range(ke):
-            gg.gg_render_host(R.ctx, E, h_ids, h_vm[k % len(h_vm)], h_in, W, H, None, h_rgb, h_depth, None, stream)
+            gg.gg_render_host(R.ctx, E, h_ids, h_vm[k % len(h_vm)], h_in, W, H, hopts, h_rgb, h_depth, None, stream)
         torch.cuda.synchronize()
         dt = max_over_ranks(time.perf_counter() - t0, cdev)
         h2d = E * (4 + 64 + 16)
@@ -362,7 +366,9 @@ def main():
                           "sh_degree": scene.sh_degree, "width": W, "height": H, "depth": want_depth,
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
-                          "chunk_envs": args.chunk or 1024, "render_mode": "async (GG_ASYNC)" if use_async else "sync"},
+                          "chunk_envs": args.chunk or 1024, "render_mode": "async (GG_ASYNC)" if use_async else "sync",
+                          "tile_rects": "opacity-aware (GG_TIGHT_TILES, reading R35)" if args.tiles == "tight"
+                          else "paper 3-sigma circle"},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clocks,
                "counters": {"n_eval": n_eval, "n_contrib": n_contrib, "visible": n_vis, "keys": n_keys,

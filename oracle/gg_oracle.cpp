@@ -218,30 +218,35 @@ bool project_geom(const float* mu, const T cov[6], const Cam& cam, T near_p, T f
 // axis-aligned box of the alpha >= 1/255 ellipse.  alpha = o exp(-q/2) >=
 // 1/255  <=>  q <= qmax = 2 ln(255 o); the ellipse {d : q(d) <= qm} of the
 // f32 conic [[A,B],[B,C]] has half extents sqrt(qm C / D), sqrt(qm A / D),
-// D = AC - B^2.  qm adds a margin over qmax that covers the f32 evaluation
-// of every pixel, so a dropped tile never holds a pixel that blends the
-// Gaussian: images are unchanged, only the lists get shorter.  qmax is
-// rounded to f32 once per Gaussian; the rest is f64, each op rounded once.
-void tight_rect(Proj& P, float o, int TX, int TY) {
-  (void)TX; (void)TY;
-  const float qmax32 = (float)(2.0 * std::log(255.0 * (double)o));
-  const double qmax = (double)qmax32;
-  if (!(qmax >= 0.0)) { P.x0 = P.x1 = P.y0 = P.y1 = 0; return; }   // o < 1/255: no pixel blends
-  const double A = (double)P.A32, B = (double)P.B32, C = (double)P.C32;
-  const double D = A * C - B * B;            // exact products of f32 values, one rounding
-  if (!(D > 0.0)) return;                     // degenerate conic: keep the paper rect
-  const double ex0 = std::sqrt(qmax * C / D), ey0 = std::sqrt(qmax * A / D);
-  const double mag = (std::fabs(A) * ex0) * ex0 + ((2.0 * std::fabs(B)) * ex0) * ey0 + (std::fabs(C) * ey0) * ey0;
-  const double qm = (qmax + 1e-3) + 1e-5 * mag;
-  const double ex = std::sqrt(qm * C / D) + 1e-3, ey = std::sqrt(qm * A / D) + 1e-3;
-  const double u = (double)P.u32, v = (double)P.v32;
+// D = AC - B^2.  Evaluated in f32, each op correctly rounded in this order
+// (it decides integers: the lists), with bounds that make every rounding
+// conservative: D is replaced by a lower bound, the extents are inflated
+// relatively and absolutely, and qm adds a margin over qmax that covers the
+// f32 evaluation of every pixel.  So a dropped tile never holds a pixel that
+// blends the Gaussian: images are unchanged, only the lists get shorter.
+// qmax = f32(2 ln(255 o)) once per Gaussian (f64 log).
+void tight_rect(Proj& P, float o) {
+  const float qmax = (float)(2.0 * std::log(255.0 * (double)o));
+  if (!(qmax >= 0.0f)) { P.x0 = P.x1 = P.y0 = P.y1 = 0; return; }   // o < 1/255: no pixel blends
+  const float A = P.A32, B = P.B32, C = P.C32;
+  const float AC = A * C, BB = B * B;
+  const float Dlo = (AC - BB) - 9.5367431640625e-07f * (AC + BB);     // 2^-20 (AC + BB): D >= Dlo
+  if (!(Dlo > 0.0f) || !(A > 0.0f) || !(C > 0.0f)) return;             // degenerate: keep the paper rect
+  const float rD = 1.0f / Dlo;
+  // |A| ex0^2 + 2|B| ex0 ey0 + |C| ey0^2 at q = qmax, ex0^2 = qmax C / D, ey0^2 = qmax A / D
+  const float mag = ((qmax * rD) * ((2.0f * AC) + (2.0f * std::fabs(B)) * std::sqrt(AC)));
+  const float qm = (qmax + 1e-3f) + 1e-5f * mag;
+  const float grow = 1.0000038146972656f;                              // 1 + 2^-18
+  const float ex = std::sqrt((qm * C) * rD) * grow, ey = std::sqrt((qm * A) * rD) * grow;
+  const float u = P.u32, v = P.v32;
+  const float sx = (ex + 0.02f) + 1e-5f * std::fabs(u), sy = (ey + 0.02f) + 1e-5f * std::fabs(v);
   // tile t holds pixel centres 16 t + 0.5 .. 16 t + 15.5
-  const double lx = std::ceil((u - ex - 15.5) * 0.0625), hx = std::floor((u + ex - 0.5) * 0.0625) + 1.0;
-  const double ly = std::ceil((v - ey - 15.5) * 0.0625), hy = std::floor((v + ey - 0.5) * 0.0625) + 1.0;
-  const int x0 = (int)std::max((double)P.x0, std::min((double)P.x1, lx));
-  const int x1 = (int)std::max((double)P.x0, std::min((double)P.x1, hx));
-  const int y0 = (int)std::max((double)P.y0, std::min((double)P.y1, ly));
-  const int y1 = (int)std::max((double)P.y0, std::min((double)P.y1, hy));
+  const float lx = std::ceil(((u - sx) - 15.5f) * 0.0625f), hx = std::floor(((u + sx) - 0.5f) * 0.0625f) + 1.0f;
+  const float ly = std::ceil(((v - sy) - 15.5f) * 0.0625f), hy = std::floor(((v + sy) - 0.5f) * 0.0625f) + 1.0f;
+  const int x0 = (int)std::max((float)P.x0, std::min((float)P.x1, lx));
+  const int x1 = (int)std::max((float)P.x0, std::min((float)P.x1, hx));
+  const int y0 = (int)std::max((float)P.y0, std::min((float)P.y1, ly));
+  const int y1 = (int)std::max((float)P.y0, std::min((float)P.y1, hy));
   if (x0 >= x1 || y0 >= y1) { P.x0 = P.x1 = P.y0 = P.y1 = 0; return; }
   P.x0 = x0; P.x1 = x1; P.y0 = y0; P.y1 = y1;
 }
@@ -433,7 +438,7 @@ void* or_render_env(const void* scene, const float* view, const float* intr, int
     if (!vis) continue;
     g.o = (double)S.opac[i];
     colour_of(S, i, dr, cam, g.col);
-    if (opt->flags & F_TIGHT) tight_rect(g, S.opac[i], cam.TX, cam.TY);
+    if (opt->flags & F_TIGHT) tight_rect(g, S.opac[i]);
     R->tile_counts[i] = (g.x1 - g.x0) * (g.y1 - g.y0);
     float* d = &R->proj[i * 16];
     // dump column 0: "has at least one tile"

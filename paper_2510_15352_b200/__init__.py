@@ -24,6 +24,7 @@ GG_OK, GG_E_INVALID, GG_E_NONFINITE, GG_E_OOM, GG_E_CUDA, GG_E_BAD_SCENE, GG_E_C
 GG_KEEP_INTERMEDIATES = 1
 GG_COUNTERS = 2
 GG_ASYNC = 4
+GG_TIGHT_TILES = 8          # opacity-aware tile rects (reading R35)
 (GG_DUMP_TILE_COUNTS, GG_DUMP_SORTED_TILE, GG_DUMP_SORTED_ZBITS, GG_DUMP_SORTED_GIDS, GG_DUMP_RANGES,
  GG_DUMP_COUNTERS, GG_DUMP_N_EVAL, GG_DUMP_PROJ) = range(8)
 

@@ -18,7 +18,7 @@ void launch_validate(int64_t n, int K, const float* means, const float* scales, 
                      const float* opac, const float* sh, ValidateOut* out, cudaStream_t s);
 void launch_pack(int64_t n, int K, int sh_stride, const float* means, const float* scales,
                  const float* quats, const float* opac, const float* sh, float4* pos_op, float4* cov_a,
-                 float4* cov_b, float2* aux, float* sh_out, cudaStream_t s);
+                 float4* cov_b, float2* aux, float* qmax, float* sh_out, cudaStream_t s);
 void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, const float* viewmats,
                        const float* intr, const DevScene* scenes, int nscenes, int W, int H, int sh_degree,
                        EnvConst* out, uint32_t* err, cudaStream_t s);
@@ -68,7 +68,7 @@ struct DevBuf {
 
 struct SceneSlot {
   DevScene d{};
-  DevBuf pos_op, cov_a, cov_b, aux, sh;
+  DevBuf pos_op, cov_a, cov_b, aux, qmax, sh;
   bool live = false;
 };
 
@@ -291,7 +291,7 @@ gg_status gg_destroy(gg_context* ctx) {
   cudaDeviceSynchronize();
   for (auto& sc : ctx->scenes) {
     dev_free(ctx, sc.pos_op, s); dev_free(ctx, sc.cov_a, s); dev_free(ctx, sc.cov_b, s);
-    dev_free(ctx, sc.aux, s); dev_free(ctx, sc.sh, s);
+    dev_free(ctx, sc.aux, s); dev_free(ctx, sc.qmax, s); dev_free(ctx, sc.sh, s);
   }
   for (auto& e : ctx->a_ev) cudaEventDestroy(e);
   DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->zmm, &ctx->okflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
@@ -381,16 +381,16 @@ gg_status gg_load_scene(gg_context* ctx, int64_t n, int32_t d, const float* mean
   SceneSlot slot;
   const int sh_stride = d > 0 ? ((K * 3 + 3) / 4) * 4 : 0;
   bool ok = ensure(ctx, slot.pos_op, n * 16, s) && ensure(ctx, slot.cov_a, n * 16, s) &&
-            ensure(ctx, slot.cov_b, n * 16, s) && ensure(ctx, slot.aux, n * 8, s) &&
+            ensure(ctx, slot.cov_b, n * 16, s) && ensure(ctx, slot.aux, n * 8, s) && ensure(ctx, slot.qmax, n * 4, s) &&
             (d == 0 || ensure(ctx, slot.sh, (size_t)n * sh_stride * 4, s));
   if (!ok) {
     for (auto& b : stage) dev_free(ctx, b, s);
     dev_free(ctx, slot.pos_op, s); dev_free(ctx, slot.cov_a, s); dev_free(ctx, slot.cov_b, s);
-    dev_free(ctx, slot.aux, s); dev_free(ctx, slot.sh, s);
+    dev_free(ctx, slot.aux, s); dev_free(ctx, slot.qmax, s); dev_free(ctx, slot.sh, s);
     return fail(ctx, GG_E_OOM, "gg_load_scene: out of device memory for %lld Gaussians", (long long)n);
   }
   launch_pack(n, K, sh_stride, dsrc[0], dsrc[1], dsrc[2], dsrc[3], dsrc[4], P<float4>(slot.pos_op),
-              P<float4>(slot.cov_a), P<float4>(slot.cov_b), P<float2>(slot.aux),
+              P<float4>(slot.cov_a), P<float4>(slot.cov_b), P<float2>(slot.aux), P<float>(slot.qmax),
               d > 0 ? P<float>(slot.sh) : nullptr, s);
   ctx->launches++;
   CK(cudaGetLastError());
@@ -399,6 +399,7 @@ gg_status gg_load_scene(gg_context* ctx, int64_t n, int32_t d, const float* mean
   slot.d.cov_a = P<float4>(slot.cov_a);
   slot.d.cov_b = P<float4>(slot.cov_b);
   slot.d.aux = P<float2>(slot.aux);
+  slot.d.qmax = P<float>(slot.qmax);
   slot.d.sh = d > 0 ? P<float>(slot.sh) : nullptr;
   slot.d.n = (int32_t)n;
   slot.d.degree = d;
@@ -429,7 +430,7 @@ gg_status gg_unload_scene(gg_context* ctx, int32_t id) {
   CK(cudaDeviceSynchronize());
   SceneSlot& sc = ctx->scenes[id];
   dev_free(ctx, sc.pos_op, ctx->own); dev_free(ctx, sc.cov_a, ctx->own); dev_free(ctx, sc.cov_b, ctx->own);
-  dev_free(ctx, sc.aux, ctx->own); dev_free(ctx, sc.sh, ctx->own);
+  dev_free(ctx, sc.aux, ctx->own); dev_free(ctx, sc.qmax, ctx->own); dev_free(ctx, sc.sh, ctx->own);
   sc.live = false;
   sc.d = DevScene{};
   return upload_scene_table(ctx);
@@ -507,6 +508,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   rp.near_p = opts.near_plane; rp.far_p = opts.far_plane;
   rp.bg[0] = opts.background[0]; rp.bg[1] = opts.background[1]; rp.bg[2] = opts.background[2];
   rp.rgb_format = opts.rgb_format;
+  rp.tight = (opts.flags & GG_TIGHT_TILES) != 0;
   const bool counters = (opts.flags & GG_COUNTERS) != 0;
   const bool keep = (opts.flags & GG_KEEP_INTERMEDIATES) != 0 && opts.debug_env >= 0 && opts.debug_env < E;
 
@@ -757,6 +759,7 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
   rp.near_p = opts.near_plane; rp.far_p = opts.far_plane;
   rp.bg[0] = opts.background[0]; rp.bg[1] = opts.background[1]; rp.bg[2] = opts.background[2];
   rp.rgb_format = opts.rgb_format;
+  rp.tight = (opts.flags & GG_TIGHT_TILES) != 0;
   const bool counters = (opts.flags & GG_COUNTERS) != 0;
   const int chunk = ctx->a_chunk, nblk = ctx->a_nblk, nwords = nblk * (PROJ_BLOCK / 32);
   if (nblk < (max_scene_n(ctx) + PROJ_BLOCK - 1) / PROJ_BLOCK)

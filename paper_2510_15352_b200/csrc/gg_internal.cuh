@@ -18,6 +18,7 @@ struct DevScene {
   const float4* cov_a;   // (Sxx, Sxy, Sxz, Syy)
   const float4* cov_b;   // (Syz, Szz, dc_r, dc_g)
   const float2* aux;     // (dc_b, max_j s_j^2)
+  const float* qmax;     // f32(2 ln(255 o)): alpha >= 1/255 <=> q <= qmax (reading R35)
   const float* sh;       // [n][sh_stride] coefficient-major (k, ch), zero padded; null if d = 0
   int32_t n;
   int32_t degree;
@@ -62,6 +63,7 @@ struct RenderParams {
   float near_p, far_p;
   float bg[3];
   int rgb_format;
+  int tight;             // GG_TIGHT_TILES: opacity-aware tile rects (reading R35)
 };
 
 // Workspace pointers for one env chunk (indices are chunk-local envs).

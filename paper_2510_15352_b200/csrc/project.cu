@@ -222,6 +222,34 @@ __device__ __forceinline__ void sh_eval(int deg, float x, float y, float z, floa
   Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
 }
 
+// Opacity-aware tile rect (GG_TIGHT_TILES, reading R35): the
+// paper rect cut to the tiles whose pixel centres can reach the box of the
+// alpha >= 1/255 ellipse {q <= qm} of the f32 conic.  Canonical f32 order
+// with conservative rounding bounds (it decides integers: the tile lists).
+__device__ __forceinline__ void tight_rect(float u, float v, float A, float B, float C, float qmax,
+                                           uint32_t& x0, uint32_t& x1, uint32_t& y0, uint32_t& y1) {
+  if (!(qmax >= 0.f)) { x0 = x1 = y0 = y1 = 0; return; }      // o < 1/255: no pixel blends
+  const float AC = fm(A, C), BB = fm(B, B);
+  const float Dlo = fs(fs(AC, BB), fm(9.5367431640625e-07f, fa(AC, BB)));   // D >= Dlo
+  if (!(Dlo > 0.f) || !(A > 0.f) || !(C > 0.f)) return;        // degenerate: keep the paper rect
+  const float rD = fd(1.f, Dlo);
+  const float mag = fm(fm(qmax, rD), fa(fm(2.f, AC), fm(fm(2.f, fabsf(B)), fsq(AC))));
+  const float qm = fa(fa(qmax, 1e-3f), fm(1e-5f, mag));
+  const float grow = 1.0000038146972656f;                      // 1 + 2^-18
+  const float ex = fm(fsq(fm(fm(qm, C), rD)), grow), ey = fm(fsq(fm(fm(qm, A), rD)), grow);
+  const float sx = fa(fa(ex, 0.02f), fm(1e-5f, fabsf(u))), sy = fa(fa(ey, 0.02f), fm(1e-5f, fabsf(v)));
+  const float lx = ceilf(fm(fs(fs(u, sx), 15.5f), 0.0625f));
+  const float hx = fa(floorf(fm(fs(fa(u, sx), 0.5f), 0.0625f)), 1.f);
+  const float ly = ceilf(fm(fs(fs(v, sy), 15.5f), 0.0625f));
+  const float hy = fa(floorf(fm(fs(fa(v, sy), 0.5f), 0.0625f)), 1.f);
+  const uint32_t nx0 = (uint32_t)fmaxf((float)x0, fminf((float)x1, lx));
+  const uint32_t nx1 = (uint32_t)fmaxf((float)x0, fminf((float)x1, hx));
+  const uint32_t ny0 = (uint32_t)fmaxf((float)y0, fminf((float)y1, ly));
+  const uint32_t ny1 = (uint32_t)fmaxf((float)y0, fminf((float)y1, hy));
+  if (nx0 >= nx1 || ny0 >= ny1) { x0 = x1 = y0 = y1 = 0; return; }
+  x0 = nx0; x1 = nx1; y0 = ny0; y1 = ny1;
+}
+
 constexpr int SH_MAX = 48;              // floats per Gaussian at degree 3
 constexpr int SH_PITCH = PROJ_BLOCK + 1;   // transposed [coefficient][Gaussian], conflict-free
 
@@ -406,6 +434,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
       const float fy1 = fminf(fmaxf(ceilf(fm(fa(v, rr), 0.0625f)), 0.f), (float)rp.TY);
       if (fx0 < fx1 && fy0 < fy1) {
         x0 = (uint32_t)fx0; x1 = (uint32_t)fx1; y0 = (uint32_t)fy0; y1 = (uint32_t)fy1;
+        if (rp.tight) tight_rect(u, v, cA, cB, cC, __ldg(&scn.qmax[gi]), x0, x1, y0, y1);
       }
     }
     const uint32_t ntiles = (x1 - x0) * (y1 - y0);

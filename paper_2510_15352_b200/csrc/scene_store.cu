@@ -34,7 +34,8 @@ __global__ void validate_kernel(int64_t n, int K, const float* __restrict__ mean
 __global__ void pack_kernel(int64_t n, int K, int sh_stride, const float* __restrict__ means,
                             const float* __restrict__ scales, const float* __restrict__ quats,
                             const float* __restrict__ opac, const float* __restrict__ sh,
-                            float4* pos_op, float4* cov_a, float4* cov_b, float2* aux, float* sh_out) {
+                            float4* pos_op, float4* cov_a, float4* cov_b, float2* aux, float* qmax,
+                            float* sh_out) {
   const float SH_C0 = 0.28209479177387814f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -78,6 +79,8 @@ __global__ void pack_kernel(int64_t n, int K, int sh_stride, const float* __rest
     cov_a[i] = make_float4(Sxx, Sxy, Sxz, Syy);
     cov_b[i] = make_float4(Syz, Szz, dc[0], dc[1]);
     aux[i] = make_float2(dc[2], smax * smax);
+    // reading R35: q_max = f32(2 ln(255 o)) from an f64 log (once per Gaussian)
+    qmax[i] = (float)__dmul_rn(2.0, log(__dmul_rn(255.0, (double)opac[i])));
     if (sh_out) {
       for (int k = 0; k < sh_stride; ++k)
         sh_out[i * sh_stride + k] = k < K * 3 ? sh[i * K * 3 + k] : 0.f;
@@ -94,11 +97,11 @@ void launch_validate(int64_t n, int K, const float* means, const float* scales, 
 
 void launch_pack(int64_t n, int K, int sh_stride, const float* means, const float* scales,
                  const float* quats, const float* opac, const float* sh, float4* pos_op, float4* cov_a,
-                 float4* cov_b, float2* aux, float* sh_out, cudaStream_t s) {
+                 float4* cov_b, float2* aux, float* qmax, float* sh_out, cudaStream_t s) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
   pack_kernel<<<blocks, 256, 0, s>>>(n, K, sh_stride, means, scales, quats, opac, sh, pos_op, cov_a,
-                                     cov_b, aux, sh_out);
+                                     cov_b, aux, qmax, sh_out);
 }
 
 }  // namespace gg

@@ -51,22 +51,25 @@ def render(gg, r, ids, cams, want_depth=True, want_alpha=True, fmt=0, **kw):
 
 
 def parity_envs(gg, r, scenes, sids, cams, envs, tally, ints=True, sh_degree=-1, background=(0.0, 0.0, 0.0),
-                **kw):
+                tight=False, **kw):
     """Render all envs on the GPU; compare `envs` with the oracle (and their
-    integer artefacts, one debug render per env)."""
+    integer artefacts, one debug render per env).  tight: GG_TIGHT_TILES on
+    the GPU, F_TIGHT in the oracle (reading R35)."""
     kw["background"] = background
-    rgb, depth, alpha = render(gg, r, sids, cams, sh_degree=sh_degree, **kw)
+    gflag = gg.GG_TIGHT_TILES if tight else 0
+    rgb, depth, alpha = render(gg, r, sids, cams, sh_degree=sh_degree, flags=gflag, **kw)
     oscenes = {}
     for e in envs:
         s = int(sids[e])
         if s not in oscenes:
             oscenes[s] = oracle.OracleScene.from_inputs(scenes[s])
         o = oracle.render_env(oscenes[s], cams.viewmats[e], cams.intrinsics[e], cams.width, cams.height,
-                              sh_degree=sh_degree, background=tuple(float(np.float32(b)) for b in background))
+                              sh_degree=sh_degree, background=tuple(float(np.float32(b)) for b in background),
+                              flags=oracle.F_TIGHT if tight else 0)
         tally.add(rgb[e], depth[e], alpha[e], o)
         if ints:
-            render(gg, r, sids, cams, sh_degree=sh_degree, flags=gg.GG_KEEP_INTERMEDIATES | gg.GG_COUNTERS,
-                   debug_env=e, **kw)
+            render(gg, r, sids, cams, sh_degree=sh_degree,
+                   flags=gg.GG_KEEP_INTERMEDIATES | gg.GG_COUNTERS | gflag, debug_env=e, **kw)
             check_integer_dumps(gg, r.ctx, o, scenes[s].n)
             neval = gg.gg_debug_dump(r.ctx, gg.GG_DUMP_N_EVAL).reshape(cams.height, cams.width)
             same = ~o.exempt
