@@ -1,6 +1,6 @@
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -3 gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?; tail -2 gpurun_out/pytest_gpu.log
 B="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu"
-for v in ${VARIANTS:-"--tiles=paper" "--tiles=tight"}; do
-  $B $v > gpurun_out/ab.json 2>gpurun_out/ab.err
-  python -c "import json;d=json.load(open('gpurun_out/ab.json'));print('$v', round(d['value']), d['roofline']['stage_ms_per_step'], d['counters']['per_env'])" || tail -3 gpurun_out/ab.err
+for v in ${VARIANTS:-"X=1"}; do
+  env $v $B > gpurun_out/ab.json 2>gpurun_out/ab.err
+  python -c "import json;d=json.load(open('gpurun_out/ab.json'));print('$v', round(d['value']), d['roofline']['stage_ms_per_step'])" || tail -3 gpurun_out/ab.err
 done

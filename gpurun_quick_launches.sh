@@ -1,4 +1,4 @@
-CMD="python bench.py --envs 1024 --steps 1 --warmup 3 --no-e2e --no-cpu --mode ${MODE:-sync}"
+CMD="python bench.py --envs 1024 --steps 1 --warmup 3 --no-e2e --no-cpu --mode ${MODE:-sync} ${EXTRA}"
 $CMD > gpurun_out/b1024.json 2> gpurun_out/b1024.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_q.csv $CMD > /dev/null 2>&1
 python - <<'PY'

@@ -251,26 +251,21 @@ __device__ __forceinline__ void tight_rect(float u, float v, float A, float B, f
 }
 
 constexpr int SH_MAX = 48;              // floats per Gaussian at degree 3
-constexpr int SH_PITCH = PROJ_BLOCK + 1;   // transposed [coefficient][Gaussian], conflict-free
 
 struct ProjSmem {
   EnvConst cams[ENV_GROUP];
-  float4 pos[PROJ_BLOCK], ca[PROJ_BLOCK], cb[PROJ_BLOCK];
-  float dcb[PROJ_BLOCK];
   uint32_t fw[ENV_GROUP * 8];        // visibility words (env, word)
   uint32_t cnt[ENV_GROUP * 8];       // popc per (env, word), then exclusive prefix within the env
   uint32_t wsum[PROJ_BLOCK / 32];
   uint32_t kacc[ENV_GROUP];
   uint32_t total;
   uint16_t list[ENV_GROUP * PROJ_BLOCK];   // (k << 8) | local
-  __align__(16) float sh[4];         // [SH_MAX][SH_PITCH] when degree > 0 (dynamic tail)
 };
 
-__global__ void __launch_bounds__(PROJ_BLOCK)
+__global__ void __launch_bounds__(PROJ_BLOCK, 4)
 project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
                const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  ProjSmem& sm = *reinterpret_cast<ProjSmem*>(smem_raw);
+  __shared__ ProjSmem sm;
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0 || !chunk_ok(ws.ok)) return;
   const int tid = threadIdx.x;
@@ -278,9 +273,8 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   const int i0 = gblk * PROJ_BLOCK;
   load_group_cams(sm.cams, envs, e0, grp);
   // visibility words of the group -> (Gaussian, env) pair list in (gid, env)
-  // order: lanes that share a Gaussian broadcast its shared-memory SH/geometry
-  // and the few distinct Gaussians of a warp are adjacent (no bank
-  // conflicts).  A record's index is its rank within its env (gid order),
+  // order: lanes that share a Gaussian read the same scene lines (L1
+  // broadcast) and a warp touches only a few adjacent Gaussians.  A record's index is its rank within its env (gid order),
   // which does not depend on which thread computes it.
   if (tid < ENV_GROUP * 8) {
     const int k = tid >> 3, w = tid & 7;
@@ -339,41 +333,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   }
   const uint32_t total = sm.total;
   if (total == 0) return;
-  // stage the block's Gaussians (visible in at least one env of the group)
-  // stage the block's Gaussians of the group's first valid scene; envs of
-  // another scene (mixed groups, async mode) read theirs from global memory
-  int st_k = 0;
-  while (st_k < grp.cnt - 1 && sm.cams[st_k].scene < 0) ++st_k;
-  const EnvConst& c0 = sm.cams[st_k];
-  const int st_scene = c0.scene;
-  const DevScene& sc = scenes[st_scene < 0 ? 0 : st_scene];
-  const int deg = c0.degree;
-  const int K = (deg + 1) * (deg + 1);
-  if (st_scene >= 0 && emask) {   // only Gaussians some env of the group sees
-    const int i = i0 + tid;
-    if (i < c0.n) {
-      sm.pos[tid] = __ldg(&sc.pos_op[i]);
-      sm.ca[tid] = __ldg(&sc.cov_a[i]);
-      sm.cb[tid] = __ldg(&sc.cov_b[i]);
-      sm.dcb[tid] = __ldg(&sc.aux[i]).x;
-    }
-    if (deg > 0 && i < c0.n) {
-      // this thread's Gaussian: 128-bit loads of its SH row, transposed into
-      // [coefficient][Gaussian] so the projection reads are conflict-free
-      const int nf4 = (K * 3 + 3) / 4;
-      const float4* src = reinterpret_cast<const float4*>(sc.sh + (size_t)i * sc.sh_stride);
-#pragma unroll 4
-      for (int q = 0; q < nf4; ++q) {
-        const float4 x = __ldg(&src[q]);
-        sm.sh[(4 * q + 0) * SH_PITCH + tid] = x.x;
-        sm.sh[(4 * q + 1) * SH_PITCH + tid] = x.y;
-        sm.sh[(4 * q + 2) * SH_PITCH + tid] = x.z;
-        sm.sh[(4 * q + 3) * SH_PITCH + tid] = x.w;
-      }
-    }
-  }
-  __syncthreads();
-
+  __syncthreads();   // the pair list is complete
   for (uint32_t s = tid; s < total; s += PROJ_BLOCK) {
     const uint32_t ent = sm.list[s];
     const int k = ent >> 8, l = ent & 255;
@@ -381,12 +341,13 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     const int eloc = grp.elo + k;
     const uint32_t rank = sm.cnt[k * 8 + (l >> 5)] + __popc(sm.fw[k * 8 + (l >> 5)] & ((1u << (l & 31)) - 1u));
     const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + rank;
-    const bool staged = c.scene == st_scene;
     const DevScene& scn = scenes[c.scene];
     const int gi = i0 + l;
-    const float4 g = staged ? sm.pos[l] : __ldg(&scn.pos_op[gi]);
-    const float4 ca = staged ? sm.ca[l] : __ldg(&scn.cov_a[gi]);
-    const float4 cb = staged ? sm.cb[l] : __ldg(&scn.cov_b[gi]);
+    // the scene is read through L1: lanes of a warp share few, adjacent
+    // Gaussians (Gaussian-major pair list), reused by the group's envs
+    const float4 g = __ldg(&scn.pos_op[gi]);
+    const float4 ca = __ldg(&scn.cov_a[gi]);
+    const float4 cb = __ldg(&scn.cov_b[gi]);
     // O2.1 p = R mu + t, 1/z (canonical)
     const float3 p = to_cam(c, g);
     const float rz = fd(1.f, p.z);
@@ -442,7 +403,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     float col[3];
     const int cdeg = c.degree;
     if (cdeg == 0) {
-      col[0] = cb.z; col[1] = cb.w; col[2] = staged ? sm.dcb[l] : __ldg(&scn.aux[gi]).x;
+      col[0] = cb.z; col[1] = cb.w; col[2] = __ldg(&scn.aux[gi]).x;
     } else {
       float dx = g.x - c.C[0], dy = g.y - c.C[1], dz = g.z - c.C[2];
       const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
@@ -451,23 +412,24 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
       sh_eval(cdeg, dx, dy, dz, Y);
       const int Kc = (cdeg + 1) * (cdeg + 1);
       float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-      if (staged) {
+      // 128-bit loads of the coefficient row (coefficient-major (q, ch));
+      // each channel still accumulates q = 0, 1, ... in order
+      const float4* f4 = reinterpret_cast<const float4*>(scn.sh + (size_t)gi * scn.sh_stride);
+      float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          if (q < Kc) {
-            s0 += Y[q] * sm.sh[(q * 3 + 0) * SH_PITCH + l];
-            s1 += Y[q] * sm.sh[(q * 3 + 1) * SH_PITCH + l];
-            s2 += Y[q] * sm.sh[(q * 3 + 2) * SH_PITCH + l];
+      for (int q4 = 0; q4 < SH_MAX / 4; ++q4) {
+        if (4 * q4 < Kc * 3) {
+          const float4 x = __ldg(&f4[q4]);
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int idx = 4 * q4 + m;
+            if (idx < Kc * 3) acc[idx % 3] += Y[idx / 3] * xs[m];
           }
         }
-      } else {
-        const float* f = scn.sh + (size_t)gi * scn.sh_stride;
-        for (int q = 0; q < Kc; ++q) {
-          s0 += Y[q] * __ldg(&f[q * 3 + 0]);
-          s1 += Y[q] * __ldg(&f[q * 3 + 1]);
-          s2 += Y[q] * __ldg(&f[q * 3 + 2]);
-        }
       }
+      s0 = acc[0]; s1 = acc[1]; s2 = acc[2];
+
       col[0] = fminf(1.f, fmaxf(0.f, s0 + 0.5f));
       col[1] = fminf(1.f, fmaxf(0.f, s1 + 0.5f));
       col[2] = fminf(1.f, fmaxf(0.f, s2 + 0.5f));
@@ -501,15 +463,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   if (tid < grp.cnt && sm.kacc[tid]) atomicAdd(&ws.kcnt[grp.elo + tid], sm.kacc[tid]);
 }
 
-size_t project_smem(int degree) {
-  size_t base = offsetof(ProjSmem, sh);
-  base = (base + 15) & ~(size_t)15;
-  return base + (degree > 0 ? (size_t)SH_MAX * SH_PITCH * 4 : 16);
-}
-
-cudaError_t project_init() {
-  return cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)project_smem(3));
-}
+cudaError_t project_init() { return cudaSuccess; }
 
 void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, const float* viewmats,
                        const float* intr, const DevScene* scenes, int nscenes, int W, int H, int sh_degree,
@@ -529,8 +483,7 @@ void launch_scan_blocks(int ec, int nblk, uint32_t* data, uint32_t* totals, cuda
 
 void launch_project(int e0, int ngroups, int nblk, int max_degree, const EnvGroup* groups, const EnvConst* envs,
                     const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
-  project_kernel<<<dim3(ngroups, nblk), PROJ_BLOCK, project_smem(max_degree), s>>>(e0, groups, envs, scenes, rp,
-                                                                                    ws);
+  project_kernel<<<dim3(ngroups, nblk), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws);
 }
 
 }  // namespace gg
