@@ -41,6 +41,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 constexpr float LOG2_CUTOFF = -7.99435343685885793f;   // log2(1/255)
+constexpr float LOG2_099 = -0.014499569695115089f;      // log2(0.99): the alpha cap as an exponent bound
 
 // One pixel-Gaussian step (R12-R15 with the R30 log2-domain cutoff).
 __device__ __forceinline__ void blend_step(const float4 a0, const float4 a1, const float4 a2, float fpx, float fpy,
@@ -51,7 +52,8 @@ __device__ __forceinline__ void blend_step(const float4 a0, const float4 a1, con
   float x = fmaf(dx, fmaf(a1.x, dx, a1.y * dy), fmaf(a1.z * dy, dy, a0.z));
   x = fminf(x, a0.z);
   if (x >= LOG2_CUTOFF) {
-    const float al = fminf(0.99f, ex2_approx(x));
+    // alpha = min(0.99, 2^x) taken as 2^min(x, log2 0.99) (exp2 is monotone)
+    const float al = ex2_approx(fminf(x, LOG2_099));
     const float w = al * T;
     const float Tn = T - w;
     if (Tn < 1e-4f) {
@@ -247,19 +249,21 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
   const float fpx = (float)px + 0.5f;
   const f2 FPX = pk(fpx, fpx), FPY = pk((float)py0 + 0.5f, (float)py1 + 0.5f);
   const float bx0 = (float)(tx * TILE + bx * 8) + 0.5f, by0 = (float)(ty * TILE + by * 8) + 0.5f;
-  float4* wrec = srec[warp];
 
   const uint2 rg = chunk_ok(ws.ok) ? ws.ranges[(size_t)eloc * rp.ntiles + tile] : make_uint2(0u, 0u);
   const uint64_t rb = ws.rec_base[eloc];
   const uint32_t* __restrict__ list = ws.sorted + ws.k_base[eloc];
 
   f2 T = pk(1.f, 1.f), Cr = pk(0.f, 0.f), Cg = Cr, Cb = Cr, Dn = Cr, Aw = Cr;
-  bool done0 = !in0, done1 = !in1;
+  // per-pixel pass threshold: the cutoff while the pixel is live, +inf once
+  // it stopped (or lies outside the image) -- one compare per pixel
+  const float INF = __int_as_float(0x7f800000);
+  float cut0 = in0 ? LOG2_CUTOFF : INF, cut1 = in1 ? LOG2_CUTOFF : INF;
   const uint32_t lt = (1u << lane) - 1u;
 
   uint32_t nidx = rg.x + lane < rg.y ? __ldg(&list[rg.x + lane]) : 0u;
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
-    if (__all_sync(0xffffffffu, done0 && done1)) break;
+    if (__all_sync(0xffffffffu, cut0 == INF && cut1 == INF)) break;
     const bool valid = b + lane < rg.y;
     const uint64_t r = rb + nidx;
     nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
@@ -269,7 +273,9 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
       a0 = __ldg(&ws.rec0[r]);
       a1 = __ldg(&ws.rec1[r]);
       a2 = __ldg(&ws.rec2[r]);
-      if (a1.w >= 0.f) {
+      // o >= 1/255 (else no pixel can pass; this makes the log2 o clamp
+      // irrelevant to the pass decision), extents and exact block test
+      if (a1.w >= 0.f && a0.z >= LOG2_CUTOFF) {
         const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
         mine = xh >= bx0 && xl <= bx0 + 7.f && yh >= by0 && yl <= by0 + 7.f && block_hit(a0, a1, bx0, by0);
       }
@@ -277,50 +283,41 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
     const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (mine) {
       const int pos = __popc(m & lt);
-      wrec[3 * pos] = a0;
-      wrec[3 * pos + 1] = a1;
-      wrec[3 * pos + 2] = a2;
+      srec[warp][3 * pos] = a0;
+      // the extent slot now carries the alpha exponent bound min(log2 o, log2 0.99)
+      srec[warp][3 * pos + 1] = make_float4(a1.x, a1.y, a1.z, fminf(a0.z, LOG2_099));
+      srec[warp][3 * pos + 2] = a2;
     }
     __syncwarp();
     const uint32_t cnt = __popc(m);
     for (uint32_t i = 0; i < cnt; ++i) {
-      const float4* q = &wrec[3 * i];
-      const float4 r0 = q[0], r1 = q[1];
-      const float L = r0.z;
+      const float4 r0 = srec[warp][3 * i], r1 = srec[warp][3 * i + 1];
       const f2 dx = sub2(pk(r0.x, r0.x), FPX), dy = sub2(pk(r0.y, r0.y), FPY);
       const f2 t = fma2(pk(r1.x, r1.x), dx, mul2(pk(r1.y, r1.y), dy));
-      const f2 sv = fma2(mul2(pk(r1.z, r1.z), dy), dy, pk(L, L));
+      const f2 sv = fma2(mul2(pk(r1.z, r1.z), dy), dy, pk(r0.z, r0.z));
       float x0, x1;
       upk(fma2(dx, t, sv), x0, x1);
-      x0 = fminf(x0, L);
-      x1 = fminf(x1, L);
-      const bool p0 = !done0 && x0 >= LOG2_CUTOFF;
-      const bool p1 = !done1 && x1 >= LOG2_CUTOFF;
-      if (p0 || p1) {
-        const float al0 = p0 ? fminf(0.99f, ex2_approx(x0)) : 0.f;
-        const float al1 = p1 ? fminf(0.99f, ex2_approx(x1)) : 0.f;
-        f2 W = mul2(pk(al0, al1), T);
-        f2 TN = sub2(T, W);
-        float tn0, tn1;
-        upk(TN, tn0, tn1);
-        const bool s0 = p0 && tn0 < 1e-4f, s1 = p1 && tn1 < 1e-4f;
-        if (s0 || s1) {   // stopping pixel: not blended, transmittance kept
-          float w0, w1, t0, t1;
-          upk(W, w0, w1);
-          upk(T, t0, t1);
-          done0 |= s0;
-          done1 |= s1;
-          W = pk(s0 ? 0.f : w0, s1 ? 0.f : w1);
-          TN = pk(s0 ? t0 : tn0, s1 ? t1 : tn1);
-        }
-        const float4 r2 = q[2];
-        Cr = fma2(W, pk(r2.x, r2.x), Cr);
-        Cg = fma2(W, pk(r2.y, r2.y), Cg);
-        Cb = fma2(W, pk(r2.z, r2.z), Cb);
-        Dn = fma2(W, pk(r0.w, r0.w), Dn);
-        Aw = add2(Aw, W);
-        T = TN;
-      }
+      const bool p0 = x0 >= cut0, p1 = x1 >= cut1;
+      // Branch-free blend: a pixel that does not pass gets alpha = 0, so
+      // w = 0 and C + 0 c, T - 0 are exact no-ops (bit-identical to skipping).
+      // alpha = min(0.99, 2^min(x, log2 o)) = 2^min(x, log2 o, log2 0.99)
+      const float al0 = p0 ? ex2_approx(fminf(x0, r1.w)) : 0.f;
+      const float al1 = p1 ? ex2_approx(fminf(x1, r1.w)) : 0.f;
+      f2 W = mul2(pk(al0, al1), T);
+      float tn0, tn1;
+      upk(sub2(T, W), tn0, tn1);
+      // a stopping pixel is not blended and keeps T: w *= 0 (exact; w *= 1 otherwise)
+      const bool s0 = p0 && tn0 < 1e-4f, s1 = p1 && tn1 < 1e-4f;
+      W = mul2(W, pk(s0 ? 0.f : 1.f, s1 ? 0.f : 1.f));
+      cut0 = s0 ? INF : cut0;
+      cut1 = s1 ? INF : cut1;
+      const float4 r2 = srec[warp][3 * i + 2];
+      Cr = fma2(W, pk(r2.x, r2.x), Cr);
+      Cg = fma2(W, pk(r2.y, r2.y), Cg);
+      Cb = fma2(W, pk(r2.z, r2.z), Cb);
+      Dn = fma2(W, pk(r0.w, r0.w), Dn);
+      Aw = add2(Aw, W);
+      T = sub2(T, W);   // = T - w, or T unchanged for a stopping pixel (w = 0)
     }
     __syncwarp();
   }
