@@ -482,7 +482,11 @@ gg_status gg_get_stage_ms(gg_context* ctx, float* out3) {
 
 // Core pipeline.  `after_chunk` (optional) is invoked after each chunk's
 // rasterize is enqueued (used by gg_render_host to stream outputs out).
-typedef gg_status (*chunk_cb)(gg_context*, int e0, int ec, void* user);
+// Called after the rasterisation of processing positions [p0, p0 + n) has
+// been enqueued on the render stream (ctx->h_perm maps positions to caller
+// env indices).
+typedef gg_status (*chunk_cb)(gg_context*, int p0, int n, void* user);
+constexpr int HOST_COPY_SLICE = 256;   // envs per raster launch when frames stream to the host
 
 static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
                              const float* intr, int32_t W, int32_t H, const gg_render_opts* opts_in,
@@ -657,10 +661,32 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       if (!ensure(ctx, ctx->dbg_neval, (size_t)W * H * 4, s)) return fail(ctx, GG_E_OOM, "debug alloc");
       dbg_neval = P<int32_t>(ctx->dbg_neval);
     }
-    launch_raster(e0, ec, P<EnvConst>(ctx->envc), rp, ws, rgb, depth, alpha, counters,
-                  counters ? P<unsigned long long>(ctx->counters) : nullptr, dbg_neval, dbg_eloc, s);
-    ctx->launches++;
-    CK(cudaGetLastError());
+    if (cb) {
+      // host path: raster in slices, each slice's frames start copying to the
+      // host while the next slice renders (only the last slice's copy is exposed)
+      for (int s0 = 0; s0 < ec; s0 += HOST_COPY_SLICE) {
+        const int n = std::min(HOST_COPY_SLICE, ec - s0);
+        ChunkWS wss = ws;
+        wss.ranges = ws.ranges + (size_t)s0 * ntiles;
+        wss.rec_base = ws.rec_base + s0;
+        wss.k_base = ws.k_base + s0;
+        wss.vcnt = ws.vcnt + s0;
+        wss.kcnt = ws.kcnt + s0;
+        const int dl = (dbg_eloc >= s0 && dbg_eloc < s0 + n) ? dbg_eloc - s0 : -1;
+        launch_raster(e0 + s0, n, P<EnvConst>(ctx->envc), rp, wss, rgb, depth, alpha, counters,
+                      counters ? P<unsigned long long>(ctx->counters) : nullptr, dl >= 0 ? dbg_neval : nullptr, dl,
+                      s);
+        ctx->launches++;
+        CK(cudaGetLastError());
+        gg_status cs = cb(ctx, e0 + s0, n, cb_user);
+        if (cs != GG_OK) return cs;
+      }
+    } else {
+      launch_raster(e0, ec, P<EnvConst>(ctx->envc), rp, ws, rgb, depth, alpha, counters,
+                    counters ? P<unsigned long long>(ctx->counters) : nullptr, dbg_neval, dbg_eloc, s);
+      ctx->launches++;
+      CK(cudaGetLastError());
+    }
     if (ctx->timing) {
       CK(cudaEventRecord(ctx->ev[3], s));
       CK(cudaEventSynchronize(ctx->ev[3]));
@@ -714,10 +740,6 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
         ctx->d_counters[0] = ctx->d_counters[1] = -1;
         ctx->d_neval.clear();
       }
-    }
-    if (cb) {
-      gg_status cs = cb(ctx, e0, ec, cb_user);
-      if (cs != GG_OK) return cs;
     }
   }
   if (ctx->timing) for (int i = 0; i < 3; ++i) ctx->stage_ms[i] = ms[i];
@@ -893,22 +915,29 @@ struct HostCopy {
   cudaStream_t s;
 };
 
-static gg_status copy_out_chunk(gg_context* ctx, int e0, int ec, void* user) {
+static gg_status copy_out_chunk(gg_context* ctx, int p0, int n, void* user) {
   HostCopy* h = (HostCopy*)user;
   const size_t P_ = (size_t)h->W * h->H;
-  // outputs of this chunk are final once its rasterize completes: the copy
-  // stream waits for that point and overlaps the copy with the next chunk.
+  // the slice's outputs are final once its rasterisation completes: the copy
+  // stream waits for that point and overlaps the copy with later work
   CK(cudaEventRecord(ctx->ev_copy, h->s));
   CK(cudaStreamWaitEvent(ctx->own, ctx->ev_copy, 0));
-  if (h->rgb_h)
-    CK(cudaMemcpyAsync((uint8_t*)h->rgb_h + (size_t)e0 * P_ * h->rgb_px_bytes, h->rgb_d + (size_t)e0 * P_ * h->rgb_px_bytes,
-                       (size_t)ec * P_ * h->rgb_px_bytes, cudaMemcpyDeviceToHost, ctx->own));
-  if (h->depth_h)
-    CK(cudaMemcpyAsync(h->depth_h + (size_t)e0 * P_, h->depth_d + (size_t)e0 * P_, (size_t)ec * P_ * 4,
-                       cudaMemcpyDeviceToHost, ctx->own));
-  if (h->alpha_h)
-    CK(cudaMemcpyAsync(h->alpha_h + (size_t)e0 * P_, h->alpha_d + (size_t)e0 * P_, (size_t)ec * P_ * 4,
-                       cudaMemcpyDeviceToHost, ctx->own));
+  // caller env indices of processing positions [p0, p0 + n), as sorted runs
+  std::vector<int32_t> idx(ctx->h_perm + p0, ctx->h_perm + p0 + n);
+  std::sort(idx.begin(), idx.end());
+  for (size_t a = 0; a < idx.size();) {
+    size_t b = a + 1;
+    while (b < idx.size() && idx[b] == idx[b - 1] + 1) ++b;
+    const size_t e0 = (size_t)idx[a], ec = b - a;
+    if (h->rgb_h)
+      CK(cudaMemcpyAsync((uint8_t*)h->rgb_h + e0 * P_ * h->rgb_px_bytes, h->rgb_d + e0 * P_ * h->rgb_px_bytes,
+                         ec * P_ * h->rgb_px_bytes, cudaMemcpyDeviceToHost, ctx->own));
+    if (h->depth_h)
+      CK(cudaMemcpyAsync(h->depth_h + e0 * P_, h->depth_d + e0 * P_, ec * P_ * 4, cudaMemcpyDeviceToHost, ctx->own));
+    if (h->alpha_h)
+      CK(cudaMemcpyAsync(h->alpha_h + e0 * P_, h->alpha_d + e0 * P_, ec * P_ * 4, cudaMemcpyDeviceToHost, ctx->own));
+    a = b;
+  }
   return GG_OK;
 }
 

@@ -210,6 +210,26 @@ def test_render_host_matches_device(gg, R):
     assert np.array_equal(alpha.numpy(), ref[2])
 
 
+def test_render_host_multi_scene_slices(gg, R):
+    """gg_render_host with a random binding to 3 scenes (processing order !=
+    caller order) and chunks of 512 envs streamed in raster slices: the host
+    frames equal the device render."""
+    scs = [gi.random_cloud(710 + k, 120 + 40 * k, sh_degree=k) for k in range(3)]
+    sids = [load(R, sc) for sc in scs]
+    E, W, H = 600, 32, 32
+    cams = gi.cloud_cameras(710, E, W, H)
+    ids = np.array(sids, np.int32)[gi.rng(gi.KIND_CAMERAS, 711).integers(0, 3, E)]
+    gg.gg_reserve(R.ctx, E, W, H, 512)
+    ref = render(gg, R, ids, cams)
+    rgb = torch.zeros((E, H, W, 3), dtype=torch.uint8).pin_memory()
+    depth = torch.zeros((E, H, W), dtype=torch.float32).pin_memory()
+    alpha = torch.zeros((E, H, W), dtype=torch.float32).pin_memory()
+    gg.gg_render_host(R.ctx, E, ids, cams.viewmats, cams.intrinsics, W, H, None, rgb, depth, alpha)
+    assert np.array_equal(rgb.numpy(), ref[0])
+    assert np.array_equal(depth.numpy(), ref[1])
+    assert np.array_equal(alpha.numpy(), ref[2])
+
+
 def test_errors(gg, R):
     sc = gi.random_cloud(800, 10)
     with pytest.raises(gg.GGError) as ei:
