@@ -486,7 +486,7 @@ gg_status gg_get_stage_ms(gg_context* ctx, float* out3) {
 // been enqueued on the render stream (ctx->h_perm maps positions to caller
 // env indices).
 typedef gg_status (*chunk_cb)(gg_context*, int p0, int n, void* user);
-constexpr int HOST_COPY_SLICE = 256;   // envs per raster launch when frames stream to the host
+constexpr int HOST_COPY_SLICE = 128;   // envs per raster launch when frames stream to the host
 
 static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
                              const float* intr, int32_t W, int32_t H, const gg_render_opts* opts_in,
