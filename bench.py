@@ -128,13 +128,13 @@ def ncu_traffic(kernel: str):
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_summary.json")))
     if not files:
-        return None, None
+        return None, None, None
     try:
         d = json.load(open(files[-1]))
         r = d["full_captures"][kernel]
-        return r.get("dram_bytes_total"), os.path.relpath(files[-1], ROOT)
+        return r.get("dram_bytes_total"), os.path.relpath(files[-1], ROOT), d.get("capture_envs_per_launch")
     except Exception:
-        return None, None
+        return None, None, None
 
 
 def measured_peaks():
@@ -331,10 +331,14 @@ def main():
     bytes_proj = scene.n * 56 + n_vis * 64
     if names[dom] == "raster":
         ach = flops / (stage_ms[2] / 1000.0) / 1e12
-        tr, src = ncu_traffic("raster_warp_kernel")
+        tr, src, cap_envs = ncu_traffic("raster_warp_kernel")
+        launch_envs = min(E, args.chunk or 1024)
+        if tr and cap_envs:
+            tr = tr * launch_envs / cap_envs          # per launch of this run (DRAM bytes scale with envs)
         roof = {"kernel": "raster_warp_kernel (K6)", "bound": "alu", "achieved": ach, "peak": alu_peak,
                 "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": tr,
-                "traffic_note": f"DRAM bytes per launch (one {args.chunk or 1024}-env chunk) from {src}" if tr else None,
+                "traffic_note": (f"DRAM bytes per launch ({launch_envs} envs), scaled from the {cap_envs}-env ncu "
+                                 f"--set full capture in {src}") if tr else None,
                 "peak_basis": f"148 SM x 128 FP32 lanes x 2 (FFMA) x {clock_mhz:.0f} MHz median SM clock under load",
                 "work": f"{n_eval:,} evaluated pairs x {FLOP_EVAL} + {n_contrib:,} blended x {FLOP_CONTRIB} flops"}
     elif names[dom] == "sort_bin":

@@ -79,15 +79,16 @@ def full(kernel):
 agg, tot, nl = launches()
 kern = {}
 for k in ["raster_warp_kernel", "project_kernel", "cull_count_kernel", "depth_downsweep", "place_downsweep",
-          "depth_upsweep", "place_upsweep"]:
+          "depth_upsweep", "place_upsweep", "depth_scan", "place_scan"]:
     r = full(k)
     if r:
         kern[k] = r
 summary = {"round": R, "step_kernel_seconds": tot, "per_kernel_step": agg, "full_captures": kern,
+           "capture_envs_per_launch": 512,
            "notes": "launch list: ncu --metrics gpu__time_duration.sum --clock-control none of "
-                    "`bench.py --steps 2 --warmup 1 --no-e2e --no-cpu` (cold-cache, serialised: compare shares); "
-                    "full captures: ncu --set full on one steady-state launch of each kernel at 512 envs "
-                    "(= one env chunk of the bench workload)."}
+                    "`bench.py --steps 2 --warmup 3 --no-e2e --no-cpu` (cold-cache, serialised: compare shares); "
+                    "full captures: ncu --set full on one steady-state launch of each kernel of "
+                    "`bench.py --envs 512` (one launch = 512 envs; the default bench launch covers 1024)."}
 json.dump(summary, open(os.path.join(DST, "ncu_summary.json"), "w"), indent=1)
 with open(os.path.join(DST, "ncu_summary.md"), "w") as f:
     f.write(f"# ncu summary — {R}\n\nLaunch list (last gg_render of the bench run = one step, {nl} launches "
