@@ -59,6 +59,8 @@ def parse():
                    help="async: sync-free GG_ASYNC render (default); sync: host-sized workspace per chunk")
     p.add_argument("--tiles", default="tight", choices=["paper", "tight"],
                    help="tile rects: the paper's 3-sigma circle, or opacity-aware (GG_TIGHT_TILES, identical images)")
+    p.add_argument("--outputs", default="rgbd", choices=["rgbd", "depth"],
+                   help="rgbd (the headline) or depth-only (rgb = NULL: no SH/colour work; the paper's depth-only baseline)")
     p.add_argument("--blur", type=int, default=0, help="motion blur with K samples (gg_render_blur); 0 = off")
     p.add_argument("--shutter", type=float, default=0.01, help="shutter time (s) for --blur")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -211,7 +213,8 @@ def main():
     cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")   # collective tensors
     c, name = workload(args)
     E, W, H = c["n_envs"], c["width"], c["height"]
-    want_depth = c["depth"]
+    want_depth = c["depth"] or args.outputs == "depth"
+    want_rgb = args.outputs == "rgbd"
 
     # ---- inputs: scene replica + pre-generated pose sets, resident in HBM
     scene = gi.config_scene(args.config, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])
@@ -230,7 +233,7 @@ def main():
     intr = t(np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1)))
     vm_d = t(vm)
     ids = torch.full((E,), sid, dtype=torch.int32, device=dev)
-    rgb = torch.empty((E, H, W, 3), dtype=torch.uint8, device=dev)
+    rgb = torch.empty((E, H, W, 3), dtype=torch.uint8, device=dev) if want_rgb else None
     depth = torch.empty((E, H, W), dtype=torch.float32, device=dev) if want_depth else None
     stream = torch.cuda.current_stream()
 
@@ -299,7 +302,7 @@ def main():
         h_ids = np.full(E, sid, np.int32)
         h_vm = vm[: max(2, min(n_sets, 4))]
         h_in = np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1))
-        h_rgb = torch.empty((E, H, W, 3), dtype=torch.uint8).pin_memory()
+        h_rgb = torch.empty((E, H, W, 3), dtype=torch.uint8).pin_memory() if want_rgb else None
         h_depth = torch.empty((E, H, W), dtype=torch.float32).pin_memory() if want_depth else None
         hopts = gg.default_opts(flags=gg.GG_TIGHT_TILES if args.tiles == "tight" else 0)
         gg.gg_render_host(R.ctx, E, h_ids, h_vm[0], h_in, W, H, hopts, h_rgb, h_depth, None, stream)
@@ -313,7 +316,7 @@ def main():
         torch.cuda.synchronize()
         dt = max_over_ranks(time.perf_counter() - t0, cdev)
         h2d = E * (4 + 64 + 16)
-        d2h = E * W * H * (3 + (4 if want_depth else 0))
+        d2h = E * W * H * ((3 if want_rgb else 0) + (4 if want_depth else 0))
         e2e = {"value": E * world * ke / dt, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": d2h * world, "steps": ke,
                "note": "gg_render_host: pinned host inputs -> device, frames -> pinned host, every step"}
@@ -366,8 +369,8 @@ def main():
         rec = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": tmax_ms / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-               "config": {"workload": name, "envs_per_gpu": E, "total_envs": E * world, "n_gauss": scene.n,
-                          "sh_degree": scene.sh_degree, "width": W, "height": H, "depth": want_depth,
+               "config": {"workload": name + ("" if want_rgb else " [depth-only outputs]"), "envs_per_gpu": E, "total_envs": E * world, "n_gauss": scene.n,
+                          "sh_degree": scene.sh_degree, "width": W, "height": H, "depth": want_depth, "rgb": want_rgb,
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
                           "chunk_envs": args.chunk or 1024, "render_mode": "async (GG_ASYNC)" if use_async else "sync",

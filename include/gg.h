@@ -130,7 +130,10 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t width, int
  *              (+x right, +y down, +z forward) (reading R2); only the top
  *              3x4 block is read
  *   intrinsics DEVICE f32 [E,4] = fx, fy, cx, cy in pixels
- *   rgb        DEVICE [E,H,W,3] u8 (rgb_format 0) or f32 (1), or NULL
+ *   rgb        DEVICE [E,H,W,3] u8 (rgb_format 0) or f32 (1), or NULL.  NULL selects the
+ *              depth-only render (the paper's depth-only baseline): no SH
+ *              colour is evaluated or blended; depth/alpha are bit-identical to the
+ *              RGB+depth render.
  *   depth      DEVICE f32 [E,H,W] expected camera-z depth in metres,
  *              sum(w z)/sum(w), 0 where nothing contributes (reading R14), or NULL
  *   alpha      DEVICE f32 [E,H,W] accumulated alpha sum(w), or NULL

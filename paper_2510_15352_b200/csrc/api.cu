@@ -513,6 +513,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   rp.bg[0] = opts.background[0]; rp.bg[1] = opts.background[1]; rp.bg[2] = opts.background[2];
   rp.rgb_format = opts.rgb_format;
   rp.tight = (opts.flags & GG_TIGHT_TILES) != 0;
+  rp.color = rgb != nullptr;
   const bool counters = (opts.flags & GG_COUNTERS) != 0;
   const bool keep = (opts.flags & GG_KEEP_INTERMEDIATES) != 0 && opts.debug_env >= 0 && opts.debug_env < E;
 
@@ -782,6 +783,7 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
   rp.bg[0] = opts.background[0]; rp.bg[1] = opts.background[1]; rp.bg[2] = opts.background[2];
   rp.rgb_format = opts.rgb_format;
   rp.tight = (opts.flags & GG_TIGHT_TILES) != 0;
+  rp.color = rgb != nullptr;
   const bool counters = (opts.flags & GG_COUNTERS) != 0;
   const int chunk = ctx->a_chunk, nblk = ctx->a_nblk, nwords = nblk * (PROJ_BLOCK / 32);
   if (nblk < (max_scene_n(ctx) + PROJ_BLOCK - 1) / PROJ_BLOCK)

@@ -64,6 +64,7 @@ struct RenderParams {
   float bg[3];
   int rgb_format;
   int tight;             // GG_TIGHT_TILES: opacity-aware tile rects (reading R35)
+  int color;             // 0 = depth-only render (rgb == null): no SH/colour work
 };
 
 // Workspace pointers for one env chunk (indices are chunk-local envs).

@@ -400,9 +400,11 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     }
     const uint32_t ntiles = (x1 - x0) * (y1 - y0);
     // O2.8 colour
-    float col[3];
+    float col[3] = {0.f, 0.f, 0.f};
     const int cdeg = c.degree;
-    if (cdeg == 0) {
+    if (!rp.color) {
+      // depth-only render: no colour is consumed
+    } else if (cdeg == 0) {
       col[0] = cb.z; col[1] = cb.w; col[2] = __ldg(&scn.aux[gi]).x;
     } else {
       float dx = g.x - c.C[0], dy = g.y - c.C[1], dz = g.z - c.C[2];

@@ -233,6 +233,7 @@ __device__ __forceinline__ bool block_hit(const float4 a0, const float4 a1, floa
   return m + a0.z >= LOG2_CUTOFF - (0.01f + mag * 1.2e-5f);
 }
 
+template <bool RGB>   // false: depth-only render (no colour accumulation)
 __global__ void __launch_bounds__(RW_THREADS, 8)
 raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
                float* __restrict__ depth, float* __restrict__ alpha_out) {
@@ -311,10 +312,12 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
       W = mul2(W, pk(s0 ? 0.f : 1.f, s1 ? 0.f : 1.f));
       cut0 = s0 ? INF : cut0;
       cut1 = s1 ? INF : cut1;
-      const float4 r2 = srec[warp][3 * i + 2];
-      Cr = fma2(W, pk(r2.x, r2.x), Cr);
-      Cg = fma2(W, pk(r2.y, r2.y), Cg);
-      Cb = fma2(W, pk(r2.z, r2.z), Cb);
+      if (RGB) {
+        const float4 r2 = srec[warp][3 * i + 2];
+        Cr = fma2(W, pk(r2.x, r2.x), Cr);
+        Cg = fma2(W, pk(r2.y, r2.y), Cg);
+        Cb = fma2(W, pk(r2.z, r2.z), Cb);
+      }
       Dn = fma2(W, pk(r0.w, r0.w), Dn);
       Aw = add2(Aw, W);
       T = sub2(T, W);   // = T - w, or T unchanged for a stopping pixel (w = 0)
@@ -331,7 +334,7 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
     const int py = k == 0 ? py0 : py1;
     const size_t p = ((size_t)e * rp.H + py) * rp.W + px;
     const float r = fmaf(t[k], rp.bg[0], cr[k]), g = fmaf(t[k], rp.bg[1], cg[k]), bl = fmaf(t[k], rp.bg[2], cb[k]);
-    if (rgb) {
+    if (RGB && rgb) {
       if (rp.rgb_format == 0) {
         uint8_t* o = reinterpret_cast<uint8_t*>(rgb) + p * 3;
         o[0] = (uint8_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 255.f);
@@ -354,8 +357,10 @@ void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp,
   dim3 grid(rp.ntiles, ec);
   if (counters)
     raster_kernel<true><<<grid, TILE_PX, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha, co);
+  else if (rgb)
+    raster_warp_kernel<true><<<grid, RW_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
   else
-    raster_warp_kernel<<<grid, RW_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
+    raster_warp_kernel<false><<<grid, RW_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
 }
 
 }  // namespace gg
