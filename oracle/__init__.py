@@ -16,6 +16,7 @@ and camera parameters are not available).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from dataclasses import dataclass
@@ -244,3 +245,47 @@ def render_blur_env(scene: OracleScene, viewmat, intr, width: int, height: int, 
     rgb8 = np.rint(np.clip(rgb, 0.0, 1.0) * 255.0).astype(np.uint8)   # numpy rint = half-to-even
     exempt = np.any([s.exempt for s in samples], axis=0)
     return BlurResult(rgb, rgb8, samples[K // 2].depth, alpha, exempt, samples[K // 2].alpha, samples)
+
+
+# ---------------------------------------------------------------- DinoV2 input
+# SURVEY §8(f) row 4 ("fused render -> DinoV2 input (224^2 resize, normalise,
+# bf16 planar)"); PAPER.md:253 feeds DinoV2 "the raw RGB frame".  Reading R36
+# (DESIGN.md): the whole u8 frame is resized to S x S by bilinear
+# interpolation with half-pixel centres (src = (dst + 0.5) * in/out - 0.5,
+# clamped at 0; the upper neighbour clamped to the last pixel), no
+# antialiasing; values u8/255 are normalised with the ImageNet mean/std
+# DinoV2 was trained with; output is channel-planar [3, S, S].
+IMAGENET_MEAN = (0.485, 0.456, 0.406)
+IMAGENET_STD = (0.229, 0.224, 0.225)
+
+
+def _bilinear_axis(n_in: int, n_out: int):
+    """Per output index: (lower index, upper index, upper weight), f64."""
+    scale = n_in / n_out
+    lo = np.zeros(n_out, np.int64)
+    hi = np.zeros(n_out, np.int64)
+    w = np.zeros(n_out, np.float64)
+    for d in range(n_out):
+        src = max((d + 0.5) * scale - 0.5, 0.0)
+        i0 = int(math.floor(src))
+        i0 = min(i0, n_in - 1)
+        lo[d] = i0
+        hi[d] = min(i0 + 1, n_in - 1)
+        w[d] = src - i0
+    return lo, hi, w
+
+
+def dino_input(rgb_u8, size: int = 224) -> np.ndarray:
+    """[H, W, 3] u8 frame -> [3, size, size] f64 normalised DinoV2 input."""
+    img = np.asarray(rgb_u8, np.float64) / 255.0
+    H, W = img.shape[0], img.shape[1]
+    ylo, yhi, wy = _bilinear_axis(H, size)
+    xlo, xhi, wx = _bilinear_axis(W, size)
+    out = np.zeros((3, size, size), np.float64)
+    for c in range(3):
+        ch = img[:, :, c]
+        top = ch[ylo][:, xlo] * (1.0 - wx)[None, :] + ch[ylo][:, xhi] * wx[None, :]
+        bot = ch[yhi][:, xlo] * (1.0 - wx)[None, :] + ch[yhi][:, xhi] * wx[None, :]
+        v = top * (1.0 - wy)[:, None] + bot * wy[:, None]
+        out[c] = (v - IMAGENET_MEAN[c]) / IMAGENET_STD[c]
+    return out
