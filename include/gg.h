@@ -187,6 +187,16 @@ gg_status gg_checksum(gg_context* ctx, int32_t n_envs, int32_t width, int32_t he
                       const void* rgb, int32_t rgb_format, const float* depth, uint64_t* out,
                       void* stream);
 
+/* Rendered frames -> DinoV2 input ("DinoV2
+ * embeddings extracted from the raw RGB frame"; reading R36):
+ *   rgb   DEVICE u8 [E,H,W,3] (gg_render's rgb_format 0 output)
+ *   out   DEVICE bf16 [E,3,S,S]: bilinear resize (half-pixel centres, no
+ *         antialiasing) of the whole frame to S x S, /255, ImageNet mean/std,
+ *         round-to-nearest-even, channel-planar.  Caller-owned.
+ * Enqueued on `stream`; GG_E_INVALID for null pointers or sizes <= 0. */
+gg_status gg_dino_input(gg_context* ctx, int32_t n_envs, int32_t width, int32_t height, const uint8_t* rgb,
+                        int32_t size, void* out_bf16, void* stream);
+
 /* 3DGS binary PLY scenes (SPEC.md:51-59 load_splat_ply).
  * gg_read_ply parses `path` into ACTIVATED host arrays (scale = exp,
  * opacity = sigmoid, quaternion = rot_0..3 as (w,x,y,z), SH reordered from

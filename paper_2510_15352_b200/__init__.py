@@ -32,7 +32,7 @@ GG_TIGHT_TILES = 8          # opacity-aware tile rects (reading R35)
 EXPORTS = ["gg_default_opts", "gg_create", "gg_destroy", "gg_load_scene", "gg_unload_scene", "gg_reserve",
            "gg_render", "gg_render_host", "gg_render_blur", "gg_blur_poses", "gg_checksum", "gg_check_errors", "gg_debug_dump", "gg_get_counters",
            "gg_launch_count", "gg_set_timing", "gg_get_stage_ms", "gg_last_error", "gg_status_string",
-           "gg_read_ply", "gg_load_ply", "gg_ply_error", "gg_reserve_async"]
+           "gg_read_ply", "gg_load_ply", "gg_ply_error", "gg_reserve_async", "gg_dino_input"]
 
 
 class GGError(RuntimeError):
@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH):
                                  vp, vp, vp, vp]
     L.gg_blur_poses.argtypes = [vp, i32, vp, vp, vp, C.c_float, i32, vp, vp]
     L.gg_checksum.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp, vp]
+    L.gg_dino_input.argtypes = [vp, i32, i32, i32, vp, i32, vp, vp]
     L.gg_check_errors.argtypes = [vp, vp]
     L.gg_debug_dump.argtypes = [vp, i32, vp, i64, C.POINTER(i64)]
     L.gg_get_counters.argtypes = [vp, i32, vp]
@@ -237,6 +238,12 @@ def gg_blur_poses(ctx, n_envs, viewmats, lin_vel, ang_vel, shutter, K, out, stre
 def gg_checksum(ctx, n_envs, width, height, rgb, rgb_format, depth, out, stream=None):
     _check(ctx, load_library().gg_checksum(ctx, int(n_envs), int(width), int(height), _ptr(rgb), int(rgb_format),
                                            _ptr(depth), _ptr(out), _stream_handle(stream)))
+
+
+def gg_dino_input(ctx, n_envs, width, height, rgb, size, out, stream=None):
+    """u8 [E,H,W,3] device frames -> bf16 [E,3,size,size] DinoV2 input (R36)."""
+    _check(ctx, load_library().gg_dino_input(ctx, int(n_envs), int(width), int(height), _ptr(rgb), int(size),
+                                             _ptr(out), _stream_handle(stream)))
 
 
 def gg_check_errors(ctx, stream=None):

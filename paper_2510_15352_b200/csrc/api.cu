@@ -50,6 +50,7 @@ void launch_tables_k(int ec, const uint32_t* vcnt, const uint32_t* kcnt, uint64_
                      int sort_blk, uint64_t kcap, uint64_t nbcap, uint32_t* ok, uint32_t* err, cudaStream_t s);
 void launch_checksum(int E, int W, int H, const uint8_t* rgb8, const float* rgbf, const float* depth,
                      unsigned long long* out, cudaStream_t s);
+void launch_dino_input(int E, int W, int H, int S, const uint8_t* rgb, void* out, cudaStream_t s);
 int launch_copy_words(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void launch_debug_records(uint32_t V, uint64_t rb, const ChunkWS& ws, int32_t* tile_counts, float* proj,
                           cudaStream_t s);
@@ -1036,6 +1037,18 @@ gg_status gg_render_blur(gg_context* ctx, int32_t E, const int32_t* scene_ids, c
     ctx->launches++;
     CK(cudaGetLastError());
   }
+  return GG_OK;
+}
+
+gg_status gg_dino_input(gg_context* ctx, int32_t E, int32_t W, int32_t H, const uint8_t* rgb, int32_t S,
+                        void* out, void* stream) {
+  if (!ctx) return GG_E_INVALID;
+  if (E <= 0 || W <= 0 || H <= 0 || S <= 0 || !rgb || !out)
+    return fail(ctx, GG_E_INVALID, "gg_dino_input: bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  launch_dino_input(E, W, H, S, rgb, out, (cudaStream_t)stream);
+  ctx->launches++;
+  CK(cudaGetLastError());
   return GG_OK;
 }
 
