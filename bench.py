@@ -59,8 +59,9 @@ def parse():
                    help="async: sync-free GG_ASYNC render (default); sync: host-sized workspace per chunk")
     p.add_argument("--tiles", default="tight", choices=["paper", "tight"],
                    help="tile rects: the paper's 3-sigma circle, or opacity-aware (GG_TIGHT_TILES, identical images)")
-    p.add_argument("--outputs", default="rgbd", choices=["rgbd", "depth"],
-                   help="rgbd (the headline) or depth-only (rgb = NULL: no SH/colour work; the paper's depth-only baseline)")
+    p.add_argument("--outputs", default="rgbd", choices=["rgbd", "rgb", "depth"],
+                   help="rgbd (the headline), rgb only, or depth-only (rgb = NULL: no SH/colour work; the paper's "
+                        "depth-only baseline)")
     p.add_argument("--blur", type=int, default=0, help="motion blur with K samples (gg_render_blur); 0 = off")
     p.add_argument("--shutter", type=float, default=0.01, help="shutter time (s) for --blur")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -139,6 +140,16 @@ def ncu_traffic(kernel: str):
         return None, None, None
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def measured_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -183,7 +194,7 @@ def run_reference(args):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
            "data": "synthetic", "config": {"workload": name, "sample_per_step": "1 env (of the config's "
                                            f"{c['n_envs']} envs/GPU)"},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                             "sample": f"{args.steps} envs, one per step, {c['width']}x{c['height']}, "
                                       f"{c['n_gauss']:,} Gaussians SH{c['sh_degree']}"},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -213,8 +224,8 @@ def main():
     cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")   # collective tensors
     c, name = workload(args)
     E, W, H = c["n_envs"], c["width"], c["height"]
-    want_depth = c["depth"] or args.outputs == "depth"
-    want_rgb = args.outputs == "rgbd"
+    want_depth = (c["depth"] and args.outputs != "rgb") or args.outputs == "depth"
+    want_rgb = args.outputs != "depth"
 
     # ---- inputs: scene replica + pre-generated pose sets, resident in HBM
     scene = gi.config_scene(args.config, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])
@@ -355,13 +366,42 @@ def main():
     roof["stage_ms_per_step"] = {n: float(v) for n, v in zip(names, stage_ms)}
     roof["stage_share"] = {n: float(v / max(stage_ms.sum(), 1e-9)) for n, v in zip(names, stage_ms)}
 
+    # ---- whole-path roofline: each stage's algorithmic work on
+    # its bounding resource, summed, against the measured stage times
+    lane_ops = SM_COUNT * FP32_LANES * clock_mhz * 1e6             # FP32 lane-ops/s
+    ex2_rate = SM_COUNT * 16 * clock_mhz * 1e6                      # MUFU ex2/s
+    hbm = hbm_peak * 1e9
+    sh_eff = scene.sh_degree if want_rgb else 0
+    b_g = 60 + (4 * 3 * (sh_eff + 1) ** 2 if sh_eff > 0 else 0)     # scene bytes per Gaussian
+    ops_proj = E * scene.n * 25 + n_vis * (150 + (130 if sh_eff > 0 else 0))
+    by_proj = scene.n * b_g + n_vis * 60
+    passes = 3                                                     # 10-bit digits over the ~26-bit depth span
+    by_sort = n_vis * 8 * 2 * passes + n_vis * 4 + n_keys * 12
+    by_out = E * W * H * ((3 if want_rgb else 0) + (4 if want_depth else 0))
+    t_alg = {
+        "project": (max(ops_proj / lane_ops, by_proj / hbm), "fp32" if ops_proj / lane_ops > by_proj / hbm else "hbm"),
+        "sort_bin": (by_sort / hbm, "hbm"),
+        "raster": max((flops / (alu_peak * 1e12), "fp32"), (n_contrib / ex2_rate, "mufu"), (by_out / hbm, "hbm")),
+    }
+    stages = {}
+    for n_, v in zip(names, stage_ms):
+        ta, bnd = t_alg[n_]
+        stages[n_] = {"bound": bnd, "alg_ms": ta * 1e3, "measured_ms": float(v), "frac": ta * 1e3 / max(float(v), 1e-9)}
+    t_roof = sum(v["alg_ms"] for v in stages.values())
+    roof_path = {"stages": stages, "t_roof_ms": t_roof, "measured_ms": float(stage_ms.sum()),
+                 "frac": t_roof / max(float(stage_ms.sum()), 1e-9),
+                 "basis": ("SURVEY §8(d).2: project = max(25 ops per (env, Gaussian) candidate + 150 (+130 SH) per "
+                           "visible record on FP32 lanes, scene + 60 B/record on HBM); sort = 16 B x passes + 4 B per "
+                           "record + 12 B per key on HBM; raster = max(definition flops on FP32, one ex2 per blended "
+                           "pair on MUFU, frame bytes on HBM); counts from the GG_COUNTERS pass")}
+
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cams0 = gi.Cameras(vm[0], np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1)), W, H)
         envs = list(range(min(args.cpu_envs, E)))
         dt, cores = oracle_sample(scene, cams0, envs, -1)
-        cpu = {"value": len(envs) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+        cpu = {"value": len(envs) / dt, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"{len(envs)} envs of pose set 0 (full {W}x{H} frames, {scene.n:,} Gaussians "
                          f"SH{scene.sh_degree}), incl. O1 preprocessing"}
 
@@ -369,14 +409,16 @@ def main():
         rec = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": tmax_ms / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-               "config": {"workload": name + ("" if want_rgb else " [depth-only outputs]"), "envs_per_gpu": E, "total_envs": E * world, "n_gauss": scene.n,
+               "config": {"workload": name + ("" if want_rgb and want_depth == c["depth"] else
+                                              " [depth-only outputs]" if not want_rgb else " [RGB-only outputs]"),
+                          "envs_per_gpu": E, "total_envs": E * world, "n_gauss": scene.n,
                           "sh_degree": scene.sh_degree, "width": W, "height": H, "depth": want_depth, "rgb": want_rgb,
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
                           "chunk_envs": args.chunk or 1024, "render_mode": "async (GG_ASYNC)" if use_async else "sync",
                           "tile_rects": "opacity-aware (GG_TIGHT_TILES, reading R35)" if args.tiles == "tight"
                           else "paper 3-sigma circle"},
-               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+               "roofline": roof, "roofline_path": roof_path, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clocks,
                "counters": {"n_eval": n_eval, "n_contrib": n_contrib, "visible": n_vis, "keys": n_keys,
                             "per_env": {"visible": n_vis / E, "keys": n_keys / E,
