@@ -40,19 +40,21 @@ constexpr int DS_IPT = SORT_BLK / DS_THREADS;
 constexpr int DS_BITS = 10;                     // digit width of the depth passes
 constexpr int DS_RADIX = 1 << DS_BITS;
 
-// blocks of the chunk: env of block b is the e with blk_base[e] <= b < blk_base[e+1]
+// blocks of the chunk: env of block b is the e with blk_base[e] <= b < blk_base[e+1],
+// tabulated once per chunk (blk_env_kernel) so a block finds it with one load
 struct BlockTable {
   const uint32_t* blk_base;   // [ec + 1]
+  const uint32_t* blk_env;    // [blk_base[ec]]
   int ec;
 };
 
-__device__ __forceinline__ int block_env(const BlockTable& bt, uint32_t b) {
-  int lo = 0, hi = bt.ec;   // last e with blk_base[e] <= b
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (bt.blk_base[mid] <= b) lo = mid; else hi = mid;
-  }
-  return lo;
+__device__ __forceinline__ int block_env(const BlockTable& bt, uint32_t b) { return (int)bt.blk_env[b]; }
+
+__global__ void blk_env_kernel(const uint32_t* __restrict__ blk_base, int ec, uint32_t* __restrict__ blk_env) {
+  const int e = blockIdx.x;
+  const uint32_t end = blk_base[ec];
+  const uint32_t b0 = blk_base[e], b1 = min(blk_base[e + 1], end);
+  for (uint32_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) blk_env[b] = (uint32_t)e;
 }
 
 __device__ __forceinline__ uint32_t peers_of(uint32_t v, int bits, uint32_t active) {
@@ -251,6 +253,8 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
   for (int i = tid; i < DS_WARPS * DS_RADIX / 2; i += DS_THREADS) (&sm.u.r.wcnt[0][0])[i] = 0u;
   for (int i = tid; i < DS_WARPS * 32; i += DS_THREADS) (&sm.u.r.pm[0][0])[i] = 0u;
   uint32_t k[DS_IPT], v[DS_IPT], d[DS_IPT], lp[DS_IPT];
+  // this block's output offset of its digits 2 tid, 2 tid + 1 (loaded early)
+  const uint2 off = reinterpret_cast<const uint2*>(ghist + (size_t)b * DS_RADIX)[tid];
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t i = warp * 32 * DS_IPT + j * 32 + lane;
@@ -261,19 +265,23 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
   }
   __syncthreads();
   block_rank(d, n, lp, sm);
+  // fold: dstart[d] <- (global offset of digit d) - (its start in the block),
+  // so staged element q of digit d goes to rb + dstart[d] + q
+  sm.dstart[2 * tid] = off.x - sm.dstart[2 * tid];
+  sm.dstart[2 * tid + 1] = off.y - sm.dstart[2 * tid + 1];
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t i = warp * 32 * DS_IPT + j * 32 + lane;
     if (i < n) { sm.u.o.sk[lp[j]] = k[j]; sm.u.o.sv[lp[j]] = v[j]; }
   }
   __syncthreads();
-  const uint32_t* off = ghist + (size_t)b * DS_RADIX;
+  uint32_t* kout = io.kout ? io.kout + rb : nullptr;
+  uint32_t* vout = io.vout + rb;
   for (uint32_t q = tid; q < n; q += DS_THREADS) {
     const uint32_t kk = sm.u.o.sk[q];
-    const uint32_t dd = depth_digit(kk, zmin, shift);
-    const uint64_t pos = rb + off[dd] + (q - sm.dstart[dd]);
-    if (io.kout) io.kout[pos] = kk;
-    io.vout[pos] = sm.u.o.sv[q];
+    const uint32_t pos = sm.dstart[depth_digit(kk, zmin, shift)] + q;
+    if (kout) kout[pos] = kk;
+    vout[pos] = sm.u.o.sv[q];
   }
 }
 
@@ -605,15 +613,17 @@ static int launch_sort_bin_t(int ec, uint32_t nb, const BlockTable& bt, int pass
 // Enqueue K3-K5 for a chunk.  blk_base: device [ec+1] block prefix; nb total
 // blocks (a capacity if nb_is_capacity); ghist >= nb*DS_RADIX u32; thist >=
 // nb*ntiles u32.  Returns the number of launches.
-int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, int passes, const RenderParams& rp,
-                    const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s, bool nb_is_capacity) {
+int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, uint32_t* blk_env, int passes,
+                    const RenderParams& rp, const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s,
+                    bool nb_is_capacity) {
   if (nb == 0) {
     cudaMemsetAsync(ws.ranges, 0, (size_t)ec * rp.ntiles * sizeof(uint2), s);
     return 0;
   }
-  BlockTable bt{blk_base, ec};
-  return nb_is_capacity ? launch_sort_bin_t<true>(ec, nb, bt, passes, rp, ws, ghist, thist, s)
-                        : launch_sort_bin_t<false>(ec, nb, bt, passes, rp, ws, ghist, thist, s);
+  blk_env_kernel<<<ec, 128, 0, s>>>(blk_base, ec, blk_env);
+  BlockTable bt{blk_base, blk_env, ec};
+  return 1 + (nb_is_capacity ? launch_sort_bin_t<true>(ec, nb, bt, passes, rp, ws, ghist, thist, s)
+                            : launch_sort_bin_t<false>(ec, nb, bt, passes, rp, ws, ghist, thist, s));
 }
 
 }  // namespace gg
