@@ -154,18 +154,26 @@ __global__ void __launch_bounds__(DS_RADIX) depth_scan_kernel(BlockTable bt, uin
   const uint32_t b0 = bt.blk_base[e], b1 = bt.blk_base[e + 1];
   const int d = threadIdx.x;
   uint32_t* col = ghist + d;
+  // pass 1: the digit's total over the env's blocks (16 independent loads in flight)
   uint32_t run = 0;
-  for (uint32_t b = b0; b < b1; b += 8) {          // 8 independent loads in flight
-    uint32_t x[8];
+  for (uint32_t b = b0; b < b1; b += 16) {
+    uint32_t x[16];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = b + u < b1 ? col[(size_t)(b + u) * DS_RADIX] : 0u;
+    for (int u = 0; u < 16; ++u) x[u] = b + u < b1 ? col[(size_t)(b + u) * DS_RADIX] : 0u;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (b + u < b1) { col[(size_t)(b + u) * DS_RADIX] = run; run += x[u]; }
+    for (int u = 0; u < 16; ++u) run += x[u];
   }
   uint32_t total;
-  const uint32_t base = block_scan(run, wsum, &total);
-  for (uint32_t b = b0; b < b1; ++b) col[(size_t)b * DS_RADIX] += base;
+  uint32_t acc = block_scan(run, wsum, &total);   // digits below d, all blocks
+  // pass 2: exclusive prefix over blocks, offset by the lower digits
+  for (uint32_t b = b0; b < b1; b += 16) {
+    uint32_t x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = b + u < b1 ? col[(size_t)(b + u) * DS_RADIX] : 0u;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (b + u < b1) { col[(size_t)(b + u) * DS_RADIX] = acc; acc += x[u]; }
+  }
 }
 
 struct DownSmem {
@@ -351,22 +359,29 @@ __global__ void __launch_bounds__(SB_THREADS) place_scan_kernel(BlockTable bt, C
   for (int base = 0; base < ntiles; base += SB_THREADS) {
     const int t = base + threadIdx.x;
     uint32_t run = 0;
-    if (t < ntiles) {
-      uint32_t* col = thist + t;
-      for (uint32_t b = b0; b < b1; b += 8) {       // 8 independent loads in flight
-        uint32_t x[8];
+    uint32_t* col = thist + t;
+    if (t < ntiles) {                               // pass 1: the tile's total (16 loads in flight)
+      for (uint32_t b = b0; b < b1; b += 16) {
+        uint32_t x[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = b + u < b1 ? col[(size_t)(b + u) * ntiles] : 0u;
+        for (int u = 0; u < 16; ++u) x[u] = b + u < b1 ? col[(size_t)(b + u) * ntiles] : 0u;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (b + u < b1) { col[(size_t)(b + u) * ntiles] = run; run += x[u]; }
+        for (int u = 0; u < 16; ++u) run += x[u];
       }
     }
     uint32_t total;
     const uint32_t ex = carry + block_scan(t < ntiles ? run : 0u, wsum, &total);
-    if (t < ntiles) {
+    if (t < ntiles) {                               // pass 2: exclusive prefix over blocks
       ws.ranges[(size_t)e * ntiles + t] = make_uint2(ex, ex + run);
-      for (uint32_t b = b0; b < b1; ++b) thist[(size_t)b * ntiles + t] += ex;
+      uint32_t acc = ex;
+      for (uint32_t b = b0; b < b1; b += 16) {
+        uint32_t x[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) x[u] = b + u < b1 ? col[(size_t)(b + u) * ntiles] : 0u;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (b + u < b1) { col[(size_t)(b + u) * ntiles] = acc; acc += x[u]; }
+      }
     }
     carry += total;
   }
