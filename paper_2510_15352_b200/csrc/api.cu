@@ -35,7 +35,8 @@ size_t sort_ghist_words();
 int depth_passes(uint32_t span);
 int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, uint32_t* blk_env, int passes,
                     const RenderParams& rp,
-                    const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s, bool nb_is_capacity);
+                    const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s, bool nb_is_capacity,
+                    uint32_t* qctr);
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s);
@@ -92,7 +93,7 @@ struct gg_context {
   // workspace
   DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase, zmm;
   DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1;
-  DevBuf sorted, ranges, counters, valid_out, perm, groups, blkbase, blkenv, ghist, thist;
+  DevBuf sorted, ranges, counters, valid_out, perm, groups, blkbase, blkenv, ghist, thist, qctr;
   DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval, dconic;
   DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
   DevBuf blur_vm, blur_ids, blur_intr, blur_rgb, blur_depth, blur_alpha;   // gg_render_blur
@@ -299,7 +300,7 @@ gg_status gg_destroy(gg_context* ctx) {
   DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->zmm, &ctx->okflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
                    &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect,
                    &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->perm, &ctx->groups,
-                   &ctx->blkbase, &ctx->blkenv, &ctx->ghist, &ctx->thist,
+                   &ctx->blkbase, &ctx->blkenv, &ctx->ghist, &ctx->thist, &ctx->qctr,
                    &ctx->sorted, &ctx->ranges, &ctx->counters, &ctx->valid_out,
                    &ctx->dbg_tc, &ctx->dbg_proj, &ctx->dbg_stile, &ctx->dbg_sz, &ctx->dbg_sgid,
                    &ctx->dbg_neval, &ctx->dconic, &ctx->h_in, &ctx->blur_vm, &ctx->blur_ids,
@@ -655,7 +656,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ctx->launches += launch_copy_words(ctx->blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, s);
     ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->blkbase), P<uint32_t>(ctx->blkenv), passes, rp, ws,
                                      P<uint32_t>(ctx->ghist),
-                                     P<uint32_t>(ctx->thist), s, false);
+                                     P<uint32_t>(ctx->thist), s, false, nullptr);
     CK(cudaGetLastError());
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], s));
     // K6
@@ -843,7 +844,8 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 1], s));
     ctx->launches += launch_sort_bin(ec, (uint32_t)ctx->a_nbcap, P<uint32_t>(ctx->blkbase), P<uint32_t>(ctx->blkenv),
                                      passes, rp, ws,
-                                     P<uint32_t>(ctx->ghist), P<uint32_t>(ctx->thist), s, true);
+                                     P<uint32_t>(ctx->ghist), P<uint32_t>(ctx->thist), s, true,
+                                     P<uint32_t>(ctx->qctr));
     if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 2], s));
     launch_raster(e0, ec, P<EnvConst>(ctx->envc), rp, ws, rgb, depth, alpha, counters,
                   counters ? P<unsigned long long>(ctx->counters) : nullptr, nullptr, -1, s);
@@ -887,7 +889,7 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
              ensure(ctx, ctx->dk0, vcap * 4, s) && ensure(ctx, ctx->dv0, vcap * 4, s) &&
              ensure(ctx, ctx->dk1, vcap * 4, s) && ensure(ctx, ctx->dv1, vcap * 4, s) &&
              ensure(ctx, ctx->sorted, kcap * 4, s) && ensure(ctx, ctx->blkbase, (size_t)(ch + 1) * 4, s) &&
-             ensure(ctx, ctx->blkenv, nbcap * 4 + 4, s) &&
+             ensure(ctx, ctx->blkenv, nbcap * 4 + 4, s) && ensure(ctx, ctx->qctr, 64 * 4, s) &&
              ensure(ctx, ctx->ghist, nbcap * sort_ghist_words() * 4, s) &&
              ensure(ctx, ctx->thist, nbcap * ntiles * 4, s);
   CK(cudaStreamSynchronize(s));

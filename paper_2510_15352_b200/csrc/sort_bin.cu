@@ -39,6 +39,7 @@ constexpr int DS_WARPS = DS_THREADS / 32;
 constexpr int DS_IPT = SORT_BLK / DS_THREADS;
 constexpr int DS_BITS = 10;                     // digit width of the depth passes
 constexpr int DS_RADIX = 1 << DS_BITS;
+constexpr int SORT_QCTR = 16;                   // async-mode work counters per chunk (2 per pass + 2)
 
 // blocks of the chunk: env of block b is the e with blk_base[e] <= b < blk_base[e+1],
 // tabulated once per chunk (blk_env_kernel) so a block finds it with one load
@@ -46,7 +47,18 @@ struct BlockTable {
   const uint32_t* blk_base;   // [ec + 1]
   const uint32_t* blk_env;    // [blk_base[ec]]
   int ec;
+  uint32_t* q;                // async mode: this launch's work counter (zeroed before the launch)
 };
+
+// async mode: CTAs take blocks from a shared counter (dynamic balance, like
+// the hardware's CTA scheduling in sync mode, within a bounded grid)
+__device__ __forceinline__ uint32_t next_block(uint32_t* q) {
+  __shared__ uint32_t b_s;
+  __syncthreads();             // every thread has read the previous value
+  if (threadIdx.x == 0) b_s = atomicAdd(q, 1u);
+  __syncthreads();
+  return b_s;
+}
 
 __device__ __forceinline__ int block_env(const BlockTable& bt, uint32_t b) { return (int)bt.blk_env[b]; }
 
@@ -139,9 +151,10 @@ depth_upsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, uint32_t*
     if (blockIdx.x < nb) depth_upsweep_block(blockIdx.x, bt, ws, io, shift, ghist, h);
     return;
   }
-  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {   // async mode: bounded grid strides over blocks
+  for (;;) {   // async mode: bounded grid, blocks taken dynamically
+    const uint32_t b = next_block(bt.q);
+    if (b >= nb) break;
     depth_upsweep_block(b, bt, ws, io, shift, ghist, h);
-    __syncthreads();
   }
 }
 
@@ -304,9 +317,10 @@ depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const u
     if (blockIdx.x < nb) depth_downsweep_block(blockIdx.x, bt, ws, io, shift, ghist, sm);
     return;
   }
-  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {   // async mode: bounded grid strides over blocks
+  for (;;) {   // async mode: bounded grid, blocks taken dynamically
+    const uint32_t b = next_block(bt.q);
+    if (b >= nb) break;
     depth_downsweep_block(b, bt, ws, io, shift, ghist, sm);
-    __syncthreads();
   }
 }
 
@@ -341,9 +355,10 @@ place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntile
     if (blockIdx.x < nb) place_upsweep_block(blockIdx.x, bt, ws, order, ntiles, TX, thist, h);
     return;
   }
-  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {   // async mode: bounded grid strides over blocks
+  for (;;) {   // async mode: bounded grid, blocks taken dynamically
+    const uint32_t b = next_block(bt.q);
+    if (b >= nb) break;
     place_upsweep_block(b, bt, ws, order, ntiles, TX, thist, h);
-    __syncthreads();
   }
 }
 
@@ -531,9 +546,10 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
     if (blockIdx.x < nb) place_downsweep_block<TB>(blockIdx.x, bt, ws, order, rp, thist, S, smem_raw);
     return;
   }
-  for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {   // async mode: bounded grid strides over blocks
+  for (;;) {   // async mode: bounded grid, blocks taken dynamically
+    const uint32_t b = next_block(bt.q);
+    if (b >= nb) break;
     place_downsweep_block<TB>(b, bt, ws, order, rp, thist, S, smem_raw);
-    __syncthreads();
   }
 }
 
@@ -593,27 +609,34 @@ int depth_passes(uint32_t span) {
 // Enqueue K3-K5 for a chunk.  blk_base: device [ec+1] block prefix; nb total
 // blocks; ghist >= nb*DS_RADIX u32; thist >= nb*ntiles u32.  Returns launches.
 template <bool LOOP>
-static int launch_sort_bin_t(int ec, uint32_t nb, const BlockTable& bt, int passes, const RenderParams& rp,
-                             const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s) {
+static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, const RenderParams& rp,
+                             const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s, uint32_t* qctr) {
   // sync mode (LOOP = false): one CTA per block; async mode: nb is only a
-  // capacity, so a bounded grid strides over the blocks that exist
-  const uint32_t g1 = LOOP ? std::min<uint32_t>(nb, 148u * 64u) : nb;
-  const uint32_t g2 = LOOP ? std::min<uint32_t>(nb, 148u * 32u) : nb;
+  // capacity, so a bounded grid (a few waves of resident CTAs) takes the
+  // blocks that exist from per-launch work counters
+  const uint32_t g1 = LOOP ? std::min<uint32_t>(nb, 148u * 8u) : nb;
+  const uint32_t g2 = LOOP ? std::min<uint32_t>(nb, 148u * 6u) : nb;
   int launches = 0;
+  int qi = 0;
+  if (LOOP) cudaMemsetAsync(qctr, 0, SORT_QCTR * sizeof(uint32_t), s);
   for (int p = 0; p < passes; ++p) {
     DepthIO io;
     io.kin = p == 0 ? ws.zkey : ((p & 1) ? ws.dk0 : ws.dk1);
     io.vin = p == 0 ? nullptr : ((p & 1) ? ws.dv0 : ws.dv1);
     io.kout = p == passes - 1 ? nullptr : ((p & 1) ? ws.dk1 : ws.dk0);
     io.vout = (p & 1) ? ws.dv1 : ws.dv0;
+    if (LOOP) bt.q = qctr + qi++;
     depth_upsweep_kernel<LOOP><<<g1, DS_THREADS, 0, s>>>(bt, ws, io, DS_BITS * p, ghist);
     depth_scan_kernel<<<ec, DS_RADIX, 0, s>>>(bt, ghist, ws.ok);
+    if (LOOP) bt.q = qctr + qi++;
     depth_downsweep_kernel<LOOP><<<g1, DS_THREADS, depth_down_smem(), s>>>(bt, ws, io, DS_BITS * p, ghist);
     launches += 3;
   }
   const uint32_t* order = ((passes - 1) & 1) ? ws.dv1 : ws.dv0;   // values of the last depth pass
+  if (LOOP) bt.q = qctr + qi++;
   place_upsweep_kernel<LOOP><<<g2, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
   place_scan_kernel<<<ec, SB_THREADS, 0, s>>>(bt, ws, thist, rp.ntiles);
+  if (LOOP) bt.q = qctr + qi++;
   const size_t psm = place_down_smem(rp.ntiles);
   const int S = place_segments(rp.ntiles);
   if (rp.ntiles <= 256)
@@ -630,15 +653,15 @@ static int launch_sort_bin_t(int ec, uint32_t nb, const BlockTable& bt, int pass
 // nb*ntiles u32.  Returns the number of launches.
 int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, uint32_t* blk_env, int passes,
                     const RenderParams& rp, const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s,
-                    bool nb_is_capacity) {
+                    bool nb_is_capacity, uint32_t* qctr) {
   if (nb == 0) {
     cudaMemsetAsync(ws.ranges, 0, (size_t)ec * rp.ntiles * sizeof(uint2), s);
     return 0;
   }
   blk_env_kernel<<<ec, 128, 0, s>>>(blk_base, ec, blk_env);
-  BlockTable bt{blk_base, blk_env, ec};
-  return 1 + (nb_is_capacity ? launch_sort_bin_t<true>(ec, nb, bt, passes, rp, ws, ghist, thist, s)
-                            : launch_sort_bin_t<false>(ec, nb, bt, passes, rp, ws, ghist, thist, s));
+  BlockTable bt{blk_base, blk_env, ec, nullptr};
+  return 1 + (nb_is_capacity ? launch_sort_bin_t<true>(ec, nb, bt, passes, rp, ws, ghist, thist, s, qctr)
+                            : launch_sort_bin_t<false>(ec, nb, bt, passes, rp, ws, ghist, thist, s, nullptr));
 }
 
 }  // namespace gg
