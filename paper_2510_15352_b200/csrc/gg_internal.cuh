@@ -38,7 +38,9 @@ struct __align__(16) EnvConst {
   int32_t n;           // Gaussians in that scene (0 if invalid)
   int32_t degree;      // SH degree used at render
   int32_t out_index;   // caller's env index (outputs, counters); envs are processed scene-sorted
+  float rgram;         // bound on the Gram matrices of R's row pairs (0,2), (1,2); 1 if R is orthonormal
 };
+static_assert(sizeof(EnvConst) == 112, "EnvConst: 7 x 16 B (its shared-memory stride avoids bank conflicts)");
 
 // 128-bit loads of a camera from shared memory (7 x LDS.128 instead of 28 LDS)
 __device__ __forceinline__ EnvConst load_cam(const EnvConst* p) {

@@ -54,6 +54,15 @@ __global__ void setup_envs_kernel(int E, const int32_t* __restrict__ perm, const
 #pragma unroll
   for (int k = 0; k < 3; ++k)
     c.C[k] = -(c.R[0 * 3 + k] * c.t[0] + c.R[1 * 3 + k] * c.t[1] + c.R[2 * 3 + k] * c.t[2]);
+  {
+    // sum_j (a R0j + b R2j)^2 <= (a^2 + b^2) lambda_max(Gram(R0, R2)) <= (a^2 + b^2)(max(|R0|^2,|R2|^2) + |R0.R2|)
+    float a[3], cr[2];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) a[r] = c.R[r * 3] * c.R[r * 3] + c.R[r * 3 + 1] * c.R[r * 3 + 1] + c.R[r * 3 + 2] * c.R[r * 3 + 2];
+    cr[0] = c.R[0] * c.R[6] + c.R[1] * c.R[7] + c.R[2] * c.R[8];
+    cr[1] = c.R[3] * c.R[6] + c.R[4] * c.R[7] + c.R[5] * c.R[8];
+    c.rgram = fmaxf(fmaxf(a[0], a[2]) + fabsf(cr[0]), fmaxf(a[1], a[2]) + fabsf(cr[1])) * 1.0001f;
+  }
   const int sid = scene_ids[e];
   c.out_index = e;
   if (sid < 0 || sid >= nscenes || !scenes[sid].valid) {
@@ -89,23 +98,22 @@ __device__ __forceinline__ void load_group_cams(EnvConst* cams, const EnvConst* 
 // and a + c <= s_max^2 |T|_F^2 + 0.6; generous margins absorb f32 rounding.
 __device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float smax2, const RenderParams& rp,
                                               uint32_t& zbits) {
-  const float3 p = to_cam(c, g);
-  zbits = __float_as_uint(p.z);
-  if (!(p.z > rp.near_p && p.z <= rp.far_p)) return false;   // exact (canonical p_z)
-  const float rz = __fdividef(1.f, p.z);      // approximate: the test has margins
-  const float u = c.fx * p.x * rz + c.cx;
-  const float v = c.fy * p.y * rz + c.cy;
-  const float txz = fminf(c.lim_xp, fmaxf(-c.lim_xn, p.x * rz));
-  const float tyz = fminf(c.lim_yp, fmaxf(-c.lim_yn, p.y * rz));
+  // p_z in the canonical order (it decides near/far exactly); p_x, p_y only
+  // feed the margin-protected footprint test
+  const float pz = fa(dot3(c.R[6], g.x, c.R[7], g.y, c.R[8], g.z), c.t[2]);
+  zbits = __float_as_uint(pz);
+  if (!(pz > rp.near_p && pz <= rp.far_p)) return false;
+  const float px = fmaf(c.R[2], g.z, fmaf(c.R[1], g.y, fmaf(c.R[0], g.x, c.t[0])));
+  const float py = fmaf(c.R[5], g.z, fmaf(c.R[4], g.y, fmaf(c.R[3], g.x, c.t[1])));
+  const float rz = __fdividef(1.f, pz);       // approximate: the test has margins
+  const float u = c.fx * px * rz + c.cx;
+  const float v = c.fy * py * rz + c.cy;
+  const float txz = fminf(c.lim_xp, fmaxf(-c.lim_xn, px * rz));
+  const float tyz = fminf(c.lim_yp, fmaxf(-c.lim_yn, py * rz));
   const float J00 = c.fx * rz, J11 = c.fy * rz;
   const float J02 = -c.fx * txz * rz, J12 = -c.fy * tyz * rz;
-  float nT = 0.f;
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const float t0 = J00 * c.R[j] + J02 * c.R[6 + j];
-    const float t1 = J11 * c.R[3 + j] + J12 * c.R[6 + j];
-    nT += t0 * t0 + t1 * t1;
-  }
+  // |T|_F^2 = |J00 R0 + J02 R2|^2 + |J11 R1 + J12 R2|^2 <= rgram (J00^2 + J02^2 + J11^2 + J12^2)
+  const float nT = c.rgram * fmaf(J00, J00, fmaf(J02, J02, fmaf(J11, J11, J12 * J12)));
   const float lam_b = (smax2 * nT + 0.9163f) * 1.001f + 0.01f;
   const float rb = 3.f * (lam_b * rsqrtf(lam_b)) * 1.002f + 2.f;
   return (u + rb > 0.f) && (u - rb < (float)(rp.TX * TILE)) && (v + rb > 0.f) && (v - rb < (float)(rp.TY * TILE));
@@ -116,9 +124,11 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
                   const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
   __shared__ EnvConst cams[ENV_GROUP];
   __shared__ uint32_t wc[ENV_GROUP][PROJ_BLOCK / 32];
+  __shared__ uint32_t szmn[ENV_GROUP], szmx[ENV_GROUP];   // the CTA's depth-key range per env
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0) return;
   load_group_cams(cams, envs, e0, grp);
+  if (threadIdx.x < ENV_GROUP) { szmn[threadIdx.x] = 0xffffffffu; szmx[threadIdx.x] = 0u; }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.y * PROJ_BLOCK + threadIdx.x;
@@ -146,8 +156,8 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
       ws.flags[(size_t)(grp.elo + k) * ws.nwords + wi] = word;
       wc[k][warp] = __popc(word);
       if (word) {
-        atomicMin(&ws.zmin[grp.elo + k], zmn);
-        atomicMax(&ws.zmax[grp.elo + k], zmx);
+        atomicMin(&szmn[k], zmn);
+        atomicMax(&szmx[k], zmx);
       }
     }
   }
@@ -157,6 +167,10 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
 #pragma unroll
     for (int w = 0; w < PROJ_BLOCK / 32; ++w) s += wc[threadIdx.x][w];
     ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blockIdx.y] = s;
+    if (s) {
+      atomicMin(&ws.zmin[grp.elo + threadIdx.x], szmn[threadIdx.x]);
+      atomicMax(&ws.zmax[grp.elo + threadIdx.x], szmx[threadIdx.x]);
+    }
   }
 }
 
