@@ -236,6 +236,33 @@ __device__ __forceinline__ void sh_eval(int deg, float x, float y, float z, floa
   Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
 }
 
+// O2.8 colour at a compile-time SH degree D >= 1: 128-bit loads of the
+// coefficient row (coefficient-major (q, ch), zero-padded to a multiple of 4);
+// each channel accumulates q = 0, 1, ... in order.
+template <int D>
+__device__ __forceinline__ void sh_colour(const float* __restrict__ row, float x, float y, float z, float col[3]) {
+  constexpr int KC = (D + 1) * (D + 1);
+  constexpr int NF4 = (KC * 3 + 3) / 4;
+  float Y[16];
+  sh_eval(D, x, y, z, Y);
+  const float4* f4 = reinterpret_cast<const float4*>(row);
+  float4 sh[NF4];
+#pragma unroll
+  for (int q4 = 0; q4 < NF4; ++q4) sh[q4] = __ldg(&f4[q4]);
+  float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int q4 = 0; q4 < NF4; ++q4) {
+    const float xs[4] = {sh[q4].x, sh[q4].y, sh[q4].z, sh[q4].w};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int idx = 4 * q4 + m;
+      if (idx < KC * 3) acc[idx % 3] += Y[idx / 3] * xs[m];
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) col[ch] = fminf(1.f, fmaxf(0.f, acc[ch] + 0.5f));
+}
+
 // Opacity-aware tile rect (GG_TIGHT_TILES, reading R35): the
 // paper rect cut to the tiles whose pixel centres can reach the box of the
 // alpha >= 1/255 ellipse {q <= qm} of the f32 conic.  Canonical f32 order
@@ -424,31 +451,10 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
       float dx = g.x - c.C[0], dy = g.y - c.C[1], dz = g.z - c.C[2];
       const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
       dx *= inv; dy *= inv; dz *= inv;
-      float Y[16];
-      sh_eval(cdeg, dx, dy, dz, Y);
-      const int Kc = (cdeg + 1) * (cdeg + 1);
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-      // 128-bit loads of the coefficient row (coefficient-major (q, ch));
-      // each channel still accumulates q = 0, 1, ... in order
-      const float4* f4 = reinterpret_cast<const float4*>(scn.sh + (size_t)gi * scn.sh_stride);
-      float acc[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-      for (int q4 = 0; q4 < SH_MAX / 4; ++q4) {
-        if (4 * q4 < Kc * 3) {
-          const float4 x = __ldg(&f4[q4]);
-          const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            const int idx = 4 * q4 + m;
-            if (idx < Kc * 3) acc[idx % 3] += Y[idx / 3] * xs[m];
-          }
-        }
-      }
-      s0 = acc[0]; s1 = acc[1]; s2 = acc[2];
-
-      col[0] = fminf(1.f, fmaxf(0.f, s0 + 0.5f));
-      col[1] = fminf(1.f, fmaxf(0.f, s1 + 0.5f));
-      col[2] = fminf(1.f, fmaxf(0.f, s2 + 0.5f));
+      const float* row = scn.sh + (size_t)gi * scn.sh_stride;
+      if (cdeg == 3) sh_colour<3>(row, dx, dy, dz, col);
+      else if (cdeg == 2) sh_colour<2>(row, dx, dy, dz, col);
+      else sh_colour<1>(row, dx, dy, dz, col);
     }
     // blend-side culling extents: alpha >= 1/255 needs q <= 2 ln(255 o); the
     // ellipse's half extents are sqrt(qmax Sigma2_xx), sqrt(qmax Sigma2_yy)
