@@ -32,6 +32,7 @@ F_NO_EARLY_OUT = 1
 F_UNTRUNCATED = 2
 F_PLAIN = 4
 F_TIGHT = 8         # work-reduction variant: opacity-aware tile rects (R35)
+F_ELLIPSE = 16      # work-reduction variant: ellipse ∩ tile masks on tight rects (R37)
 
 K_RGB, K_DEPTH, K_ALPHA, K_NEVAL, K_NCONTRIB, K_EXEMPT = 0, 1, 2, 3, 4, 5
 K_TILE_COUNTS, K_SORTED_TILE, K_SORTED_ZBITS, K_SORTED_GID, K_RANGES = 6, 7, 8, 9, 10

@@ -127,6 +127,8 @@ struct Proj {
   float u32 = 0, v32 = 0, A32 = 0, B32 = 0, C32 = 0, z32 = 0;   // f32 values (mode A dump)
   int r = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
   uint32_t zbits = 0;
+  float qm = 0.f;                // R35 cutoff with margin (set by tight_rect)
+  uint32_t mask = 0xffffffffu;   // R37: kept tiles of a <= 32-tile rect, row-major bits
 };
 
 struct Cam {
@@ -226,6 +228,7 @@ bool project_geom(const float* mu, const T cov[6], const Cam& cam, T near_p, T f
 // blends the Gaussian: images are unchanged, only the lists get shorter.
 // qmax = f32(2 ln(255 o)) once per Gaussian (f64 log).
 void tight_rect(Proj& P, float o) {
+  P.qm = INFINITY;                                   // no pruning unless the tight rect is computed
   const float qmax = (float)(2.0 * std::log(255.0 * (double)o));
   if (!(qmax >= 0.0f)) { P.x0 = P.x1 = P.y0 = P.y1 = 0; return; }   // o < 1/255: no pixel blends
   const float A = P.A32, B = P.B32, C = P.C32;
@@ -236,6 +239,7 @@ void tight_rect(Proj& P, float o) {
   // |A| ex0^2 + 2|B| ex0 ey0 + |C| ey0^2 at q = qmax, ex0^2 = qmax C / D, ey0^2 = qmax A / D
   const float mag = ((qmax * rD) * ((2.0f * AC) + (2.0f * std::fabs(B)) * std::sqrt(AC)));
   const float qm = (qmax + 1e-3f) + 1e-5f * mag;
+  P.qm = qm;
   const float grow = 1.0000038146972656f;                              // 1 + 2^-18
   const float ex = std::sqrt((qm * C) * rD) * grow, ey = std::sqrt((qm * A) * rD) * grow;
   const float u = P.u32, v = P.v32;
@@ -249,6 +253,50 @@ void tight_rect(Proj& P, float o) {
   const int y1 = (int)std::max((float)P.y0, std::min((float)P.y1, hy));
   if (x0 >= x1 || y0 >= y1) { P.x0 = P.x1 = P.y0 = P.y1 = 0; return; }
   P.x0 = x0; P.x1 = x1; P.y0 = y0; P.y1 = y1;
+}
+
+// Work-reduction variant "ellipse ∩ tile" (DESIGN.md
+// reading R37; needs F_TIGHT): a tile of a tight rect of at most 32 tiles is
+// kept only if the f32 conic's quadratic q(d) = A dx^2 + 2B dx dy + C dy^2,
+// minimised over the tile's rectangle of pixel centres, reaches q_m (R35) plus
+// a rounding margin.  The minimum of a convex quadratic over a rectangle is 0
+// if the mean lies inside, else on an edge: on the edge dx = e it is at
+// dy = clamp(-B e / C) (and symmetrically).  Evaluated in f32 in this order.
+bool tile_keeps(const Proj& P, int tx, int ty) {
+  const float A = P.A32, B = P.B32, C = P.C32;
+  const float dxl = (16.0f * (float)tx + 0.5f) - P.u32, dxh = (16.0f * (float)tx + 15.5f) - P.u32;
+  const float dyl = (16.0f * (float)ty + 0.5f) - P.v32, dyh = (16.0f * (float)ty + 15.5f) - P.v32;
+  if (dxl <= 0.0f && dxh >= 0.0f && dyl <= 0.0f && dyh >= 0.0f) return true;
+  float best = INFINITY, mag = 0.0f;
+  auto consider = [&](float dx, float dy) {
+    const float q = ((A * dx) * dx + ((2.0f * B) * dx) * dy) + (C * dy) * dy;
+    if (q < best) {
+      best = q;
+      mag = ((std::fabs(A) * dx) * dx + ((2.0f * std::fabs(B)) * std::fabs(dx)) * std::fabs(dy)) + (std::fabs(C) * dy) * dy;
+    }
+  };
+  const float ex[2] = {dxl, dxh}, ey[2] = {dyl, dyh};
+  for (int k = 0; k < 2; ++k) {
+    consider(ex[k], std::min(std::max((-B * ex[k]) / C, dyl), dyh));
+    consider(std::min(std::max((-B * ey[k]) / A, dxl), dxh), ey[k]);
+  }
+  return best <= (P.qm + 1e-3f) + 1e-5f * mag;
+}
+
+void ellipse_mask(Proj& P) {
+  const int w = P.x1 - P.x0, h = P.y1 - P.y0;
+  if (w * h <= 0 || w * h > 32) return;                  // larger rects are not pruned (R37)
+  uint32_t m = 0;
+  for (int ty = P.y0; ty < P.y1; ++ty)
+    for (int tx = P.x0; tx < P.x1; ++tx)
+      if (tile_keeps(P, tx, ty)) m |= 1u << ((ty - P.y0) * w + (tx - P.x0));
+  P.mask = m;
+}
+
+bool in_list(const Proj& P, int tx, int ty) {
+  if (tx < P.x0 || tx >= P.x1 || ty < P.y0 || ty >= P.y1) return false;
+  const int w = P.x1 - P.x0, h = P.y1 - P.y0;
+  return w * h > 32 || ((P.mask >> ((ty - P.y0) * w + (tx - P.x0))) & 1u);
 }
 
 // O2.8 colour (f64): degree 0 from O1, else SH at dir = (mu - C)/|mu - C|.
@@ -295,7 +343,7 @@ struct Result {
   std::vector<float> proj;     // [n*16]
 };
 
-enum { F_NO_EARLY_OUT = 1, F_UNTRUNCATED = 2, F_PLAIN = 4, F_TIGHT = 8 };
+enum { F_NO_EARLY_OUT = 1, F_UNTRUNCATED = 2, F_PLAIN = 4, F_TIGHT = 8, F_ELLIPSE = 16 };
 
 // O4 + O5 for one pixel over an ordered sequence of records.
 struct PixelOut {
@@ -352,7 +400,7 @@ struct OrOpts {
   double background[3];
   int32_t sh_degree;   // -1: scene degree
   int32_t mode;        // 0 = A (f32 canonical projection), 1 = B (f64 projection)
-  int32_t flags;       // F_NO_EARLY_OUT | F_UNTRUNCATED | F_PLAIN | F_TIGHT
+  int32_t flags;       // F_NO_EARLY_OUT | F_UNTRUNCATED | F_PLAIN | F_TIGHT | F_ELLIPSE
 };
 
 void* or_scene_create(int64_t n, int32_t d, const float* means, const float* scales,
@@ -438,8 +486,13 @@ void* or_render_env(const void* scene, const float* view, const float* intr, int
     if (!vis) continue;
     g.o = (double)S.opac[i];
     colour_of(S, i, dr, cam, g.col);
-    if (opt->flags & F_TIGHT) tight_rect(g, S.opac[i]);
-    R->tile_counts[i] = (g.x1 - g.x0) * (g.y1 - g.y0);
+    if (opt->flags & (F_TIGHT | F_ELLIPSE)) tight_rect(g, S.opac[i]);
+    if (opt->flags & F_ELLIPSE) ellipse_mask(g);
+    {
+      const int area = (g.x1 - g.x0) * (g.y1 - g.y0);
+      R->tile_counts[i] = area <= 32 ? __builtin_popcount(g.mask & (area == 32 ? 0xffffffffu : ((1u << area) - 1u)))
+                                     : area;
+    }
     float* d = &R->proj[i * 16];
     // dump column 0: "has at least one tile"
     d[0] = R->tile_counts[i] > 0 ? 1.0f : 0.0f; d[1] = g.u32; d[2] = g.v32; d[3] = g.A32; d[4] = g.B32; d[5] = g.C32; d[6] = g.z32;
@@ -453,7 +506,8 @@ void* or_render_env(const void* scene, const float* view, const float* intr, int
     const Proj& g = P[i];
     if (!g.vis) continue;
     for (int ty = g.y0; ty < g.y1; ++ty)
-      for (int tx = g.x0; tx < g.x1; ++tx) items.push_back({ty * cam.TX + tx, g.zbits, (int)i});
+      for (int tx = g.x0; tx < g.x1; ++tx)
+        if (in_list(g, tx, ty)) items.push_back({ty * cam.TX + tx, g.zbits, (int)i});
   }
   std::stable_sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
     if (a.t != b.t) return a.t < b.t;
@@ -510,7 +564,7 @@ void* or_render_env(const void* scene, const float* view, const float* intr, int
     } else if (flags & F_PLAIN) {
       for (int gid : global) {
         const Proj& g = P[gid];
-        if (g.x0 <= tx && tx < g.x1 && g.y0 <= ty && ty < g.y1) seq.push_back(gid);
+        if (in_list(g, tx, ty)) seq.push_back(gid);
       }
     } else {
       for (int k = R->ranges[t * 2]; k < R->ranges[t * 2 + 1]; ++k) seq.push_back(items[k].gid);
