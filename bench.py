@@ -57,8 +57,9 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--mode", default="sync", choices=["async", "sync"],
                    help="async: sync-free GG_ASYNC render (default); sync: host-sized workspace per chunk")
-    p.add_argument("--tiles", default="tight", choices=["paper", "tight"],
-                   help="tile rects: the paper's 3-sigma circle, or opacity-aware (GG_TIGHT_TILES, identical images)")
+    p.add_argument("--tiles", default="tight", choices=["paper", "tight", "ellipse"],
+                   help="tile lists: the paper's 3-sigma circle rects, opacity-aware rects (GG_TIGHT_TILES), or those "
+                        "plus ellipse-intersects-tile masks (GG_ELLIPSE_TILES); images are identical")
     p.add_argument("--outputs", default="rgbd", choices=["rgbd", "rgb", "depth"],
                    help="rgbd (the headline), rgb only, or depth-only (rgb = NULL: no SH/colour work; the paper's "
                         "depth-only baseline)")
@@ -237,7 +238,8 @@ def main():
     use_async = args.mode == "async" and not args.blur
     if use_async:
         gg.gg_reserve_async(R.ctx, E, W, H, args.chunk, 0.7, 4.0)
-    mflag = (gg.GG_ASYNC if use_async else 0) | (gg.GG_TIGHT_TILES if args.tiles == "tight" else 0)
+    tiles_flag = {"paper": 0, "tight": gg.GG_TIGHT_TILES, "ellipse": gg.GG_ELLIPSE_TILES}[args.tiles]
+    mflag = (gg.GG_ASYNC if use_async else 0) | tiles_flag
     n_sets = args.warmup + args.steps
     # a fresh, seeded pose set for every step, all resident in HBM
     vm = np.stack([gi.cameras(10_000 * (rank + 1) + s, E, W, H, scene).viewmats for s in range(n_sets)])
@@ -255,7 +257,7 @@ def main():
 
     def step(s, **kw):
         if args.blur:
-            kw["flags"] = kw.get("flags", 0) | (mflag & gg.GG_TIGHT_TILES)
+            kw["flags"] = kw.get("flags", 0) | tiles_flag
             gg.gg_render_blur(R.ctx, E, ids, vm_d[s], intr, lin_d, ang_d, args.shutter, args.blur, W, H,
                               gg.default_opts(**kw), rgb, depth, None, stream)
         else:
@@ -267,7 +269,7 @@ def main():
     # SURVEY §8(d).2); the lists actually rendered (tight by default) are
     # counted as well and reported beside it.
     kb = max(1, args.blur)     # blur renders K sample frames per env (work scaled by K, static-pose counts)
-    paper_flags = gg.GG_COUNTERS | (mflag & ~gg.GG_TIGHT_TILES)
+    paper_flags = gg.GG_COUNTERS | (mflag & ~(gg.GG_TIGHT_TILES | gg.GG_ELLIPSE_TILES))
     gg.gg_render(R.ctx, E, ids, vm_d[0], intr, W, H, gg.default_opts(flags=paper_flags), rgb, depth, None, stream)
     n_eval, n_contrib, n_vis, n_keys = (int(x) * kb for x in gg.gg_get_counters(R.ctx, E).sum(axis=0))
     gg.gg_render(R.ctx, E, ids, vm_d[0], intr, W, H, gg.default_opts(flags=gg.GG_COUNTERS | mflag), rgb, depth,
@@ -320,7 +322,7 @@ def main():
         h_in = np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1))
         h_rgb = torch.empty((E, H, W, 3), dtype=torch.uint8).pin_memory() if want_rgb else None
         h_depth = torch.empty((E, H, W), dtype=torch.float32).pin_memory() if want_depth else None
-        hopts = gg.default_opts(flags=gg.GG_TIGHT_TILES if args.tiles == "tight" else 0)
+        hopts = gg.default_opts(flags=tiles_flag)
         gg.gg_render_host(R.ctx, E, h_ids, h_vm[0], h_in, W, H, hopts, h_rgb, h_depth, None, stream)
         ke = max(2, min(args.steps, 5))
         if world > 1:
@@ -422,8 +424,10 @@ def main():
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
                           "chunk_envs": args.chunk or 1024, "render_mode": "async (GG_ASYNC)" if use_async else "sync",
-                          "tile_rects": "opacity-aware (GG_TIGHT_TILES, reading R35)" if args.tiles == "tight"
-                          else "paper 3-sigma circle"},
+                          "tile_lists": {"paper": "paper 3-sigma circle rects",
+                                         "tight": "opacity-aware rects (GG_TIGHT_TILES, reading R35)",
+                                         "ellipse": "opacity-aware rects + ellipse-tile masks (GG_ELLIPSE_TILES, R35+R37)"
+                                         }[args.tiles]},
                "roofline": roof, "roofline_path": roof_path, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clocks,
                "counters": {"n_eval": n_eval, "n_contrib": n_contrib, "visible": n_vis, "keys": n_keys,

@@ -53,10 +53,13 @@ enum {
   GG_KEEP_INTERMEDIATES = 1u, /* keep opts.debug_env's integer artefacts for gg_debug_dump */
   GG_COUNTERS = 2u,           /* accumulate per-env n_eval / n_contrib totals */
   GG_ASYNC = 4u,              /* sync-free, CUDA-graph-capturable render (needs gg_reserve_async) */
-  GG_TIGHT_TILES = 8u         /* work-reduction variant (reading R35):
+  GG_TIGHT_TILES = 8u,        /* work-reduction variant (reading R35):
                                  each Gaussian's tile rect is cut to the tiles that can hold a pixel
                                  with alpha >= 1/255.  Images are bit-identical to the paper's 3-sigma
                                  rects; the tile lists (and gg_debug_dump's artefacts) are shorter. */
+  GG_ELLIPSE_TILES = 16u      /* work-reduction variant (reading R37),
+                                 implies GG_TIGHT_TILES: tiles of a <= 32-tile rect whose pixel centres
+                                 cannot reach the alpha >= 1/255 ellipse are dropped.  Images unchanged. */
 };
 
 typedef struct {
@@ -65,7 +68,7 @@ typedef struct {
   float background[3];   /* rgb in [0,1] blended as C + T*bg; default 0 */
   int32_t sh_degree;     /* SH degree used at render, -1 = each scene's own (reading R18) */
   int32_t rgb_format;    /* 0 = u8 [E,H,W,3] round-half-even; 1 = f32 [E,H,W,3] */
-  uint32_t flags;        /* GG_KEEP_INTERMEDIATES | GG_COUNTERS | GG_ASYNC | GG_TIGHT_TILES */
+  uint32_t flags;        /* GG_KEEP_INTERMEDIATES | GG_COUNTERS | GG_ASYNC | GG_TIGHT_TILES | GG_ELLIPSE_TILES */
   int32_t debug_env;     /* env index whose intermediates are kept (-1 = none) */
 } gg_render_opts;
 

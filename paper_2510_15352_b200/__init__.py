@@ -25,6 +25,7 @@ GG_KEEP_INTERMEDIATES = 1
 GG_COUNTERS = 2
 GG_ASYNC = 4
 GG_TIGHT_TILES = 8          # opacity-aware tile rects (reading R35)
+GG_ELLIPSE_TILES = 16       # + ellipse-intersects-tile masks (reading R37)
 (GG_DUMP_TILE_COUNTS, GG_DUMP_SORTED_TILE, GG_DUMP_SORTED_ZBITS, GG_DUMP_SORTED_GIDS, GG_DUMP_RANGES,
  GG_DUMP_COUNTERS, GG_DUMP_N_EVAL, GG_DUMP_PROJ) = range(8)
 

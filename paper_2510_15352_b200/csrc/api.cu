@@ -92,7 +92,7 @@ struct gg_context {
   int chunk = DEFAULT_CHUNK;
   // workspace
   DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase, zmm;
-  DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1;
+  DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1, rmask;
   DevBuf sorted, ranges, counters, valid_out, perm, groups, blkbase, blkenv, ghist, thist, qctr;
   DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval, dconic;
   DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
@@ -298,7 +298,7 @@ gg_status gg_destroy(gg_context* ctx) {
   }
   for (auto& e : ctx->a_ev) cudaEventDestroy(e);
   DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->zmm, &ctx->okflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
-                   &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect,
+                   &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect, &ctx->rmask,
                    &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->perm, &ctx->groups,
                    &ctx->blkbase, &ctx->blkenv, &ctx->ghist, &ctx->thist, &ctx->qctr,
                    &ctx->sorted, &ctx->ranges, &ctx->counters, &ctx->valid_out,
@@ -515,7 +515,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   rp.near_p = opts.near_plane; rp.far_p = opts.far_plane;
   rp.bg[0] = opts.background[0]; rp.bg[1] = opts.background[1]; rp.bg[2] = opts.background[2];
   rp.rgb_format = opts.rgb_format;
-  rp.tight = (opts.flags & GG_TIGHT_TILES) != 0;
+  rp.tight = (opts.flags & (GG_TIGHT_TILES | GG_ELLIPSE_TILES)) != 0;
+  rp.ellipse = (opts.flags & GG_ELLIPSE_TILES) != 0;
   rp.color = rgb != nullptr;
   const bool counters = (opts.flags & GG_COUNTERS) != 0;
   const bool keep = (opts.flags & GG_KEEP_INTERMEDIATES) != 0 && opts.debug_env >= 0 && opts.debug_env < E;
@@ -610,6 +611,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     if (!ensure(ctx, ctx->rec0, V * 16, s) || !ensure(ctx, ctx->rec1, V * 16, s) ||
         !ensure(ctx, ctx->rec2, V * 16, s) || !ensure(ctx, ctx->rect, V * 8, s) ||
         !ensure(ctx, ctx->zkey, V * 4, s) || (keep && !ensure(ctx, ctx->gid, V * 4, s)) ||
+        (rp.ellipse && !ensure(ctx, ctx->rmask, V * 4 + 4, s)) ||
         (keep && !ensure(ctx, ctx->dconic, V * 16, s)) ||
         !ensure(ctx, ctx->dk0, V * 4, s) || !ensure(ctx, ctx->dv0, V * 4, s) ||
         !ensure(ctx, ctx->dk1, V * 4, s) || !ensure(ctx, ctx->dv1, V * 4, s))
@@ -619,6 +621,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     CK(cudaMemsetAsync(ws.kcnt, 0, ec * 4, s));
     ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
     ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
+    ws.rmask = rp.ellipse ? P<uint32_t>(ctx->rmask) : nullptr;
     ws.gid = keep ? P<uint32_t>(ctx->gid) : nullptr;
     ws.dconic = keep ? P<float4>(ctx->dconic) : nullptr;
     ws.dk0 = P<uint32_t>(ctx->dk0); ws.dv0 = P<uint32_t>(ctx->dv0);
@@ -786,7 +789,8 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
   rp.near_p = opts.near_plane; rp.far_p = opts.far_plane;
   rp.bg[0] = opts.background[0]; rp.bg[1] = opts.background[1]; rp.bg[2] = opts.background[2];
   rp.rgb_format = opts.rgb_format;
-  rp.tight = (opts.flags & GG_TIGHT_TILES) != 0;
+  rp.tight = (opts.flags & (GG_TIGHT_TILES | GG_ELLIPSE_TILES)) != 0;
+  rp.ellipse = (opts.flags & GG_ELLIPSE_TILES) != 0;
   rp.color = rgb != nullptr;
   const bool counters = (opts.flags & GG_COUNTERS) != 0;
   const int chunk = ctx->a_chunk, nblk = ctx->a_nblk, nwords = nblk * (PROJ_BLOCK / 32);
@@ -819,6 +823,7 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     ws.k_base = P<uint64_t>(ctx->kbase);
     ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
     ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
+    ws.rmask = rp.ellipse ? P<uint32_t>(ctx->rmask) : nullptr;
     ws.zmin = P<uint32_t>(ctx->zmm); ws.zmax = P<uint32_t>(ctx->zmm) + chunk;
     ws.dk0 = P<uint32_t>(ctx->dk0); ws.dv0 = P<uint32_t>(ctx->dv0);
     ws.dk1 = P<uint32_t>(ctx->dk1); ws.dv1 = P<uint32_t>(ctx->dv1);
@@ -886,6 +891,7 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
              ensure(ctx, ctx->counters, (size_t)max_envs * 32, s) && ensure(ctx, ctx->rec0, vcap * 16, s) &&
              ensure(ctx, ctx->rec1, vcap * 16, s) && ensure(ctx, ctx->rec2, vcap * 16, s) &&
              ensure(ctx, ctx->rect, vcap * 8, s) && ensure(ctx, ctx->zkey, vcap * 4, s) &&
+             ensure(ctx, ctx->rmask, vcap * 4 + 4, s) &&
              ensure(ctx, ctx->dk0, vcap * 4, s) && ensure(ctx, ctx->dv0, vcap * 4, s) &&
              ensure(ctx, ctx->dk1, vcap * 4, s) && ensure(ctx, ctx->dv1, vcap * 4, s) &&
              ensure(ctx, ctx->sorted, kcap * 4, s) && ensure(ctx, ctx->blkbase, (size_t)(ch + 1) * 4, s) &&

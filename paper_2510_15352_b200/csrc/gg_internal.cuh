@@ -67,6 +67,7 @@ struct RenderParams {
   int rgb_format;
   int tight;             // GG_TIGHT_TILES: opacity-aware tile rects (reading R35)
   int color;             // 0 = depth-only render (rgb == null): no SH/colour work
+  int ellipse;           // GG_ELLIPSE_TILES: per-record tile masks (reading R37)
 };
 
 // Workspace pointers for one env chunk (indices are chunk-local envs).
@@ -84,6 +85,7 @@ struct ChunkWS {
   float4* rec2;         // (r, g, b, ext_y)
   float4* dconic;       // debug only (null unless intermediates are kept): raw conic A, B, C, opacity
   uint2* rect;          // (x0 | x1<<16, y0 | y1<<16)
+  uint32_t* rmask;      // [V] R37 kept-tile masks of <= 32-tile rects (null: variant off)
   uint32_t* zkey;       // f32 bits of z
   uint32_t* zmin;       // [Ec] min / max depth bits per env (depth-sort key offset)
   uint32_t* zmax;
@@ -118,6 +120,15 @@ struct ValidateOut {
 
 // sticky error bits
 enum { ERR_BAD_SCENE = 1, ERR_CAPACITY = 2 };
+
+// Tiles of a record (R37): rects of <= 32 tiles may carry a row-major mask of
+// kept tiles; ~0u = every tile of the rect.
+__device__ __forceinline__ uint32_t rec_mask(const uint32_t* rmask, uint64_t r, uint32_t area) {
+  return (rmask && area <= 32u) ? rmask[r] : 0xffffffffu;
+}
+__device__ __forceinline__ uint32_t rec_tiles(uint32_t mask, uint32_t area) {
+  return area <= 32u ? (uint32_t)__popc(mask & (area == 32u ? 0xffffffffu : ((1u << area) - 1u))) : area;
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;

@@ -46,7 +46,8 @@ __global__ void debug_records_kernel(uint32_t V, uint64_t rb, const ChunkWS ws, 
     const uint64_t r = rb + j;
     const uint2 rc = ws.rect[r];
     const uint32_t x0 = rc.x & 0xffffu, x1 = rc.x >> 16, y0 = rc.y & 0xffffu, y1 = rc.y >> 16;
-    const uint32_t nt = (x1 - x0) * (y1 - y0);
+    const uint32_t area = (x1 - x0) * (y1 - y0);
+    const uint32_t nt = rec_tiles(rec_mask(ws.rmask, r, area), area);
     const uint32_t g = ws.gid[r];
     tile_counts[g] = (int32_t)nt;
     if (nt) {

@@ -267,12 +267,14 @@ __device__ __forceinline__ void sh_colour(const float* __restrict__ row, float x
 // paper rect cut to the tiles whose pixel centres can reach the box of the
 // alpha >= 1/255 ellipse {q <= qm} of the f32 conic.  Canonical f32 order
 // with conservative rounding bounds (it decides integers: the tile lists).
-__device__ __forceinline__ void tight_rect(float u, float v, float A, float B, float C, float qmax,
-                                           uint32_t& x0, uint32_t& x1, uint32_t& y0, uint32_t& y1) {
-  if (!(qmax >= 0.f)) { x0 = x1 = y0 = y1 = 0; return; }      // o < 1/255: no pixel blends
+// Returns q_m (R35), or +inf if the rect stays the paper's (no R37 pruning).
+__device__ __forceinline__ float tight_rect(float u, float v, float A, float B, float C, float qmax,
+                                            uint32_t& x0, uint32_t& x1, uint32_t& y0, uint32_t& y1) {
+  const float INF = __int_as_float(0x7f800000);
+  if (!(qmax >= 0.f)) { x0 = x1 = y0 = y1 = 0; return INF; }    // o < 1/255: no pixel blends
   const float AC = fm(A, C), BB = fm(B, B);
   const float Dlo = fs(fs(AC, BB), fm(9.5367431640625e-07f, fa(AC, BB)));   // D >= Dlo
-  if (!(Dlo > 0.f) || !(A > 0.f) || !(C > 0.f)) return;        // degenerate: keep the paper rect
+  if (!(Dlo > 0.f) || !(A > 0.f) || !(C > 0.f)) return INF;     // degenerate: keep the paper rect
   const float rD = fd(1.f, Dlo);
   const float mag = fm(fm(qmax, rD), fa(fm(2.f, AC), fm(fm(2.f, fabsf(B)), fsq(AC))));
   const float qm = fa(fa(qmax, 1e-3f), fm(1e-5f, mag));
@@ -287,8 +289,32 @@ __device__ __forceinline__ void tight_rect(float u, float v, float A, float B, f
   const uint32_t nx1 = (uint32_t)fmaxf((float)x0, fminf((float)x1, hx));
   const uint32_t ny0 = (uint32_t)fmaxf((float)y0, fminf((float)y1, ly));
   const uint32_t ny1 = (uint32_t)fmaxf((float)y0, fminf((float)y1, hy));
-  if (nx0 >= nx1 || ny0 >= ny1) { x0 = x1 = y0 = y1 = 0; return; }
+  if (nx0 >= nx1 || ny0 >= ny1) { x0 = x1 = y0 = y1 = 0; return qm; }
   x0 = nx0; x1 = nx1; y0 = ny0; y1 = ny1;
+  return qm;
+}
+
+// R37: does tile (tx, ty)'s rectangle of pixel centres reach {q <= qm}?  The
+// minimum of the convex quadratic over the rectangle: 0 if the mean is
+// inside, else the least edge minimum.  Same f32 op order as the oracle.
+__device__ __forceinline__ bool tile_keeps(float u, float v, float A, float B, float C, float qm, int tx, int ty) {
+  const float dxl = fs(fa(fm(16.f, (float)tx), 0.5f), u), dxh = fs(fa(fm(16.f, (float)tx), 15.5f), u);
+  const float dyl = fs(fa(fm(16.f, (float)ty), 0.5f), v), dyh = fs(fa(fm(16.f, (float)ty), 15.5f), v);
+  if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return true;
+  float best = __int_as_float(0x7f800000), mag = 0.f;
+  const float B2 = fm(2.f, B), aA = fabsf(A), aB2 = fm(2.f, fabsf(B)), aC = fabsf(C);
+  auto consider = [&](float dx, float dy) {
+    const float q = fa(fa(fm(fm(A, dx), dx), fm(fm(B2, dx), dy)), fm(fm(C, dy), dy));
+    if (q < best) {
+      best = q;
+      mag = fa(fa(fm(fm(aA, dx), dx), fm(fm(aB2, fabsf(dx)), fabsf(dy))), fm(fm(aC, dy), dy));
+    }
+  };
+  consider(dxl, fminf(fmaxf(fd(fm(-B, dxl), C), dyl), dyh));
+  consider(fminf(fmaxf(fd(fm(-B, dyl), A), dxl), dxh), dyl);
+  consider(dxh, fminf(fmaxf(fd(fm(-B, dxh), C), dyl), dyh));
+  consider(fminf(fmaxf(fd(fm(-B, dyh), A), dxl), dxh), dyh);
+  return best <= fa(fa(qm, 1e-3f), fm(1e-5f, mag));
 }
 
 constexpr int SH_MAX = 48;              // floats per Gaussian at degree 3
@@ -303,6 +329,7 @@ struct ProjSmem {
   uint16_t list[ENV_GROUP * PROJ_BLOCK];   // (k << 8) | local
 };
 
+template <bool ELL>   // GG_ELLIPSE_TILES (reading R37): per-record tile masks
 __global__ void __launch_bounds__(PROJ_BLOCK, 4)
 project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
                const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
@@ -423,6 +450,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     const float det = fs(fm(a, cc), fm(b, b));
     uint32_t x0 = 0, x1 = 0, y0 = 0, y1 = 0;
     float cA = 0.f, cB = 0.f, cC = 0.f;
+    float qm_r = __int_as_float(0x7f800000);   // R35 q_m (+inf: no R37 pruning)
     if (det > 0.f) {
       cA = fd(cc, det); cB = fd(-b, det); cC = fd(a, det);
       // O2.5 radius
@@ -436,10 +464,23 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
       const float fy1 = fminf(fmaxf(ceilf(fm(fa(v, rr), 0.0625f)), 0.f), (float)rp.TY);
       if (fx0 < fx1 && fy0 < fy1) {
         x0 = (uint32_t)fx0; x1 = (uint32_t)fx1; y0 = (uint32_t)fy0; y1 = (uint32_t)fy1;
-        if (rp.tight) tight_rect(u, v, cA, cB, cC, __ldg(&scn.qmax[gi]), x0, x1, y0, y1);
+        if (rp.tight) qm_r = tight_rect(u, v, cA, cB, cC, __ldg(&scn.qmax[gi]), x0, x1, y0, y1);
       }
     }
-    const uint32_t ntiles = (x1 - x0) * (y1 - y0);
+    uint32_t ntiles = (x1 - x0) * (y1 - y0);
+    if (ELL) {
+      uint32_t m = 0xffffffffu;
+      if (ntiles > 0u && ntiles <= 32u && qm_r < __int_as_float(0x7f800000)) {
+        const uint32_t w = x1 - x0;
+        m = 0u;
+        for (uint32_t b = 0; b < ntiles; ++b) {
+          const uint32_t ry = b / w, rx = b - ry * w;
+          if (tile_keeps(u, v, cA, cB, cC, qm_r, (int)(x0 + rx), (int)(y0 + ry))) m |= 1u << b;
+        }
+        ntiles = __popc(m);
+      }
+      ws.rmask[r] = m;
+    }
     // O2.8 colour
     float col[3] = {0.f, 0.f, 0.f};
     const int cdeg = c.degree;
@@ -505,7 +546,10 @@ void launch_scan_blocks(int ec, int nblk, uint32_t* data, uint32_t* totals, cuda
 
 void launch_project(int e0, int ngroups, int nblk, int max_degree, const EnvGroup* groups, const EnvConst* envs,
                     const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
-  project_kernel<<<dim3(ngroups, nblk), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws);
+  if (rp.ellipse)
+    project_kernel<true><<<dim3(ngroups, nblk), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws);
+  else
+    project_kernel<false><<<dim3(ngroups, nblk), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws);
 }
 
 }  // namespace gg

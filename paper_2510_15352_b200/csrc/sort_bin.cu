@@ -326,7 +326,9 @@ depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const u
 
 // ---- tile placement ------------------------------------------------------
 // order[rb + j] = record (gid-ordered local index) of depth rank j
+template <bool MASK>   // R37 tile masks present (GG_ELLIPSE_TILES)
 __device__ __forceinline__ void place_upsweep_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws, const uint32_t* order, int ntiles, int TX, uint32_t* thist, uint32_t* h) {
+  const uint32_t* rmask = MASK ? ws.rmask : nullptr;
   const int e = block_env(bt, b);
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
@@ -334,17 +336,27 @@ __device__ __forceinline__ void place_upsweep_block(uint32_t b, const BlockTable
   for (int i = threadIdx.x; i < ntiles; i += SB_THREADS) h[i] = 0u;
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < n; i += SB_THREADS) {
-    const uint2 r = ws.rect[rb + order[rb + j0 + i]];
+    const uint32_t idx = order[rb + j0 + i];
+    const uint2 r = ws.rect[rb + idx];
     uint32_t x0, x1, y0, y1;
     unpack_rect(r, x0, x1, y0, y1);
-    for (uint32_t ty = y0; ty < y1; ++ty)
-      for (uint32_t tx = x0; tx < x1; ++tx) atomicAdd(&h[ty * TX + tx], 1u);
+    const uint32_t w = x1 - x0, area = w * (y1 - y0);
+    const uint32_t m = rec_mask(rmask, rb + idx, area);
+    if (m != 0xffffffffu) {                       // R37 mask: the kept tiles only
+      for (uint32_t mm = m; mm; mm &= mm - 1u) {
+        const uint32_t b = __ffs(mm) - 1, ry = b / w;
+        atomicAdd(&h[(y0 + ry) * TX + x0 + (b - ry * w)], 1u);
+      }
+    } else {
+      for (uint32_t ty = y0; ty < y1; ++ty)
+        for (uint32_t tx = x0; tx < x1; ++tx) atomicAdd(&h[ty * TX + tx], 1u);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < ntiles; i += SB_THREADS) thist[(size_t)b * ntiles + i] = h[i];
 }
 
-template <bool LOOP>
+template <bool LOOP, bool MASK>
 __global__ void __launch_bounds__(SB_THREADS)
 place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntiles, int TX, uint32_t* thist) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -352,13 +364,13 @@ place_upsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, int ntile
   if (!chunk_ok(ws.ok)) return;
   const uint32_t nb = bt.blk_base[bt.ec];
   if (!LOOP) {                                     // one CTA per block (sync mode)
-    if (blockIdx.x < nb) place_upsweep_block(blockIdx.x, bt, ws, order, ntiles, TX, thist, h);
+    if (blockIdx.x < nb) place_upsweep_block<MASK>(blockIdx.x, bt, ws, order, ntiles, TX, thist, h);
     return;
   }
   for (;;) {   // async mode: bounded grid, blocks taken dynamically
     const uint32_t b = next_block(bt.q);
     if (b >= nb) break;
-    place_upsweep_block(b, bt, ws, order, ntiles, TX, thist, h);
+    place_upsweep_block<MASK>(b, bt, ws, order, ntiles, TX, thist, h);
   }
 }
 
@@ -409,7 +421,7 @@ __global__ void __launch_bounds__(SB_THREADS) place_scan_kernel(BlockTable bt, C
 // warp walks its records in order, 32 (record, tile) pairs per step, ranks
 // equal tiles among the lanes with a ballot multisplit and writes each
 // record index at its final slot; no block barrier inside the walk.
-template <int TB>   // tile-id bits (compile time: the multisplit fully unrolls)
+template <int TB, bool MASK>   // tile-id bits (compile time: the multisplit fully unrolls); R37 masks
 __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws,
                                                       const uint32_t* order, const RenderParams& rp,
                                                       const uint32_t* thist, int S, unsigned char* smem_raw) {
@@ -439,13 +451,24 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
   if (warp < S) {
     uint32_t* h = wh + (size_t)warp * nw2;
     for (uint32_t j = s0 + lane; j < s1; j += 32) {
-      const uint2 r = ws.rect[rb + order[rb + j0 + j]];
+      const uint32_t idx = order[rb + j0 + j];
+      const uint2 r = ws.rect[rb + idx];
       const uint32_t x0 = r.x & 0xffffu, x1 = r.x >> 16, y0 = r.y & 0xffffu, y1 = r.y >> 16;
-      for (uint32_t ty = y0; ty < y1; ++ty)
-        for (uint32_t tx = x0; tx < x1; ++tx) {
-          const uint32_t t = ty * rp.TX + tx;
+      const uint32_t w = x1 - x0;
+      const uint32_t m = rec_mask(MASK ? ws.rmask : nullptr, rb + idx, w * (y1 - y0));
+      if (m != 0xffffffffu) {                     // R37 mask: the kept tiles only
+        for (uint32_t mm = m; mm; mm &= mm - 1u) {
+          const uint32_t b = __ffs(mm) - 1, ry = b / w;
+          const uint32_t t = (y0 + ry) * rp.TX + x0 + (b - ry * w);
           atomicAdd(&h[t >> 1], 1u << (16 * (t & 1)));
         }
+      } else {
+        for (uint32_t ty = y0; ty < y1; ++ty)
+          for (uint32_t tx = x0; tx < x1; ++tx) {
+            const uint32_t t = ty * rp.TX + tx;
+            atomicAdd(&h[t >> 1], 1u << (16 * (t & 1)));
+          }
+      }
     }
   }
   __syncthreads();
@@ -475,7 +498,9 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
       x0 = r.x & 0xffffu; x1 = r.x >> 16; y0 = r.y & 0xffffu; y1 = r.y >> 16;
     }
     const uint32_t w = x1 - x0;
-    const uint32_t np = w * (y1 - y0);
+    const uint32_t area = w * (y1 - y0);
+    const uint32_t msk = j < s1 ? rec_mask(MASK ? ws.rmask : nullptr, rb + idx, area) : 0xffffffffu;
+    const uint32_t np = msk != 0xffffffffu ? rec_tiles(msk, area) : area;
     uint32_t incl = np;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -498,10 +523,14 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
       const uint32_t o_w = __shfl_sync(0xffffffffu, w, src);
       const uint32_t o_xy = __shfl_sync(0xffffffffu, xy0, src);
       const uint32_t o_idx = __shfl_sync(0xffffffffu, idx, src);
+      const uint32_t o_msk = MASK ? __shfl_sync(0xffffffffu, msk, src) : 0xffffffffu;
       uint32_t t = 0;
       if (ok) {
+        // the record's qq-th listed tile: the qq-th set bit of its R37 mask,
+        // else the qq-th tile of the rect (row-major)
+        uint32_t qq = f - o_ex;
+        if (o_msk != 0xffffffffu) qq = __fns(o_msk, 0u, (int)qq + 1);
         // qq / o_w for small integers via the f32 reciprocal (exact: qq < 2^20, o_w < 2^16)
-        const uint32_t qq = f - o_ex;
         const uint32_t row = (uint32_t)__fdividef((float)qq + 0.5f, (float)o_w);
         t = ((o_xy >> 16) + row) * rp.TX + (o_xy & 0xffffu) + (qq - row * o_w);
       }
@@ -535,7 +564,7 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
   }
 }
 
-template <int TB, bool LOOP>
+template <int TB, bool LOOP, bool MASK>
 __global__ void __launch_bounds__(PD_THREADS, 3)
 place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderParams rp, const uint32_t* thist,
                        int S) {
@@ -543,13 +572,13 @@ place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderP
   if (!chunk_ok(ws.ok)) return;
   const uint32_t nb = bt.blk_base[bt.ec];
   if (!LOOP) {                                     // one CTA per block (sync mode)
-    if (blockIdx.x < nb) place_downsweep_block<TB>(blockIdx.x, bt, ws, order, rp, thist, S, smem_raw);
+    if (blockIdx.x < nb) place_downsweep_block<TB, MASK>(blockIdx.x, bt, ws, order, rp, thist, S, smem_raw);
     return;
   }
   for (;;) {   // async mode: bounded grid, blocks taken dynamically
     const uint32_t b = next_block(bt.q);
     if (b >= nb) break;
-    place_downsweep_block<TB>(b, bt, ws, order, rp, thist, S, smem_raw);
+    place_downsweep_block<TB, MASK>(b, bt, ws, order, rp, thist, S, smem_raw);
   }
 }
 
@@ -571,22 +600,31 @@ size_t place_down_smem(int ntiles) {
   return (size_t)ntiles * 4 + (size_t)place_segments(ntiles) * place_seg_bytes(ntiles);
 }
 
+template <bool LOOP, bool MASK>
+static cudaError_t place_init_variant() {
+  cudaError_t e = cudaFuncSetAttribute(place_downsweep_kernel<8, LOOP, MASK>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(place_downsweep_kernel<11, LOOP, MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           72 * 1024);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(place_downsweep_kernel<13, LOOP, MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           72 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(place_upsweep_kernel<LOOP, MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(MAX_TILES * 4));
+}
+
 template <bool LOOP>
 static cudaError_t sort_bin_init_variant() {
   cudaError_t e = cudaFuncSetAttribute(depth_downsweep_kernel<LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)depth_down_smem());
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(place_downsweep_kernel<8, LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           72 * 1024);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(place_downsweep_kernel<11, LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           72 * 1024);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(place_downsweep_kernel<13, LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           72 * 1024);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(place_upsweep_kernel<LOOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(MAX_TILES * 4));
+  for (int mask = 0; mask < 2; ++mask) {
+    e = mask ? place_init_variant<LOOP, true>() : place_init_variant<LOOP, false>();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t sort_bin_init() {
@@ -634,17 +672,24 @@ static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, con
   }
   const uint32_t* order = ((passes - 1) & 1) ? ws.dv1 : ws.dv0;   // values of the last depth pass
   if (LOOP) bt.q = qctr + qi++;
-  place_upsweep_kernel<LOOP><<<g2, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
+  const bool mask = ws.rmask != nullptr;
+  if (mask)
+    place_upsweep_kernel<LOOP, true><<<g2, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
+  else
+    place_upsweep_kernel<LOOP, false><<<g2, SB_THREADS, rp.ntiles * 4, s>>>(bt, ws, order, rp.ntiles, rp.TX, thist);
   place_scan_kernel<<<ec, SB_THREADS, 0, s>>>(bt, ws, thist, rp.ntiles);
   if (LOOP) bt.q = qctr + qi++;
   const size_t psm = place_down_smem(rp.ntiles);
   const int S = place_segments(rp.ntiles);
   if (rp.ntiles <= 256)
-    place_downsweep_kernel<8, LOOP><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+    mask ? place_downsweep_kernel<8, LOOP, true><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S)
+         : place_downsweep_kernel<8, LOOP, false><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   else if (rp.ntiles <= 2048)
-    place_downsweep_kernel<11, LOOP><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+    mask ? place_downsweep_kernel<11, LOOP, true><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S)
+         : place_downsweep_kernel<11, LOOP, false><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   else
-    place_downsweep_kernel<13, LOOP><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
+    mask ? place_downsweep_kernel<13, LOOP, true><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S)
+         : place_downsweep_kernel<13, LOOP, false><<<g2, PD_THREADS, psm, s>>>(bt, ws, order, rp, thist, S);
   return launches + 3;
 }
 

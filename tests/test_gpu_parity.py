@@ -51,12 +51,14 @@ def render(gg, r, ids, cams, want_depth=True, want_alpha=True, fmt=0, **kw):
 
 
 def parity_envs(gg, r, scenes, sids, cams, envs, tally, ints=True, sh_degree=-1, background=(0.0, 0.0, 0.0),
-                tight=False, **kw):
+                tight=False, ellipse=False, **kw):
     """Render all envs on the GPU; compare `envs` with the oracle (and their
     integer artefacts, one debug render per env).  tight: GG_TIGHT_TILES on
-    the GPU, F_TIGHT in the oracle (reading R35)."""
+    the GPU, F_TIGHT in the oracle (reading R35); ellipse: GG_ELLIPSE_TILES /
+    F_ELLIPSE (reading R37)."""
     kw["background"] = background
-    gflag = gg.GG_TIGHT_TILES if tight else 0
+    gflag = gg.GG_ELLIPSE_TILES if ellipse else (gg.GG_TIGHT_TILES if tight else 0)
+    oflag = oracle.F_ELLIPSE if ellipse else (oracle.F_TIGHT if tight else 0)
     rgb, depth, alpha = render(gg, r, sids, cams, sh_degree=sh_degree, flags=gflag, **kw)
     oscenes = {}
     for e in envs:
@@ -65,7 +67,7 @@ def parity_envs(gg, r, scenes, sids, cams, envs, tally, ints=True, sh_degree=-1,
             oscenes[s] = oracle.OracleScene.from_inputs(scenes[s])
         o = oracle.render_env(oscenes[s], cams.viewmats[e], cams.intrinsics[e], cams.width, cams.height,
                               sh_degree=sh_degree, background=tuple(float(np.float32(b)) for b in background),
-                              flags=oracle.F_TIGHT if tight else 0)
+                              flags=oflag)
         tally.add(rgb[e], depth[e], alpha[e], o)
         if ints:
             render(gg, r, sids, cams, sh_degree=sh_degree,
