@@ -29,7 +29,7 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def _run(gg, scenes, ids, cams, sample, depth=True, ints_env=None):
+def _run(gg, scenes, ids, cams, sample, depth=True, ints_env=None, flags=0, oflags=0):
     r = gg.Renderer(0)
     try:
         sid_map = {}
@@ -41,7 +41,7 @@ def _run(gg, scenes, ids, cams, sample, depth=True, ints_env=None):
         rgb = torch.empty((E, H, W, 3), dtype=torch.uint8, device="cuda")
         dep = torch.empty((E, H, W), dtype=torch.float32, device="cuda") if depth else None
         vm, K = dev(cams.viewmats), dev(cams.intrinsics)
-        r.render(dev_ids, vm, K, W, H, rgb=rgb, depth=dep)
+        r.render(dev_ids, vm, K, W, H, rgb=rgb, depth=dep, flags=flags)
         gg.gg_check_errors(r.ctx)
         torch.cuda.synchronize()
         t = Tally()
@@ -50,11 +50,12 @@ def _run(gg, scenes, ids, cams, sample, depth=True, ints_env=None):
             k = int(ids[e])
             if k not in osc:
                 osc[k] = oracle.OracleScene.from_inputs(scenes[k])
-            o = oracle.render_env(osc[k], cams.viewmats[e], cams.intrinsics[e], W, H)
+            o = oracle.render_env(osc[k], cams.viewmats[e], cams.intrinsics[e], W, H, flags=oflags)
             t.add(rgb[e].cpu().numpy(), None if dep is None else dep[e].cpu().numpy(), None, o)
             if e == ints_env:
                 # integer artefacts of this env from a second full-batch render
-                r.render(dev_ids, vm, K, W, H, rgb=rgb, depth=dep, flags=gg.GG_KEEP_INTERMEDIATES, debug_env=e)
+                r.render(dev_ids, vm, K, W, H, rgb=rgb, depth=dep, flags=gg.GG_KEEP_INTERMEDIATES | flags,
+                         debug_env=e)
                 torch.cuda.synchronize()
                 check_integer_dumps(gg, r.ctx, o, scenes[k].n)
         print(t)
@@ -67,6 +68,15 @@ def test_c3_sampled(gg):
     sc = gi.config_scene("c3")
     cams = gi.config_cameras("c3", sc)
     _run(gg, {0: sc}, np.zeros(cams.n, np.int32), cams, [0, 1111, 2047, 4095], ints_env=2047)
+
+
+def test_c3_sampled_bench_lists(gg):
+    """The configuration bench.py times: all 4,096 envs in one render with the
+    opacity-aware tile rects (GG_TIGHT_TILES, reading R35)."""
+    sc = gi.config_scene("c3")
+    cams = gi.config_cameras("c3", sc)
+    _run(gg, {0: sc}, np.zeros(cams.n, np.int32), cams, [7, 2500, 4000], ints_env=2500,
+         flags=gg.GG_TIGHT_TILES, oflags=oracle.F_TIGHT)
 
 
 def test_c2_sampled(gg):
