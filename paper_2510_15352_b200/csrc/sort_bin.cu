@@ -135,8 +135,15 @@ __device__ __forceinline__ void depth_upsweep_block(uint32_t b, const BlockTable
   const uint32_t zmin = ws.zmin[e];
   for (int i = threadIdx.x; i < DS_RADIX; i += DS_THREADS) h[i] = 0;
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n; i += DS_THREADS)
-    atomicAdd(&h[depth_digit(io.kin[rb + j0 + i], zmin, shift)], 1u);
+  uint32_t k[DS_IPT];                              // all of this thread's keys in flight first
+#pragma unroll
+  for (int j = 0; j < DS_IPT; ++j) {
+    const uint32_t i = threadIdx.x + j * DS_THREADS;
+    k[j] = i < n ? io.kin[rb + j0 + i] : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < DS_IPT; ++j)
+    if (threadIdx.x + j * DS_THREADS < n) atomicAdd(&h[depth_digit(k[j], zmin, shift)], 1u);
   __syncthreads();
   for (int i = threadIdx.x; i < DS_RADIX; i += DS_THREADS) ghist[(size_t)b * DS_RADIX + i] = h[i];
 }
