@@ -351,8 +351,8 @@ __device__ __forceinline__ void place_upsweep_block(uint32_t b, const BlockTable
     const uint32_t m = rec_mask(rmask, rb + idx, area);
     if (m != 0xffffffffu) {                       // R37 mask: the kept tiles only
       for (uint32_t mm = m; mm; mm &= mm - 1u) {
-        const uint32_t b = __ffs(mm) - 1, ry = b / w;
-        atomicAdd(&h[(y0 + ry) * TX + x0 + (b - ry * w)], 1u);
+        const uint32_t bit = __ffs(mm) - 1, ry = bit / w;
+        atomicAdd(&h[(y0 + ry) * TX + x0 + (bit - ry * w)], 1u);
       }
     } else {
       for (uint32_t ty = y0; ty < y1; ++ty)
@@ -465,8 +465,8 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
       const uint32_t m = rec_mask(MASK ? ws.rmask : nullptr, rb + idx, w * (y1 - y0));
       if (m != 0xffffffffu) {                     // R37 mask: the kept tiles only
         for (uint32_t mm = m; mm; mm &= mm - 1u) {
-          const uint32_t b = __ffs(mm) - 1, ry = b / w;
-          const uint32_t t = (y0 + ry) * rp.TX + x0 + (b - ry * w);
+          const uint32_t bit = __ffs(mm) - 1, ry = bit / w;
+          const uint32_t t = (y0 + ry) * rp.TX + x0 + (bit - ry * w);
           atomicAdd(&h[t >> 1], 1u << (16 * (t & 1)));
         }
       } else {
