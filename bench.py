@@ -63,11 +63,30 @@ def parse():
     p.add_argument("--outputs", default="rgbd", choices=["rgbd", "rgb", "depth"],
                    help="rgbd (the headline), rgb only, or depth-only (rgb = NULL: no SH/colour work; the paper's "
                         "depth-only baseline)")
+    p.add_argument("--scenes", type=int, default=0,
+                   help="scenes the envs are bound to (seeded uniform binding, SURVEY §8(d).1 c4); 0 = one scene "
+                        "(c1-c3) or the config's count (c4: 256; use 128 for the paper's point, PAPER.md:173)")
     p.add_argument("--blur", type=int, default=0, help="motion blur with K samples (gg_render_blur); 0 = off")
     p.add_argument("--shutter", type=float, default=0.01, help="shutter time (s) for --blur")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo only to exercise the multi-rank path on a single-GPU box")
     return p.parse_args()
+
+
+def _room(args3):
+    k, n, d = args3
+    return gi.room_scene(100 + k, n, d)
+
+
+def make_scenes(args, c):
+    """The config's scene, or S seeded rooms (generated in parallel on the host)."""
+    S = c["n_scenes"]
+    if S == 1:
+        return [gi.config_scene(args.config, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])]
+    import concurrent.futures as cf
+    n_proc = max(1, min(16, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 4))
+    with cf.ProcessPoolExecutor(n_proc) as ex:
+        return list(ex.map(_room, [(k, c["n_gauss"], c["sh_degree"]) for k in range(S)]))
 
 
 def workload(args):
@@ -78,7 +97,9 @@ def workload(args):
         c["n_gauss"] = args.gaussians
     if args.sh is not None:
         c["sh_degree"] = args.sh
-    name = (f"{args.config}: 1 scene x {c['n_gauss']:,} Gaussians SH{c['sh_degree']}, {c['n_envs']} envs/GPU, "
+    c["n_scenes"] = args.scenes or (c.get("n_scenes", 1) if args.config in ("c4", "c5") else 1)
+    sc_txt = "1 scene" if c["n_scenes"] == 1 else f"{c['n_scenes']} scenes (seeded uniform binding)"
+    name = (f"{args.config}: {sc_txt} x {c['n_gauss']:,} Gaussians SH{c['sh_degree']}, {c['n_envs']} envs/GPU, "
             f"{c['width']}x{c['height']} {'RGB+D' if c['depth'] else 'RGB'}")
     if getattr(args, "blur", 0):
         name += f", motion blur K={args.blur} shutter {args.shutter}s"
@@ -229,11 +250,15 @@ def main():
     want_rgb = args.outputs != "depth"
 
     # ---- inputs: scene replica + pre-generated pose sets, resident in HBM
-    scene = gi.config_scene(args.config, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])
+    scenes = make_scenes(args, c)
+    S = len(scenes)
+    scene = scenes[0]
     R = gg.Renderer(gpu)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    sid = R.load_scene(t(scene.means), t(scene.scales), t(scene.quats), t(scene.opacities), t(scene.sh),
-                       scene.sh_degree)
+    sids = [R.load_scene(t(sc_.means), t(sc_.scales), t(sc_.quats), t(sc_.opacities), t(sc_.sh), sc_.sh_degree)
+            for sc_ in scenes]
+    binding = gi.scene_binding(7 + rank, E, S) if S > 1 else np.zeros(E, np.int32)
+    ids_np = np.asarray(sids, np.int32)[binding]
     gg.gg_reserve(R.ctx, E, W, H, args.chunk)
     use_async = args.mode == "async" and not args.blur
     if use_async:
@@ -242,10 +267,19 @@ def main():
     mflag = (gg.GG_ASYNC if use_async else 0) | tiles_flag
     n_sets = args.warmup + args.steps
     # a fresh, seeded pose set for every step, all resident in HBM
-    vm = np.stack([gi.cameras(10_000 * (rank + 1) + s, E, W, H, scene).viewmats for s in range(n_sets)])
+    def pose_set(s):
+        if S == 1:
+            return gi.cameras(10_000 * (rank + 1) + s, E, W, H, scene).viewmats
+        V = np.empty((E, 4, 4), np.float32)
+        for k in range(S):                       # each env's camera lives in its own scene
+            idx = np.flatnonzero(binding == k)
+            if idx.size:
+                V[idx] = gi.cameras(10_000 * (rank + 1) + 4096 * s + k, idx.size, W, H, scenes[k]).viewmats
+        return V
+    vm = np.stack([pose_set(s) for s in range(n_sets)])
     intr = t(np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1)))
     vm_d = t(vm)
-    ids = torch.full((E,), sid, dtype=torch.int32, device=dev)
+    ids = t(ids_np)
     rgb = torch.empty((E, H, W, 3), dtype=torch.uint8, device=dev) if want_rgb else None
     depth = torch.empty((E, H, W), dtype=torch.float32, device=dev) if want_depth else None
     stream = torch.cuda.current_stream()
@@ -317,7 +351,7 @@ def main():
     # ---- e2e through the public API with host buffers (pinned)
     e2e = None
     if not args.no_e2e:
-        h_ids = np.full(E, sid, np.int32)
+        h_ids = ids_np
         h_vm = vm[: max(2, min(n_sets, 4))]
         h_in = np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1))
         h_rgb = torch.empty((E, H, W, 3), dtype=torch.uint8).pin_memory() if want_rgb else None
@@ -382,7 +416,7 @@ def main():
     sh_eff = scene.sh_degree if want_rgb else 0
     b_g = 60 + (4 * 3 * (sh_eff + 1) ** 2 if sh_eff > 0 else 0)     # scene bytes per Gaussian
     ops_proj = E * scene.n * 25 + n_vis * (150 + (130 if sh_eff > 0 else 0))
-    by_proj = scene.n * b_g + n_vis * 60
+    by_proj = S * scene.n * b_g + n_vis * 60
     passes = 3                                                     # 10-bit digits over the ~26-bit depth span
     by_sort = n_vis * 8 * 2 * passes + n_vis * 4 + n_keys * 12
     by_out = E * W * H * ((3 if want_rgb else 0) + (4 if want_depth else 0))
@@ -407,8 +441,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cams0 = gi.Cameras(vm[0], np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1)), W, H)
-        envs = list(range(min(args.cpu_envs, E)))
-        dt, cores = oracle_sample(scene, cams0, envs, -1)
+        envs = [int(e) for e in np.flatnonzero(binding == binding[0])[: max(1, min(args.cpu_envs, E))]]
+        dt, cores = oracle_sample(scenes[int(binding[0])], cams0, envs, -1)
         cpu = {"value": len(envs) / dt, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"{len(envs)} envs of pose set 0 (full {W}x{H} frames, {scene.n:,} Gaussians "
                          f"SH{scene.sh_degree}), incl. O1 preprocessing"}
@@ -419,7 +453,7 @@ def main():
                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                "config": {"workload": name + ("" if want_rgb and want_depth == c["depth"] else
                                               " [depth-only outputs]" if not want_rgb else " [RGB-only outputs]"),
-                          "envs_per_gpu": E, "total_envs": E * world, "n_gauss": scene.n,
+                          "envs_per_gpu": E, "total_envs": E * world, "n_gauss": scene.n, "n_scenes": S,
                           "sh_degree": scene.sh_degree, "width": W, "height": H, "depth": want_depth, "rgb": want_rgb,
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
