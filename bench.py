@@ -55,8 +55,10 @@ def parse():
     p.add_argument("--cpu-envs", type=int, default=4, help="oracle sample size for cpu_baseline")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--mode", default="sync", choices=["async", "sync"],
-                   help="async: sync-free GG_ASYNC render (default); sync: host-sized workspace per chunk")
+    p.add_argument("--mode", default="sync", choices=["async", "sync", "graph"],
+                   help="sync (default): host-sized workspace per chunk; async: sync-free GG_ASYNC render; graph: "
+                        "the GG_ASYNC render captured once in a CUDA graph, each step copying its poses into the "
+                        "graph's input buffer and replaying it (SURVEY §8(f) row 2)")
     p.add_argument("--tiles", default="tight", choices=["paper", "tight", "ellipse"],
                    help="tile lists: the paper's 3-sigma circle rects, opacity-aware rects (GG_TIGHT_TILES), or those "
                         "plus ellipse-intersects-tile masks (GG_ELLIPSE_TILES); images are identical")
@@ -260,7 +262,7 @@ def main():
     binding = gi.scene_binding(7 + rank, E, S) if S > 1 else np.zeros(E, np.int32)
     ids_np = np.asarray(sids, np.int32)[binding]
     gg.gg_reserve(R.ctx, E, W, H, args.chunk)
-    use_async = args.mode == "async" and not args.blur
+    use_async = args.mode in ("async", "graph") and not args.blur
     if use_async:
         gg.gg_reserve_async(R.ctx, E, W, H, args.chunk, 0.7, 4.0)
     tiles_flag = {"paper": 0, "tight": gg.GG_TIGHT_TILES, "ellipse": gg.GG_ELLIPSE_TILES}[args.tiles]
@@ -289,7 +291,14 @@ def main():
         lin_d = t(np.float32(g.normal(0.0, 0.5, (E, 3))))       # m/s (robot base speeds)
         ang_d = t(np.float32(g.normal(0.0, 1.0, (E, 3))))       # rad/s (stair jolts)
 
+    graph = None
+    vm_static = None
+
     def step(s, **kw):
+        if graph is not None:
+            vm_static.copy_(vm_d[s])            # this step's poses into the captured input
+            graph.replay()
+            return
         if args.blur:
             kw["flags"] = kw.get("flags", 0) | tiles_flag
             gg.gg_render_blur(R.ctx, E, ids, vm_d[s], intr, lin_d, ang_d, args.shutter, args.blur, W, H,
@@ -310,8 +319,25 @@ def main():
                  None, stream)
     r_eval, r_contrib, r_vis, r_keys = (int(x) * kb for x in gg.gg_get_counters(R.ctx, E).sum(axis=0))
 
+    # ---- graph mode: capture one render (timing off: events would be captured)
+    graph_launches = 0
+    if args.mode == "graph" and use_async:
+        vm_static = vm_d[0].clone()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):             # warm-up outside the capture
+            gg.gg_render(R.ctx, E, ids, vm_static, intr, W, H, gg.default_opts(flags=mflag), rgb, depth, None, cap)
+        stream.wait_stream(cap)
+        torch.cuda.synchronize()
+        l0 = gg.gg_launch_count(R.ctx)
+        g_ = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_, stream=cap):
+            gg.gg_render(R.ctx, E, ids, vm_static, intr, W, H, gg.default_opts(flags=mflag), rgb, depth, None, cap)
+        graph_launches = gg.gg_launch_count(R.ctx) - l0
+        graph = g_
+
     # ---- warm-up + timed region
-    gg.gg_set_timing(R.ctx, True)
+    gg.gg_set_timing(R.ctx, graph is None)
     for w in range(args.warmup):
         step(w % n_sets)
     torch.cuda.synchronize()
@@ -327,15 +353,25 @@ def main():
     ev0.record(stream)
     for k in range(args.steps):
         step(args.warmup + k)
-        stage += np.array(gg.gg_get_stage_ms(R.ctx))
+        if graph is None:
+            stage += np.array(gg.gg_get_stage_ms(R.ctx))
     ev1.record(stream)
     torch.cuda.synchronize()
     gg.gg_check_errors(R.ctx)          # async mode reports capacity overflow here
-    launches = gg.gg_launch_count(R.ctx) - launches0
+    launches = gg.gg_launch_count(R.ctx) - launches0 + graph_launches * args.steps * (graph is not None)
     clocks = clk.stop()
     if world > 1:
         dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
+    if graph is not None:
+        # the stage split of the captured render, from the same render issued
+        # outside the graph (untimed for the metric)
+        graph = None
+        gg.gg_set_timing(R.ctx, True)
+        for k in range(args.steps):
+            step(args.warmup + k)
+            stage += np.array(gg.gg_get_stage_ms(R.ctx))
+        torch.cuda.synchronize()                # (its last render is the last timed pose set)
     gg.gg_set_timing(R.ctx, False)
 
     # ---- digest of the last frame set, C1 all_gather
@@ -457,7 +493,9 @@ def main():
                           "sh_degree": scene.sh_degree, "width": W, "height": H, "depth": want_depth, "rgb": want_rgb,
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
-                          "chunk_envs": args.chunk or 1024, "render_mode": "async (GG_ASYNC)" if use_async else "sync",
+                          "chunk_envs": args.chunk or 1024, "render_mode": {"sync": "sync", "async": "async (GG_ASYNC)",
+                                          "graph": "GG_ASYNC render replayed from a CUDA graph"}[args.mode]
+                          if not args.blur else "sync",
                           "tile_lists": {"paper": "paper 3-sigma circle rects",
                                          "tight": "opacity-aware rects (GG_TIGHT_TILES, reading R35)",
                                          "ellipse": "opacity-aware rects + ellipse-tile masks (GG_ELLIPSE_TILES, R35+R37)"
