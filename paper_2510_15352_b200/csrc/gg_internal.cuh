@@ -55,6 +55,7 @@ __device__ __forceinline__ EnvConst load_cam(const EnvConst* p) {
 // A run of <= ENV_GROUP chunk-local envs bound to the same scene; the
 // projection kernels load each Gaussian once and test it against the group.
 constexpr int ENV_GROUP = 16;
+static_assert(ENV_GROUP <= 32, "cull_count keeps one env per lane");
 struct EnvGroup {
   int32_t elo;   // first chunk-local env
   int32_t cnt;   // envs in the group (1..ENV_GROUP)

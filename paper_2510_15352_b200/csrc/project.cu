@@ -136,6 +136,9 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
   float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
   float smax2 = 0.f;
   const int wi = blockIdx.y * (PROJ_BLOCK / 32) + warp;
+  // lane k keeps env k's visibility word and depth-key range (no per-env
+  // branch in the loop; ENV_GROUP <= 32)
+  uint32_t my_word = 0u, my_zmn = 0xffffffffu, my_zmx = 0u;
   for (int k = 0; k < grp.cnt; ++k) {
     const EnvConst c = load_cam(&cams[k]);
     if (c.scene != cur) {             // uniform across the CTA
@@ -152,13 +155,14 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
     // depth-key range of the kept records (= the env's record set): sort key offset
     const uint32_t zmn = __reduce_min_sync(0xffffffffu, keep ? zb : 0xffffffffu);
     const uint32_t zmx = __reduce_max_sync(0xffffffffu, keep ? zb : 0u);
-    if (lane == 0) {
-      ws.flags[(size_t)(grp.elo + k) * ws.nwords + wi] = word;
-      wc[k][warp] = __popc(word);
-      if (word) {
-        atomicMin(&szmn[k], zmn);
-        atomicMax(&szmx[k], zmx);
-      }
+    if (lane == k) { my_word = word; my_zmn = zmn; my_zmx = zmx; }
+  }
+  if (lane < grp.cnt) {
+    ws.flags[(size_t)(grp.elo + lane) * ws.nwords + wi] = my_word;
+    wc[lane][warp] = __popc(my_word);
+    if (my_word) {
+      atomicMin(&szmn[lane], my_zmn);
+      atomicMax(&szmx[lane], my_zmx);
     }
   }
   __syncthreads();
