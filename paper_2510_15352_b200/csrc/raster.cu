@@ -14,15 +14,16 @@
 // BEFORE the exponential, and alpha = min(0.99, ex2(x)) (MUFU.EX2) only for
 // Gaussians that can contribute.
 //
-// Decomposition: one CTA of 256 threads per (tile, env), one pixel per
-// thread; warp w covers an 8x4 pixel block.  Records are gathered through
-// the tile's sorted index list into shared memory 256 at a time; the
-// loading thread also computes an 8-bit mask of the warps whose 8x4 block
-// intersects the record's alpha >= 1/255 ellipse box (K1b stores its half
-// extents with safety margins).  Each warp compacts the records whose bit it
-// holds into a per-warp list (ballot + popc, order preserved) and walks only
-// that list, so work is spent only where the cutoff can be passed — this never changes a blend decision.  Early-out:
-// warp vote ends a warp's walk; __syncthreads_count ends the tile.
+// Two kernels compute the same images bit for bit:
+//  * raster_kernel<COUNTERS> — the reference walk used for GG_COUNTERS (and
+//    the per-pixel n_eval dump): one CTA of 256 threads per (tile, env), one
+//    pixel per thread, records staged 256 at a time, every list entry counted
+//    as the definition's n_eval;
+//  * raster_warp_kernel<RGB> — the timed path (see its comment below): warps
+//    walk the list independently for their 8x8 blocks, two pixels per lane in
+//    packed f32x2, skipping records whose alpha >= 1/255 region cannot reach
+//    the block (exact, conservative), branch-free blending.
+// Skipping a record that cannot pass never changes a blend decision.
 #include "gg_internal.cuh"
 #include "f32x2.cuh"
 

@@ -7,20 +7,24 @@
 // canonical list (DESIGN.md §2 O3) is the triples (tile, depth bits, gid) in
 // ascending order.  We produce it without ever materialising 64-bit keys:
 //   1. stable LSD radix sort of every env's records (already in gid order)
-//      by the f32 depth bits: 4 passes of 8 bits               -> (z, gid)
+//      by the f32 depth bits minus the env's minimum: ceil(span bits / 10)
+//      passes of 10 bits (3 for a ~26-bit span)                -> (z, gid)
 //   2. stable bucketing of the records' tiles (row-major) by tile id, the
 //      records taken in depth order                          -> (tile, z, gid)
 //   3. the per-env tile totals' exclusive scan is the range table (K5).
 //
 // Each pass is three launches over the chunk's records, split into blocks
-// of 8192 that never straddle an env segment:
+// of 4096 that never straddle an env segment (a per-block env table):
 //   upsweep   — per-block histogram (digit or tile) -> global table
 //   scan      — one CTA per env: exclusive prefix over (digit, block) in
 //               digit-major order = each block's output offset per digit
 //   downsweep — the block ranks its elements stably (warp-owned 256-element
-//               slices, ballot multisplit, per-warp counters, prefix over
-//               warps), stages them in shared memory in digit order, and
-//               writes contiguous per-digit runs at the block's offsets.
+//               slices; equal digits found with warp-private stamps and
+//               peer masks; per-warp counters; prefix over warps), stages
+//               them in shared memory in digit order, and writes contiguous
+//               per-digit runs at the block's offsets.  The placement
+//               downsweep walks per-warp segments and expands each record's
+//               tiles 32 pairs at a time instead of staging.
 // Thousands of independent blocks per pass keep HBM busy; staged runs keep
 // the writes coalesced.  No float math, no order-dependent atomics:
 // identical inputs give bit-identical lists.
