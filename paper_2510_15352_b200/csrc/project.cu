@@ -19,10 +19,12 @@
 //       canonical rect keeps — one ballot word per (env, 32 Gaussians) and a
 //       count per (env, block).
 //   K2  scan: per-env exclusive scan of the block counts (compaction offsets).
-//   K1b project: the CTA stages its 256 Gaussians (geometry + SH) in shared
-//       memory, flattens the visible (env, Gaussian) pairs of the group in
-//       (env, Gaussian) order, and projects them with full warps, writing
-//       each record at its compacted, Gaussian-ordered slot.
+//   K1b project: the CTA flattens the visible (env, Gaussian) pairs of the
+//       group in (Gaussian, env) order (lanes that share a Gaussian read the
+//       same scene lines through L1), projects them with full warps (SH at a
+//       compile-time degree; optional R35 tight rect and R37 tile mask), and
+//       writes each record at its compacted, Gaussian-ordered slot (its rank
+//       among the env's visible Gaussians).
 #include "gg_internal.cuh"
 #include "canonical.cuh"
 
