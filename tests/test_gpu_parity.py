@@ -282,3 +282,17 @@ def test_ply_scene_renders_like_arrays(gg, R, tmp_path):
     b = render(gg, R, [sid_arr, sid_arr], cams)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("W,H", [(1280, 960), (1, 1), (17, 3)])
+def test_image_sizes(gg, R, W, H):
+    """> 2048 tiles (the 13-bit placement path), and degenerate tiny images."""
+    sc = gi.random_cloud(1300, 300, sh_degree=1)
+    cams = gi.cloud_cameras(1300, 2, W, H)
+    sid = load(R, sc)
+    t = Tally()
+    parity_envs(gg, R, {sid: sc}, [sid] * 2, cams, range(2), t)
+    t.check()
+    t2 = Tally()
+    parity_envs(gg, R, {sid: sc}, [sid] * 2, cams, range(2), t2, tight=True)
+    t2.check()
