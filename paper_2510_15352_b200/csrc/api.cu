@@ -403,7 +403,7 @@ gg_status gg_load_scene(gg_context* ctx, int64_t n, int32_t d, const float* mean
   slot.d.cov_b = P<float4>(slot.cov_b);
   slot.d.aux = P<float2>(slot.aux);
   slot.d.qmax = P<float>(slot.qmax);
-  slot.d.sh = d > 0 ? P<float>(slot.sh) : nullptr;
+  slot.d.sh4 = d > 0 ? P<float4>(slot.sh) : nullptr;
   slot.d.n = (int32_t)n;
   slot.d.degree = d;
   slot.d.sh_stride = sh_stride;

@@ -19,10 +19,10 @@ struct DevScene {
   const float4* cov_b;   // (Syz, Szz, dc_r, dc_g)
   const float2* aux;     // (dc_b, max_j s_j^2)
   const float* qmax;     // f32(2 ln(255 o)): alpha >= 1/255 <=> q <= qmax (reading R35)
-  const float* sh;       // [n][sh_stride] coefficient-major (k, ch), zero padded; null if d = 0
+  const float4* sh4;     // [sh_stride/4][n] float4 planes of the (k, ch) coefficients, zero padded; null if d = 0
   int32_t n;
   int32_t degree;
-  int32_t sh_stride;     // floats per Gaussian (multiple of 4)
+  int32_t sh_stride;     // floats per Gaussian (multiple of 4) = 4 x planes
   int32_t valid;
 };
 

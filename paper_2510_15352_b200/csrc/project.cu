@@ -96,6 +96,19 @@ __device__ __forceinline__ void load_group_cams(EnvConst* cams, const EnvConst* 
   for (int i = threadIdx.x; i < grp.cnt * words; i += blockDim.x) dst[i] = src[i];
 }
 
+// single MUFU ops (no denormal range fix-ups): operands here are normal and
+// the results only feed margin-protected tests
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // conservative footprint test (DESIGN.md §4 K1a): lambda1 <= a + c + sqrt(0.1)
 // and a + c <= s_max^2 |T|_F^2 + 0.6; generous margins absorb f32 rounding.
 __device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float smax2, const RenderParams& rp,
@@ -107,7 +120,7 @@ __device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float
   if (!(pz > rp.near_p && pz <= rp.far_p)) return false;
   const float px = fmaf(c.R[2], g.z, fmaf(c.R[1], g.y, fmaf(c.R[0], g.x, c.t[0])));
   const float py = fmaf(c.R[5], g.z, fmaf(c.R[4], g.y, fmaf(c.R[3], g.x, c.t[1])));
-  const float rz = __fdividef(1.f, pz);       // approximate: the test has margins
+  const float rz = rcp_approx(pz);             // approximate: the test has margins
   const float u = c.fx * px * rz + c.cx;
   const float v = c.fy * py * rz + c.cy;
   const float txz = fminf(c.lim_xp, fmaxf(-c.lim_xn, px * rz));
@@ -117,7 +130,7 @@ __device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float
   // |T|_F^2 = |J00 R0 + J02 R2|^2 + |J11 R1 + J12 R2|^2 <= rgram (J00^2 + J02^2 + J11^2 + J12^2)
   const float nT = c.rgram * fmaf(J00, J00, fmaf(J02, J02, fmaf(J11, J11, J12 * J12)));
   const float lam_b = (smax2 * nT + 0.9163f) * 1.001f + 0.01f;
-  const float rb = 3.f * (lam_b * rsqrtf(lam_b)) * 1.002f + 2.f;
+  const float rb = 3.f * (lam_b * rsqrt_approx(lam_b)) * 1.002f + 2.f;
   return (u + rb > 0.f) && (u - rb < (float)(rp.TX * TILE)) && (v + rb > 0.f) && (v - rb < (float)(rp.TY * TILE));
 }
 
@@ -242,19 +255,19 @@ __device__ __forceinline__ void sh_eval(int deg, float x, float y, float z, floa
   Y[15] = -0.5900435899266435f * x * (xx - 3.f * yy);
 }
 
-// O2.8 colour at a compile-time SH degree D >= 1: 128-bit loads of the
-// coefficient row (coefficient-major (q, ch), zero-padded to a multiple of 4);
-// each channel accumulates q = 0, 1, ... in order.
+// O2.8 colour at a compile-time SH degree D >= 1: 128-bit loads from the
+// scene's float4 coefficient planes ((q, ch) order, zero-padded to a multiple
+// of 4; plane q4 at sh4 + q4 n); each channel accumulates q = 0, 1, ... in order.
 template <int D>
-__device__ __forceinline__ void sh_colour(const float* __restrict__ row, float x, float y, float z, float col[3]) {
+__device__ __forceinline__ void sh_colour(const float4* __restrict__ f4, int n, float x, float y, float z,
+                                          float col[3]) {
   constexpr int KC = (D + 1) * (D + 1);
   constexpr int NF4 = (KC * 3 + 3) / 4;
   float Y[16];
   sh_eval(D, x, y, z, Y);
-  const float4* f4 = reinterpret_cast<const float4*>(row);
   float4 sh[NF4];
 #pragma unroll
-  for (int q4 = 0; q4 < NF4; ++q4) sh[q4] = __ldg(&f4[q4]);
+  for (int q4 = 0; q4 < NF4; ++q4) sh[q4] = __ldg(&f4[q4 * n]);
   float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
   for (int q4 = 0; q4 < NF4; ++q4) {
@@ -498,10 +511,10 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
       float dx = g.x - c.C[0], dy = g.y - c.C[1], dz = g.z - c.C[2];
       const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
       dx *= inv; dy *= inv; dz *= inv;
-      const float* row = scn.sh + (size_t)gi * scn.sh_stride;
-      if (cdeg == 3) sh_colour<3>(row, dx, dy, dz, col);
-      else if (cdeg == 2) sh_colour<2>(row, dx, dy, dz, col);
-      else sh_colour<1>(row, dx, dy, dz, col);
+      const float4* f4 = scn.sh4 + gi;
+      if (cdeg == 3) sh_colour<3>(f4, scn.n, dx, dy, dz, col);
+      else if (cdeg == 2) sh_colour<2>(f4, scn.n, dx, dy, dz, col);
+      else sh_colour<1>(f4, scn.n, dx, dy, dz, col);
     }
     // blend-side culling extents: alpha >= 1/255 needs q <= 2 ln(255 o); the
     // ellipse's half extents are sqrt(qmax Sigma2_xx), sqrt(qmax Sigma2_yy)

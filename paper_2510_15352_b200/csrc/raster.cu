@@ -234,10 +234,14 @@ __device__ __forceinline__ bool block_hit(const float4 a0, const float4 a1, floa
   return m + a0.z >= LOG2_CUTOFF - (0.01f + mag * 1.2e-5f);
 }
 
+// The next batch's records are prefetched into registers while the current
+// batch is walked (the record gathers' latency hides behind the blend).  The
+// stop test looks at T' alone: a non-passing pixel has w = 0 and T' = T >=
+// 1e-4, so only a passing pixel can stop; its weight is zeroed by a select.
 template <bool RGB>   // false: depth-only render (no colour accumulation)
 __global__ void __launch_bounds__(RW_THREADS, 8)
 raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
-               float* __restrict__ depth, float* __restrict__ alpha_out) {
+                      float* __restrict__ depth, float* __restrict__ alpha_out) {
   __shared__ float4 srec[RW_THREADS / 32][32 * 3];
   const int eloc = blockIdx.y;
   const int tile = blockIdx.x;
@@ -253,43 +257,43 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
   const float bx0 = (float)(tx * TILE + bx * 8) + 0.5f, by0 = (float)(ty * TILE + by * 8) + 0.5f;
 
   const uint2 rg = chunk_ok(ws.ok) ? ws.ranges[(size_t)eloc * rp.ntiles + tile] : make_uint2(0u, 0u);
-  const uint64_t rb = ws.rec_base[eloc];
+  const float4* __restrict__ R0 = ws.rec0 + ws.rec_base[eloc];
+  const float4* __restrict__ R1 = ws.rec1 + ws.rec_base[eloc];
+  const float4* __restrict__ R2 = ws.rec2 + ws.rec_base[eloc];
   const uint32_t* __restrict__ list = ws.sorted + ws.k_base[eloc];
 
   f2 T = pk(1.f, 1.f), Cr = pk(0.f, 0.f), Cg = Cr, Cb = Cr, Dn = Cr, Aw = Cr;
-  // per-pixel pass threshold: the cutoff while the pixel is live, +inf once
-  // it stopped (or lies outside the image) -- one compare per pixel
   const float INF = __int_as_float(0x7f800000);
   float cut0 = in0 ? LOG2_CUTOFF : INF, cut1 = in1 ? LOG2_CUTOFF : INF;
   const uint32_t lt = (1u << lane) - 1u;
 
-  uint32_t nidx = rg.x + lane < rg.y ? __ldg(&list[rg.x + lane]) : 0u;
+  // records of the current batch in registers, the next batch's indices
+  float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
+  if (rg.x + lane < rg.y) {
+    const uint32_t i0 = __ldg(&list[rg.x + lane]);
+    a0 = __ldg(&R0[i0]); a1 = __ldg(&R1[i0]); a2 = __ldg(&R2[i0]);
+  }
+  uint32_t nidx = rg.x + 32 + lane < rg.y ? __ldg(&list[rg.x + 32 + lane]) : 0u;
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
     if (__all_sync(0xffffffffu, cut0 == INF && cut1 == INF)) break;
     const bool valid = b + lane < rg.y;
-    const uint64_t r = rb + nidx;
-    nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
     bool mine = false;
-    float4 a0, a1, a2;
-    if (valid) {
-      a0 = __ldg(&ws.rec0[r]);
-      a1 = __ldg(&ws.rec1[r]);
-      a2 = __ldg(&ws.rec2[r]);
-      // o >= 1/255 (else no pixel can pass; this makes the log2 o clamp
-      // irrelevant to the pass decision), extents and exact block test
-      if (a1.w >= 0.f && a0.z >= LOG2_CUTOFF) {
-        const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
-        mine = xh >= bx0 && xl <= bx0 + 7.f && yh >= by0 && yl <= by0 + 7.f && block_hit(a0, a1, bx0, by0);
-      }
+    if (valid && a1.w >= 0.f && a0.z >= LOG2_CUTOFF) {
+      const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
+      mine = xh >= bx0 && xl <= bx0 + 7.f && yh >= by0 && yl <= by0 + 7.f && block_hit(a0, a1, bx0, by0);
     }
     const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (mine) {
       const int pos = __popc(m & lt);
       srec[warp][3 * pos] = a0;
-      // the extent slot now carries the alpha exponent bound min(log2 o, log2 0.99)
       srec[warp][3 * pos + 1] = make_float4(a1.x, a1.y, a1.z, fminf(a0.z, LOG2_099));
       srec[warp][3 * pos + 2] = a2;
     }
+    // prefetch: the next batch's records, the batch after's indices
+    if (b + 32 + lane < rg.y) {
+      a0 = __ldg(&R0[nidx]); a1 = __ldg(&R1[nidx]); a2 = __ldg(&R2[nidx]);
+    }
+    nidx = b + 64 + lane < rg.y ? __ldg(&list[b + 64 + lane]) : 0u;
     __syncwarp();
     const uint32_t cnt = __popc(m);
     for (uint32_t i = 0; i < cnt; ++i) {
@@ -299,18 +303,15 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
       const f2 sv = fma2(mul2(pk(r1.z, r1.z), dy), dy, pk(r0.z, r0.z));
       float x0, x1;
       upk(fma2(dx, t, sv), x0, x1);
-      const bool p0 = x0 >= cut0, p1 = x1 >= cut1;
-      // Branch-free blend: a pixel that does not pass gets alpha = 0, so
-      // w = 0 and C + 0 c, T - 0 are exact no-ops (bit-identical to skipping).
-      // alpha = min(0.99, 2^min(x, log2 o)) = 2^min(x, log2 o, log2 0.99)
-      const float al0 = p0 ? ex2_approx(fminf(x0, r1.w)) : 0.f;
-      const float al1 = p1 ? ex2_approx(fminf(x1, r1.w)) : 0.f;
+      const float al0 = x0 >= cut0 ? ex2_approx(fminf(x0, r1.w)) : 0.f;
+      const float al1 = x1 >= cut1 ? ex2_approx(fminf(x1, r1.w)) : 0.f;
       f2 W = mul2(pk(al0, al1), T);
-      float tn0, tn1;
+      float tn0, tn1, w0, w1;
       upk(sub2(T, W), tn0, tn1);
-      // a stopping pixel is not blended and keeps T: w *= 0 (exact; w *= 1 otherwise)
-      const bool s0 = p0 && tn0 < 1e-4f, s1 = p1 && tn1 < 1e-4f;
-      W = mul2(W, pk(s0 ? 0.f : 1.f, s1 ? 0.f : 1.f));
+      upk(W, w0, w1);
+      // T stays >= 1e-4, so only a passing pixel can stop; it is not blended
+      const bool s0 = tn0 < 1e-4f, s1 = tn1 < 1e-4f;
+      W = pk(s0 ? 0.f : w0, s1 ? 0.f : w1);
       cut0 = s0 ? INF : cut0;
       cut1 = s1 ? INF : cut1;
       if (RGB) {
@@ -321,7 +322,7 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
       }
       Dn = fma2(W, pk(r0.w, r0.w), Dn);
       Aw = add2(Aw, W);
-      T = sub2(T, W);   // = T - w, or T unchanged for a stopping pixel (w = 0)
+      T = sub2(T, W);
     }
     __syncwarp();
   }

@@ -82,8 +82,10 @@ __global__ void pack_kernel(int64_t n, int K, int sh_stride, const float* __rest
     // reading R35: q_max = f32(2 ln(255 o)) from an f64 log (once per Gaussian)
     qmax[i] = (float)__dmul_rn(2.0, log(__dmul_rn(255.0, (double)opac[i])));
     if (sh_out) {
+      // float4 planes: plane q4 holds coefficients 4 q4 .. 4 q4 + 3 of every
+      // Gaussian (a warp reading neighbouring Gaussians reads one line per plane)
       for (int k = 0; k < sh_stride; ++k)
-        sh_out[i * sh_stride + k] = k < K * 3 ? sh[i * K * 3 + k] : 0.f;
+        sh_out[((size_t)(k >> 2) * n + i) * 4 + (k & 3)] = k < K * 3 ? sh[i * K * 3 + k] : 0.f;
     }
   }
 }
