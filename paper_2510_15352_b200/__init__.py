@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgg.so")
+LIB_PATH = os.environ.get("GG_LIB") or os.path.join(_HERE, "libgg.so")   # GG_LIB: an alternative in-tree build (A/B runs)
 
 GG_OK, GG_E_INVALID, GG_E_NONFINITE, GG_E_OOM, GG_E_CUDA, GG_E_BAD_SCENE, GG_E_CAPACITY, GG_E_UNSUPPORTED = range(8)
 GG_KEEP_INTERMEDIATES = 1

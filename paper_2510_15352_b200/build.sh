@@ -4,9 +4,10 @@ set -e
 HERE="$(cd "$(dirname "$0")" && pwd)"
 ROOT="$(dirname "$HERE")"
 NVCC="${NVCC:-nvcc}"
-OUT="$HERE/build"
+OUT="${BUILD_DIR:-$HERE/build}"
+LIB="${LIB:-$HERE/libgg.so}"
 mkdir -p "$OUT"
-FLAGS="-O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -I$ROOT/include -Xptxas -v"
+FLAGS="$EXTRA -O3 -lineinfo -std=c++17 -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -I$ROOT/include -Xptxas -v"
 pids=""
 for f in "$HERE"/csrc/*.cu; do
   b=$(basename "$f" .cu)
@@ -16,5 +17,5 @@ done
 fail=0
 for p in $pids; do wait $p || fail=1; done
 [ $fail -eq 0 ] || exit 1
-$NVCC -shared -gencode arch=compute_100a,code=sm_100a -o "$HERE/libgg.so" "$OUT"/*.o
-echo "built $HERE/libgg.so"
+$NVCC -shared -gencode arch=compute_100a,code=sm_100a -o "$LIB" "$OUT"/*.o
+echo "built $LIB"
