@@ -613,8 +613,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
         !ensure(ctx, ctx->zkey, V * 4, s) || (keep && !ensure(ctx, ctx->gid, V * 4, s)) ||
         (rp.ellipse && !ensure(ctx, ctx->rmask, V * 4 + 4, s)) ||
         (keep && !ensure(ctx, ctx->dconic, V * 16, s)) ||
-        !ensure(ctx, ctx->dk0, V * 4, s) || !ensure(ctx, ctx->dv0, V * 4, s) ||
-        !ensure(ctx, ctx->dk1, V * 4, s) || !ensure(ctx, ctx->dv1, V * 4, s))
+        !ensure(ctx, ctx->dk0, V * 8, s) || !ensure(ctx, ctx->dk1, V * 8, s) ||
+        !ensure(ctx, ctx->dv0, V * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: record workspace (%llu records) allocation failed",
                   (unsigned long long)V);
     ctx->launches += launch_copy_words(ctx->rbase.p, ctx->h_rbase, ec * 8, s);
@@ -624,8 +624,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ws.rmask = rp.ellipse ? P<uint32_t>(ctx->rmask) : nullptr;
     ws.gid = keep ? P<uint32_t>(ctx->gid) : nullptr;
     ws.dconic = keep ? P<float4>(ctx->dconic) : nullptr;
-    ws.dk0 = P<uint32_t>(ctx->dk0); ws.dv0 = P<uint32_t>(ctx->dv0);
-    ws.dk1 = P<uint32_t>(ctx->dk1); ws.dv1 = P<uint32_t>(ctx->dv1);
+    ws.dp0 = P<uint64_t>(ctx->dk0); ws.dp1 = P<uint64_t>(ctx->dk1); ws.order = P<uint32_t>(ctx->dv0);
     // K1b
     launch_project(e0, ngroups, nblk, max_deg, groups, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp,
                    ws, s);
@@ -825,8 +824,7 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
     ws.rmask = rp.ellipse ? P<uint32_t>(ctx->rmask) : nullptr;
     ws.zmin = P<uint32_t>(ctx->zmm); ws.zmax = P<uint32_t>(ctx->zmm) + chunk;
-    ws.dk0 = P<uint32_t>(ctx->dk0); ws.dv0 = P<uint32_t>(ctx->dv0);
-    ws.dk1 = P<uint32_t>(ctx->dk1); ws.dv1 = P<uint32_t>(ctx->dv1);
+    ws.dp0 = P<uint64_t>(ctx->dk0); ws.dp1 = P<uint64_t>(ctx->dk1); ws.order = P<uint32_t>(ctx->dv0);
     ws.sorted = P<uint32_t>(ctx->sorted);
     ws.ranges = P<uint2>(ctx->ranges);
     ws.ok = ok;
@@ -892,8 +890,8 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
              ensure(ctx, ctx->rec1, vcap * 16, s) && ensure(ctx, ctx->rec2, vcap * 16, s) &&
              ensure(ctx, ctx->rect, vcap * 8, s) && ensure(ctx, ctx->zkey, vcap * 4, s) &&
              ensure(ctx, ctx->rmask, vcap * 4 + 4, s) &&
-             ensure(ctx, ctx->dk0, vcap * 4, s) && ensure(ctx, ctx->dv0, vcap * 4, s) &&
-             ensure(ctx, ctx->dk1, vcap * 4, s) && ensure(ctx, ctx->dv1, vcap * 4, s) &&
+             ensure(ctx, ctx->dk0, vcap * 8, s) && ensure(ctx, ctx->dk1, vcap * 8, s) &&
+             ensure(ctx, ctx->dv0, vcap * 4, s) &&
              ensure(ctx, ctx->sorted, kcap * 4, s) && ensure(ctx, ctx->blkbase, (size_t)(ch + 1) * 4, s) &&
              ensure(ctx, ctx->blkenv, nbcap * 4 + 4, s) && ensure(ctx, ctx->qctr, 64 * 4, s) &&
              ensure(ctx, ctx->ghist, nbcap * sort_ghist_words() * 4, s) &&

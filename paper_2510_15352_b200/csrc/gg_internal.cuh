@@ -91,8 +91,10 @@ struct ChunkWS {
   uint32_t* zmin;       // [Ec] min / max depth bits per env (depth-sort key offset)
   uint32_t* zmax;
   uint32_t* gid;        // Gaussian index (debug dumps only; may be null)
-  // depth-sort scratch [V]
-  uint32_t* dk0; uint32_t* dv0; uint32_t* dk1; uint32_t* dv1;
+  // depth-sort scratch [V]: packed (key - zmin) << 32 | record ping-pong, and
+  // the last pass's output (records in depth order)
+  uint64_t* dp0; uint64_t* dp1;
+  uint32_t* order;
   uint32_t* sorted;     // [K] final record-local indices, tile-major
   uint2* ranges;        // [Ec][ntiles] [start,end) relative to k_base[e]
   const uint32_t* ok;   // chunk validity (async mode: 0 after a capacity overflow); null = always valid

@@ -119,15 +119,22 @@ __device__ __forceinline__ void unpack_rect(uint2 r, uint32_t& x0, uint32_t& x1,
 // Input / output arrays of depth pass p (all indexed rec_base[e] + j).  The
 // sort key is the f32 depth bits minus the env's minimum (a monotone map of
 // the positive f32 bits), so a typical ~27-bit span needs 3 passes of 10 bits.
+// Between passes key and record travel as one 64-bit word (key << 32 |
+// record): one load, one staging store and one scattered store per element.
 struct DepthIO {
-  const uint32_t* kin;   // keys in (f32 depth bits)
-  const uint32_t* vin;   // values in (null = identity j)
-  uint32_t* kout;        // keys out (null on the last pass)
-  uint32_t* vout;
+  const uint32_t* zin;   // first pass: f32 depth bits (records = identity j)
+  const uint64_t* pin;   // later passes: packed (key - zmin) << 32 | record
+  uint64_t* pout;        // packed out (null on the last pass)
+  uint32_t* vout;        // last pass: records in depth order
 };
 
-__device__ __forceinline__ uint32_t depth_digit(uint32_t z, uint32_t zmin, int shift) {
-  return ((z - zmin) >> shift) & (DS_RADIX - 1);
+__device__ __forceinline__ uint32_t depth_digit(uint32_t key, int shift) {
+  return (key >> shift) & (DS_RADIX - 1);
+}
+
+// element i of the block as (key - zmin) << 32 | record
+__device__ __forceinline__ uint64_t depth_elem(const DepthIO& io, uint64_t at, uint32_t j, uint32_t zmin) {
+  return io.zin ? ((uint64_t)(io.zin[at] - zmin) << 32) | j : io.pin[at];
 }
 
 // ---- depth passes --------------------------------------------------------
@@ -143,11 +150,11 @@ __device__ __forceinline__ void depth_upsweep_block(uint32_t b, const BlockTable
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t i = threadIdx.x + j * DS_THREADS;
-    k[j] = i < n ? io.kin[rb + j0 + i] : 0u;
+    k[j] = i < n ? (io.zin ? io.zin[rb + j0 + i] - zmin : (uint32_t)(io.pin[rb + j0 + i] >> 32)) : 0u;
   }
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j)
-    if (threadIdx.x + j * DS_THREADS < n) atomicAdd(&h[depth_digit(k[j], zmin, shift)], 1u);
+    if (threadIdx.x + j * DS_THREADS < n) atomicAdd(&h[depth_digit(k[j], shift)], 1u);
   __syncthreads();
   for (int i = threadIdx.x; i < DS_RADIX; i += DS_THREADS) ghist[(size_t)b * DS_RADIX + i] = h[i];
 }
@@ -208,8 +215,7 @@ struct DownSmem {
       uint8_t st[DS_WARPS][DS_RADIX];          // last lane that stamped each digit (warp-private)
     } r;
     struct {                                   // staging in digit order (after ranking)
-      uint32_t sk[SORT_BLK];
-      uint32_t sv[SORT_BLK];
+      uint64_t sp[SORT_BLK];
     } o;
   } u;
   uint32_t dstart[DS_RADIX];
@@ -223,8 +229,8 @@ struct DownSmem {
 // lane to stamp it is the digits' representative) and one shared-memory OR
 // into the representative's peer mask.  u.r is zero on entry; on exit it is
 // free (the caller stages into u.o).
-__device__ __forceinline__ void block_rank(const uint32_t (&d)[DS_IPT], uint32_t n, uint32_t (&lpos)[DS_IPT],
-                                           DownSmem& sm) {
+__device__ __forceinline__ void block_rank(const uint64_t (&x)[DS_IPT], int shift, uint32_t n,
+                                           uint32_t (&lpos)[DS_IPT], DownSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt = lanemask_lt();
   uint32_t* wc = sm.u.r.wcnt[warp];
@@ -235,7 +241,7 @@ __device__ __forceinline__ void block_rank(const uint32_t (&d)[DS_IPT], uint32_t
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t e = warp * 32 * DS_IPT + j * 32 + lane;
     const bool ok = e < n;
-    const uint32_t dd = d[j];
+    const uint32_t dd = depth_digit((uint32_t)(x[j] >> 32), shift);
     if (ok) st[dd] = (uint8_t)lane;
     __syncwarp();
     const uint32_t rep = ok ? st[dd] : 0u;
@@ -269,7 +275,7 @@ __device__ __forceinline__ void block_rank(const uint32_t (&d)[DS_IPT], uint32_t
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t e = warp * 32 * DS_IPT + j * 32 + lane;
-    const uint32_t dd = d[j];
+    const uint32_t dd = depth_digit((uint32_t)(x[j] >> 32), shift);
     lpos[j] = e < n ? sm.dstart[dd] + ((wc[dd >> 1] >> (16 * (dd & 1))) & 0xffffu) + rk[j] : 0u;
   }
   __syncthreads();
@@ -284,19 +290,17 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < DS_WARPS * DS_RADIX / 2; i += DS_THREADS) (&sm.u.r.wcnt[0][0])[i] = 0u;
   for (int i = tid; i < DS_WARPS * 32; i += DS_THREADS) (&sm.u.r.pm[0][0])[i] = 0u;
-  uint32_t k[DS_IPT], v[DS_IPT], d[DS_IPT], lp[DS_IPT];
+  uint64_t x[DS_IPT];
+  uint32_t lp[DS_IPT];
   // this block's output offset of its digits 2 tid, 2 tid + 1 (loaded early)
   const uint2 off = reinterpret_cast<const uint2*>(ghist + (size_t)b * DS_RADIX)[tid];
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t i = warp * 32 * DS_IPT + j * 32 + lane;
-    const bool ok = i < n;
-    k[j] = ok ? io.kin[rb + j0 + i] : 0u;
-    v[j] = ok ? (io.vin ? io.vin[rb + j0 + i] : j0 + i) : 0u;
-    d[j] = depth_digit(k[j], zmin, shift);
+    x[j] = i < n ? depth_elem(io, rb + j0 + i, j0 + i, zmin) : 0ull;
   }
   __syncthreads();
-  block_rank(d, n, lp, sm);
+  block_rank(x, shift, n, lp, sm);
   // fold: dstart[d] <- (global offset of digit d) - (its start in the block),
   // so staged element q of digit d goes to rb + dstart[d] + q
   sm.dstart[2 * tid] = off.x - sm.dstart[2 * tid];
@@ -304,21 +308,29 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
 #pragma unroll
   for (int j = 0; j < DS_IPT; ++j) {
     const uint32_t i = warp * 32 * DS_IPT + j * 32 + lane;
-    if (i < n) { sm.u.o.sk[lp[j]] = k[j]; sm.u.o.sv[lp[j]] = v[j]; }
+    if (i < n) sm.u.o.sp[lp[j]] = x[j];
   }
   __syncthreads();
-  uint32_t* kout = io.kout ? io.kout + rb : nullptr;
-  uint32_t* vout = io.vout + rb;
-  for (uint32_t q = tid; q < n; q += DS_THREADS) {
-    const uint32_t kk = sm.u.o.sk[q];
-    const uint32_t pos = sm.dstart[depth_digit(kk, zmin, shift)] + q;
-    if (kout) kout[pos] = kk;
-    vout[pos] = sm.u.o.sv[q];
+  if (io.pout) {
+    uint64_t* pout = io.pout + rb;
+    for (uint32_t q = tid; q < n; q += DS_THREADS) {
+      const uint64_t xx = sm.u.o.sp[q];
+      pout[sm.dstart[depth_digit((uint32_t)(xx >> 32), shift)] + q] = xx;
+    }
+  } else {
+    uint32_t* vout = io.vout + rb;
+    for (uint32_t q = tid; q < n; q += DS_THREADS) {
+      const uint64_t xx = sm.u.o.sp[q];
+      vout[sm.dstart[depth_digit((uint32_t)(xx >> 32), shift)] + q] = (uint32_t)xx;
+    }
   }
 }
 
 template <bool LOOP>
-__global__ void __launch_bounds__(DS_THREADS, 4)
+#ifndef GG_DS_MINB
+#define GG_DS_MINB 3   // 40 registers: the packed elements stay (mostly) in registers
+#endif
+__global__ void __launch_bounds__(DS_THREADS, GG_DS_MINB)
 depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const uint32_t* ghist) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   DownSmem& sm = *reinterpret_cast<DownSmem*>(smem_raw);
@@ -670,10 +682,10 @@ static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, con
   if (LOOP) cudaMemsetAsync(qctr, 0, SORT_QCTR * sizeof(uint32_t), s);
   for (int p = 0; p < passes; ++p) {
     DepthIO io;
-    io.kin = p == 0 ? ws.zkey : ((p & 1) ? ws.dk0 : ws.dk1);
-    io.vin = p == 0 ? nullptr : ((p & 1) ? ws.dv0 : ws.dv1);
-    io.kout = p == passes - 1 ? nullptr : ((p & 1) ? ws.dk1 : ws.dk0);
-    io.vout = (p & 1) ? ws.dv1 : ws.dv0;
+    io.zin = p == 0 ? ws.zkey : nullptr;
+    io.pin = p == 0 ? nullptr : ((p & 1) ? ws.dp0 : ws.dp1);
+    io.pout = p == passes - 1 ? nullptr : ((p & 1) ? ws.dp1 : ws.dp0);
+    io.vout = ws.order;
     if (LOOP) bt.q = qctr + qi++;
     depth_upsweep_kernel<LOOP><<<g1, DS_THREADS, 0, s>>>(bt, ws, io, DS_BITS * p, ghist);
     depth_scan_kernel<<<ec, DS_RADIX, 0, s>>>(bt, ghist, ws.ok);
@@ -681,7 +693,7 @@ static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, con
     depth_downsweep_kernel<LOOP><<<g1, DS_THREADS, depth_down_smem(), s>>>(bt, ws, io, DS_BITS * p, ghist);
     launches += 3;
   }
-  const uint32_t* order = ((passes - 1) & 1) ? ws.dv1 : ws.dv0;   // values of the last depth pass
+  const uint32_t* order = ws.order;   // records of the last depth pass
   if (LOOP) bt.q = qctr + qi++;
   const bool mask = ws.rmask != nullptr;
   if (mask)
