@@ -222,10 +222,10 @@ __device__ __forceinline__ float edge_max(float a, float b, float c, float e, fl
   return fmaf(fmaf(c, t, b * e), t, a * e * e);
 }
 
-__device__ __forceinline__ bool block_hit(const float4 a0, const float4 a1, float x0, float y0) {
+__device__ __forceinline__ bool block_hit(const float4 a0, const float4 a1, float x0, float y0, float x1, float y1) {
   const float A = a1.x, B = a1.y, Cc = a1.z;
   if (!(A < 0.f && Cc < 0.f)) return true;
-  const float dxl = a0.x - (x0 + 7.f), dxh = a0.x - x0, dyl = a0.y - (y0 + 7.f), dyh = a0.y - y0;
+  const float dxl = a0.x - x1, dxh = a0.x - x0, dyl = a0.y - y1, dyh = a0.y - y0;
   if (dxl <= 0.f && dxh >= 0.f && dyl <= 0.f && dyh >= 0.f) return true;
   float m = fmaxf(edge_max(A, B, Cc, dxl, dyl, dyh), edge_max(A, B, Cc, dxh, dyl, dyh));
   m = fmaxf(m, fmaxf(edge_max(Cc, B, A, dyl, dxl, dxh), edge_max(Cc, B, A, dyh, dxl, dxh)));
@@ -277,10 +277,11 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
     if (__all_sync(0xffffffffu, cut0 == INF && cut1 == INF)) break;
     const bool valid = b + lane < rg.y;
+    const float lx0 = bx0, lx1 = bx0 + 7.f, ly0 = by0, ly1 = by0 + 7.f;
     bool mine = false;
     if (valid && a1.w >= 0.f && a0.z >= LOG2_CUTOFF) {
       const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
-      mine = xh >= bx0 && xl <= bx0 + 7.f && yh >= by0 && yl <= by0 + 7.f && block_hit(a0, a1, bx0, by0);
+      mine = xh >= lx0 && xl <= lx1 && yh >= ly0 && yl <= ly1 && block_hit(a0, a1, lx0, ly0, lx1, ly1);
     }
     const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (mine) {
@@ -303,6 +304,8 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
       const f2 sv = fma2(mul2(pk(r1.z, r1.z), dy), dy, pk(r0.z, r0.z));
       float x0, x1;
       upk(fma2(dx, t, sv), x0, x1);
+      // no pixel of the warp passes: nothing to blend, nothing stops (exact)
+      if (!__any_sync(0xffffffffu, x0 >= cut0 || x1 >= cut1)) continue;
       const float al0 = x0 >= cut0 ? ex2_approx(fminf(x0, r1.w)) : 0.f;
       const float al1 = x1 >= cut1 ? ex2_approx(fminf(x1, r1.w)) : 0.f;
       f2 W = mul2(pk(al0, al1), T);
