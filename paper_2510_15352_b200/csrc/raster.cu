@@ -44,31 +44,67 @@ __device__ __forceinline__ float ex2_approx(float x) {
 constexpr float LOG2_CUTOFF = -7.99435343685885793f;   // log2(1/255)
 constexpr float LOG2_099 = -0.014499569695115089f;      // log2(0.99): the alpha cap as an exponent bound
 
-// One pixel-Gaussian step (R12-R15 with the R30 log2-domain cutoff).
-__device__ __forceinline__ void blend_step(const float4 a0, const float4 a1, const float4 a2, float fpx, float fpy,
-                                           float& T, float& Cr, float& Cg, float& Cb, float& Dn, float& Aw,
+// The exponent x(d) = A'dx^2 + B'dxdy + C'dy^2 + log2 o (d = mean - pixel
+// centre) expanded around the tile's first pixel centre (tox, toy): with
+// D = mean - (tox, toy) and the pixel's offset (lx, ly) in the tile,
+//   x = c0 + lx (c1 + A' lx) + ly (c2 + B' lx + C' ly),
+//   c0 = x(D), c1 = -(2A'Dx + B'Dy), c2 = -(B'Dx + 2C'Dy).
+// Both raster kernels evaluate exactly this sequence (bit-identical images).
+// Returns (c0, c1, c2, w) with w = min(log2 o, log2 0.99): alpha = 2^min(x, w)
+// is min(0.99, o e^(-q/2)) with q >= 0 enforced (R10, R13).
+__device__ __forceinline__ float4 tile_coefs(const float4 a0, const float4 a1, float tox, float toy) {
+  const float Dx = a0.x - tox, Dy = a0.y - toy;
+  const float c0 = fmaf(Dx, fmaf(a1.x, Dx, a1.y * Dy), fmaf(a1.z * Dy, Dy, a0.z));
+  const float c1 = -fmaf(2.f * a1.x, Dx, a1.y * Dy);
+  const float c2 = -fmaf(2.f * a1.z, Dy, a1.y * Dx);
+  return make_float4(c0, c1, c2, fminf(a0.z, LOG2_099));
+}
+
+// One pixel-Gaussian step (R12-R15 with the R30 log2-domain cutoff).  s0 =
+// (c0, c1, c2, w), s1 = (A', B', C', z), s2 = (r, g, b, -).  Alpha is not
+// accumulated: A = 1 - T at the end (R15).
+__device__ __forceinline__ void blend_step(const float4 s0, const float4 s1, const float4 s2, float lx, float ly,
+                                           float& T, float& Cr, float& Cg, float& Cb, float& Dn,
                                            bool& done, uint32_t& nc) {
-  const float dx = a0.x - fpx, dy = a0.y - fpy;
-  // x = log2(o) - q log2(e)/2; q >= 0 enforced as x <= log2(o)
-  float x = fmaf(dx, fmaf(a1.x, dx, a1.y * dy), fmaf(a1.z * dy, dy, a0.z));
-  x = fminf(x, a0.z);
+  const float P = fmaf(lx, fmaf(s1.x, lx, s0.y), s0.x);
+  const float Q = fmaf(s1.y, lx, s0.z);
+  const float x = fminf(fmaf(ly, fmaf(s1.z, ly, Q), P), s0.w);
   if (x >= LOG2_CUTOFF) {
-    // alpha = min(0.99, 2^x) taken as 2^min(x, log2 0.99) (exp2 is monotone)
-    const float al = ex2_approx(fminf(x, LOG2_099));
+    const float al = ex2_approx(x);
     const float w = al * T;
     const float Tn = T - w;
     if (Tn < 1e-4f) {
       done = true;
     } else {
-      Cr = fmaf(w, a2.x, Cr);
-      Cg = fmaf(w, a2.y, Cg);
-      Cb = fmaf(w, a2.z, Cb);
-      Dn = fmaf(w, a0.w, Dn);
-      Aw += w;
+      Cr = fmaf(w, s2.x, Cr);
+      Cg = fmaf(w, s2.y, Cg);
+      Cb = fmaf(w, s2.z, Cb);
+      Dn = fmaf(w, s1.w, Dn);
       T = Tn;
       ++nc;
     }
   }
+}
+
+// Outputs of one pixel (O5): rgb = C + T bg; A = 1 - T (= sum of the weights,
+// R15); depth = Dn / A, 0 where nothing was blended (T = 1 exactly).
+__device__ __forceinline__ void write_pixel(const RenderParams& rp, void* rgb, float* depth, float* alpha_out,
+                                            size_t p, float T, float Cr, float Cg, float Cb, float Dn) {
+  const float r = fmaf(T, rp.bg[0], Cr), g = fmaf(T, rp.bg[1], Cg), bl = fmaf(T, rp.bg[2], Cb);
+  if (rgb) {
+    if (rp.rgb_format == 0) {
+      uint8_t* o = reinterpret_cast<uint8_t*>(rgb) + p * 3;
+      o[0] = (uint8_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 255.f);
+      o[1] = (uint8_t)__float2uint_rn(fminf(fmaxf(g, 0.f), 1.f) * 255.f);
+      o[2] = (uint8_t)__float2uint_rn(fminf(fmaxf(bl, 0.f), 1.f) * 255.f);
+    } else {
+      float* o = reinterpret_cast<float*>(rgb) + p * 3;
+      o[0] = r; o[1] = g; o[2] = bl;
+    }
+  }
+  const float A = 1.f - T;
+  if (depth) depth[p] = A > 0.f ? Dn / A : 0.f;
+  if (alpha_out) alpha_out[p] = A;
 }
 
 template <bool COUNTERS>
@@ -87,7 +123,7 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
   const int px = tx * TILE + bx * 8 + (lane & 7);
   const int py = ty * TILE + by * 4 + (lane >> 3);
   const bool inside = px < rp.W && py < rp.H;
-  const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
+  const float lx = (float)(px - tx * TILE), ly = (float)(py - ty * TILE);   // offset in the tile
   // pixel-centre extents of the tile's warp blocks (columns: 2 x 8 px, rows: 4 x 4 px)
   const float tx0 = (float)(tx * TILE) + 0.5f, ty0 = (float)(ty * TILE) + 0.5f;
 
@@ -96,7 +132,7 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
   const uint64_t rb = ws.rec_base[eloc];
   const uint32_t* __restrict__ list = ws.sorted + kb;
 
-  float T = 1.f, Cr = 0.f, Cg = 0.f, Cb = 0.f, Dn = 0.f, Aw = 0.f;
+  float T = 1.f, Cr = 0.f, Cg = 0.f, Cb = 0.f, Dn = 0.f;
   bool done = !inside;
   uint32_t ne = 0, nc = 0;
 
@@ -108,8 +144,8 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
       const float4 a0 = __ldg(&ws.rec0[r]);
       const float4 a1 = __ldg(&ws.rec1[r]);
       const float4 a2 = __ldg(&ws.rec2[r]);
-      srec[3 * tid] = a0;
-      srec[3 * tid + 1] = a1;
+      srec[3 * tid] = tile_coefs(a0, a1, tx0, ty0);
+      srec[3 * tid + 1] = make_float4(a1.x, a1.y, a1.z, a0.w);
       srec[3 * tid + 2] = a2;
       uint32_t m = 0;
       if (a1.w >= 0.f) {
@@ -134,7 +170,7 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
         for (uint32_t j = 0; j < n; ++j) {
           if (!done) ++ne;
           if (!((smask[j] >> warp) & 1u)) continue;
-          if (!done) blend_step(srec[3 * j], srec[3 * j + 1], srec[3 * j + 2], fpx, fpy, T, Cr, Cg, Cb, Dn, Aw, done, nc);
+          if (!done) blend_step(srec[3 * j], srec[3 * j + 1], srec[3 * j + 2], lx, ly, T, Cr, Cg, Cb, Dn, done, nc);
           if ((j & 7) == 7 && __all_sync(0xffffffffu, done)) break;
         }
       }
@@ -152,30 +188,14 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
       __syncwarp();
       for (uint32_t i = 0; i < cnt; ++i) {
         const uint32_t j = wlist[warp][i];
-        if (!done) blend_step(srec[3 * j], srec[3 * j + 1], srec[3 * j + 2], fpx, fpy, T, Cr, Cg, Cb, Dn, Aw, done, nc);
+        if (!done) blend_step(srec[3 * j], srec[3 * j + 1], srec[3 * j + 2], lx, ly, T, Cr, Cg, Cb, Dn, done, nc);
         if ((i & 15) == 15 && __all_sync(0xffffffffu, done)) break;
       }
     }
     if (__syncthreads_count(done) == TILE_PX) break;
   }
 
-  if (inside) {
-    const size_t p = ((size_t)e * rp.H + py) * rp.W + px;
-    const float r = fmaf(T, rp.bg[0], Cr), g = fmaf(T, rp.bg[1], Cg), bl = fmaf(T, rp.bg[2], Cb);
-    if (rgb) {
-      if (rp.rgb_format == 0) {
-        uint8_t* o = reinterpret_cast<uint8_t*>(rgb) + p * 3;
-        o[0] = (uint8_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 255.f);
-        o[1] = (uint8_t)__float2uint_rn(fminf(fmaxf(g, 0.f), 1.f) * 255.f);
-        o[2] = (uint8_t)__float2uint_rn(fminf(fmaxf(bl, 0.f), 1.f) * 255.f);
-      } else {
-        float* o = reinterpret_cast<float*>(rgb) + p * 3;
-        o[0] = r; o[1] = g; o[2] = bl;
-      }
-    }
-    if (depth) depth[p] = Aw > 0.f ? Dn / Aw : 0.f;
-    if (alpha_out) alpha_out[p] = Aw;
-  }
+  if (inside) write_pixel(rp, rgb, depth, alpha_out, ((size_t)e * rp.H + py) * rp.W + px, T, Cr, Cg, Cb, Dn);
   if (COUNTERS) {
     if (co.dbg_neval && eloc == co.dbg_eloc && inside) co.dbg_neval[py * rp.W + px] = (int32_t)ne;
     unsigned long long a = ne, c = nc;
@@ -252,8 +272,10 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
   const int px = tx * TILE + bx * 8 + (lane & 7);
   const int py0 = ty * TILE + by * 8 + (lane >> 3), py1 = py0 + 4;
   const bool in0 = px < rp.W && py0 < rp.H, in1 = px < rp.W && py1 < rp.H;
-  const float fpx = (float)px + 0.5f;
-  const f2 FPX = pk(fpx, fpx), FPY = pk((float)py0 + 0.5f, (float)py1 + 0.5f);
+  // the lane's pixel offsets in the tile: (lx, ly) and (lx, ly + 4)
+  const float lx = (float)(px - tx * TILE);
+  const f2 LY = pk((float)(py0 - ty * TILE), (float)(py1 - ty * TILE));
+  const float tox = (float)(tx * TILE) + 0.5f, toy = (float)(ty * TILE) + 0.5f;
   const float bx0 = (float)(tx * TILE + bx * 8) + 0.5f, by0 = (float)(ty * TILE + by * 8) + 0.5f;
 
   const uint2 rg = chunk_ok(ws.ok) ? ws.ranges[(size_t)eloc * rp.ntiles + tile] : make_uint2(0u, 0u);
@@ -262,7 +284,7 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
   const float4* __restrict__ R2 = ws.rec2 + ws.rec_base[eloc];
   const uint32_t* __restrict__ list = ws.sorted + ws.k_base[eloc];
 
-  f2 T = pk(1.f, 1.f), Cr = pk(0.f, 0.f), Cg = Cr, Cb = Cr, Dn = Cr, Aw = Cr;
+  f2 T = pk(1.f, 1.f), Cr = pk(0.f, 0.f), Cg = Cr, Cb = Cr, Dn = Cr;
   const float INF = __int_as_float(0x7f800000);
   float cut0 = in0 ? LOG2_CUTOFF : INF, cut1 = in1 ? LOG2_CUTOFF : INF;
   const uint32_t lt = (1u << lane) - 1u;
@@ -286,8 +308,8 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
     const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (mine) {
       const int pos = __popc(m & lt);
-      srec[warp][3 * pos] = a0;
-      srec[warp][3 * pos + 1] = make_float4(a1.x, a1.y, a1.z, fminf(a0.z, LOG2_099));
+      srec[warp][3 * pos] = tile_coefs(a0, a1, tox, toy);
+      srec[warp][3 * pos + 1] = make_float4(a1.x, a1.y, a1.z, a0.w);
       srec[warp][3 * pos + 2] = a2;
     }
     // prefetch: the next batch's records, the batch after's indices
@@ -299,15 +321,15 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
     const uint32_t cnt = __popc(m);
     for (uint32_t i = 0; i < cnt; ++i) {
       const float4 r0 = srec[warp][3 * i], r1 = srec[warp][3 * i + 1];
-      const f2 dx = sub2(pk(r0.x, r0.x), FPX), dy = sub2(pk(r0.y, r0.y), FPY);
-      const f2 t = fma2(pk(r1.x, r1.x), dx, mul2(pk(r1.y, r1.y), dy));
-      const f2 sv = fma2(mul2(pk(r1.z, r1.z), dy), dy, pk(r0.z, r0.z));
+      // x = c0 + lx (c1 + A' lx) + ly (c2 + B' lx + C' ly)  (tile_coefs)
+      const float P = fmaf(lx, fmaf(r1.x, lx, r0.y), r0.x);
+      const float Q = fmaf(r1.y, lx, r0.z);
       float x0, x1;
-      upk(fma2(dx, t, sv), x0, x1);
+      upk(fma2(LY, fma2(pk(r1.z, r1.z), LY, pk(Q, Q)), pk(P, P)), x0, x1);
       // no pixel of the warp passes: nothing to blend, nothing stops (exact)
       if (!__any_sync(0xffffffffu, x0 >= cut0 || x1 >= cut1)) continue;
-      const float al0 = x0 >= cut0 ? ex2_approx(fminf(x0, r1.w)) : 0.f;
-      const float al1 = x1 >= cut1 ? ex2_approx(fminf(x1, r1.w)) : 0.f;
+      const float al0 = x0 >= cut0 ? ex2_approx(fminf(x0, r0.w)) : 0.f;
+      const float al1 = x1 >= cut1 ? ex2_approx(fminf(x1, r0.w)) : 0.f;
       f2 W = mul2(pk(al0, al1), T);
       float tn0, tn1, w0, w1;
       upk(sub2(T, W), tn0, tn1);
@@ -323,36 +345,18 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
         Cg = fma2(W, pk(r2.y, r2.y), Cg);
         Cb = fma2(W, pk(r2.z, r2.z), Cb);
       }
-      Dn = fma2(W, pk(r0.w, r0.w), Dn);
-      Aw = add2(Aw, W);
+      Dn = fma2(W, pk(r1.w, r1.w), Dn);
       T = sub2(T, W);
     }
     __syncwarp();
   }
 
-  float t[2], cr[2], cg[2], cb[2], dn[2], aw[2];
+  float t[2], cr[2], cg[2], cb[2], dn[2];
   upk(T, t[0], t[1]); upk(Cr, cr[0], cr[1]); upk(Cg, cg[0], cg[1]); upk(Cb, cb[0], cb[1]);
-  upk(Dn, dn[0], dn[1]); upk(Aw, aw[0], aw[1]);
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    if (!(k == 0 ? in0 : in1)) continue;
-    const int py = k == 0 ? py0 : py1;
-    const size_t p = ((size_t)e * rp.H + py) * rp.W + px;
-    const float r = fmaf(t[k], rp.bg[0], cr[k]), g = fmaf(t[k], rp.bg[1], cg[k]), bl = fmaf(t[k], rp.bg[2], cb[k]);
-    if (RGB && rgb) {
-      if (rp.rgb_format == 0) {
-        uint8_t* o = reinterpret_cast<uint8_t*>(rgb) + p * 3;
-        o[0] = (uint8_t)__float2uint_rn(fminf(fmaxf(r, 0.f), 1.f) * 255.f);
-        o[1] = (uint8_t)__float2uint_rn(fminf(fmaxf(g, 0.f), 1.f) * 255.f);
-        o[2] = (uint8_t)__float2uint_rn(fminf(fmaxf(bl, 0.f), 1.f) * 255.f);
-      } else {
-        float* o = reinterpret_cast<float*>(rgb) + p * 3;
-        o[0] = r; o[1] = g; o[2] = bl;
-      }
-    }
-    if (depth) depth[p] = aw[k] > 0.f ? dn[k] / aw[k] : 0.f;
-    if (alpha_out) alpha_out[p] = aw[k];
-  }
+  upk(Dn, dn[0], dn[1]);
+  const size_t p0 = ((size_t)e * rp.H + py0) * rp.W + px;
+  if (in0) write_pixel(rp, RGB ? rgb : nullptr, depth, alpha_out, p0, t[0], cr[0], cg[0], cb[0], dn[0]);
+  if (in1) write_pixel(rp, RGB ? rgb : nullptr, depth, alpha_out, p0 + 4 * (size_t)rp.W, t[1], cr[1], cg[1], cb[1], dn[1]);
 }
 
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
