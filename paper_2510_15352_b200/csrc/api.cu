@@ -91,7 +91,7 @@ struct gg_context {
   int scene_table_cap = 0;
   int chunk = DEFAULT_CHUNK;
   // workspace
-  DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase, zmm;
+  DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase;
   DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1, rmask;
   DevBuf sorted, ranges, counters, valid_out, perm, groups, blkbase, blkenv, ghist, thist, qctr;
   DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval, dconic;
@@ -107,7 +107,6 @@ struct gg_context {
   int32_t* h_perm = nullptr;
   EnvGroup* h_groups = nullptr;
   uint32_t* h_blkbase = nullptr;
-  uint32_t* h_zmm = nullptr;
   int h_cap = 0;
   // debug snapshot (host)
   std::vector<int32_t> d_tc, d_stile, d_sgid, d_ranges, d_neval;
@@ -188,10 +187,8 @@ bool ensure_host(gg_context* ctx, int n) {
   if (ctx->h_cap >= n) return true;
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase); cudaFreeHost(ctx->h_kbase);
   cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
-  cudaFreeHost(ctx->h_zmm);
   int cap = std::max(n, 1024);
   if (cudaMallocHost(&ctx->h_blkbase, (cap + 1) * 4) != cudaSuccess) return false;
-  if (cudaMallocHost(&ctx->h_zmm, cap * 8) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_ids, cap * 4) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_perm, cap * 4) != cudaSuccess) return false;
   if (cudaMallocHost(&ctx->h_groups, cap * sizeof(EnvGroup)) != cudaSuccess) return false;
@@ -297,7 +294,7 @@ gg_status gg_destroy(gg_context* ctx) {
     dev_free(ctx, sc.aux, s); dev_free(ctx, sc.qmax, s); dev_free(ctx, sc.sh, s);
   }
   for (auto& e : ctx->a_ev) cudaEventDestroy(e);
-  DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->zmm, &ctx->okflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
+  DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->okflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
                    &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect, &ctx->rmask,
                    &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->perm, &ctx->groups,
                    &ctx->blkbase, &ctx->blkenv, &ctx->ghist, &ctx->thist, &ctx->qctr,
@@ -310,7 +307,6 @@ gg_status gg_destroy(gg_context* ctx) {
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
   cudaFreeHost(ctx->h_kbase); cudaFreeHost(ctx->h_err);
   cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
-  cudaFreeHost(ctx->h_zmm);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev_copy);
   cudaStreamDestroy(s);
@@ -491,6 +487,15 @@ gg_status gg_get_stage_ms(gg_context* ctx, float* out3) {
 typedef gg_status (*chunk_cb)(gg_context*, int p0, int n, void* user);
 constexpr int HOST_COPY_SLICE = 128;   // envs per raster launch when frames stream to the host
 
+static uint32_t f32_bits(float x) {
+  uint32_t b;
+  memcpy(&b, &x, 4);
+  return b;
+}
+
+// depth-sort passes: keys are z bits - bits(near) in (0, bits(far) - bits(near)]
+static int depth_passes_for(float near_p, float far_p) { return depth_passes(f32_bits(far_p) - f32_bits(near_p)); }
+
 static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
                              const float* intr, int32_t W, int32_t H, const gg_render_opts* opts_in,
                              void* rgb, float* depth, float* alpha, cudaStream_t s, chunk_cb cb,
@@ -532,7 +537,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       !ensure(ctx, ctx->blkcnt, (size_t)chunk * nblk * 4, s) || !ensure(ctx, ctx->vcnt, chunk * 4, s) ||
       !ensure(ctx, ctx->kcnt, chunk * 4, s) || !ensure(ctx, ctx->rbase, chunk * 8, s) ||
       !ensure(ctx, ctx->kbase, chunk * 8, s) || !ensure(ctx, ctx->ranges, (size_t)chunk * ntiles * 8, s) ||
-      !ensure(ctx, ctx->zmm, (size_t)chunk * 8, s) || !ensure_host(ctx, std::max(E, chunk)) || (counters && !ensure(ctx, ctx->counters, (size_t)E * 32, s)))
+      !ensure_host(ctx, std::max(E, chunk)) || (counters && !ensure(ctx, ctx->counters, (size_t)E * 32, s)))
     return fail(ctx, GG_E_OOM, "gg_render: workspace allocation failed");
   if (counters) CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)E * 32, s));
   CK(cudaMemsetAsync(ctx->errflag.p, 0, 4, s));
@@ -590,14 +595,11 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ws.rec_base = P<uint64_t>(ctx->rbase);
     ws.k_base = P<uint64_t>(ctx->kbase);
     ws.ranges = P<uint2>(ctx->ranges);
-    ws.zmin = P<uint32_t>(ctx->zmm);
-    ws.zmax = P<uint32_t>(ctx->zmm) + chunk;
+    ws.zbase = f32_bits(opts.near_plane);
     ws.nwords = nwords;
     ws.nblk = nblk;
     ws.ec = ec;
     const EnvGroup* groups = P<EnvGroup>(ctx->groups);
-    CK(cudaMemsetAsync(ws.zmin, 0xff, ec * 4, s));
-    CK(cudaMemsetAsync(ws.zmax, 0, ec * 4, s));
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], s));
     // K1a + K2
     launch_cull_count(e0, ngroups, nblk, groups, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
@@ -631,8 +633,6 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ctx->launches++;
     CK(cudaGetLastError());
     ctx->launches += launch_copy_words(ctx->h_kcnt, ws.kcnt, ec * 4, s);
-    ctx->launches += launch_copy_words(ctx->h_zmm, ws.zmin, ec * 4, s);
-    ctx->launches += launch_copy_words(ctx->h_zmm + ctx->h_cap, ws.zmax, ec * 4, s);
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], s));
     CK(cudaStreamSynchronize(s));
     uint64_t K = 0;
@@ -647,10 +647,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     uint32_t nb = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_blkbase[i] = nb; nb += sort_blocks(ctx->h_vcnt[i]); }
     ctx->h_blkbase[ec] = nb;
-    uint32_t span = 0;
-    for (int i = 0; i < ec; ++i)
-      if (ctx->h_vcnt[i]) span = std::max(span, ctx->h_zmm[ctx->h_cap + i] - ctx->h_zmm[i]);
-    const int passes = depth_passes(span);
+    const int passes = depth_passes_for(opts.near_plane, opts.far_plane);
     if (!ensure(ctx, ctx->blkbase, (size_t)(ec + 1) * 4, s) || !ensure(ctx, ctx->blkenv, (size_t)nb * 4 + 4, s) ||
         !ensure(ctx, ctx->ghist, (size_t)nb * sort_ghist_words() * 4, s) ||
         !ensure(ctx, ctx->thist, (size_t)nb * ntiles * 4, s))
@@ -765,12 +762,6 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
 // number of depth passes follows from [near, far].  No host synchronisation
 // and no allocation: the call can be captured in a CUDA graph.  Capacity
 // overflow marks the chunk invalid and raises a sticky GG_E_CAPACITY.
-static int depth_passes_for(float near_p, float far_p) {
-  uint32_t a, b;
-  memcpy(&a, &near_p, 4);
-  memcpy(&b, &far_p, 4);
-  return depth_passes(b - a);
-}
 
 static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
                               const float* intr, int32_t W, int32_t H, const gg_render_opts& opts, void* rgb,
@@ -823,7 +814,7 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
     ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
     ws.rmask = rp.ellipse ? P<uint32_t>(ctx->rmask) : nullptr;
-    ws.zmin = P<uint32_t>(ctx->zmm); ws.zmax = P<uint32_t>(ctx->zmm) + chunk;
+    ws.zbase = f32_bits(opts.near_plane);
     ws.dp0 = P<uint64_t>(ctx->dk0); ws.dp1 = P<uint64_t>(ctx->dk1); ws.order = P<uint32_t>(ctx->dv0);
     ws.sorted = P<uint32_t>(ctx->sorted);
     ws.ranges = P<uint2>(ctx->ranges);
@@ -833,8 +824,6 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     ws.ec = ec;
     if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 0], s));
     CK(cudaMemsetAsync(ws.kcnt, 0, ec * 4, s));
-    CK(cudaMemsetAsync(ws.zmin, 0xff, ec * 4, s));
-    CK(cudaMemsetAsync(ws.zmax, 0, ec * 4, s));
     CK(cudaMemsetAsync(ok, 0x01, 4, s));
     launch_cull_count(e0, ngroups, nblk, nullptr, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
@@ -884,7 +873,7 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
   bool okb = ensure(ctx, ctx->envc, sizeof(EnvConst) * max_envs, s) &&
              ensure(ctx, ctx->flags, (size_t)ch * nblk * 8 * 4, s) && ensure(ctx, ctx->blkcnt, (size_t)ch * nblk * 4, s) &&
              ensure(ctx, ctx->vcnt, ch * 4, s) && ensure(ctx, ctx->kcnt, ch * 4, s) && ensure(ctx, ctx->rbase, ch * 8, s) &&
-             ensure(ctx, ctx->kbase, ch * 8, s) && ensure(ctx, ctx->zmm, (size_t)ch * 8, s) &&
+             ensure(ctx, ctx->kbase, ch * 8, s) &&
              ensure(ctx, ctx->ranges, (size_t)ch * ntiles * 8, s) && ensure(ctx, ctx->okflag, 16, s) &&
              ensure(ctx, ctx->counters, (size_t)max_envs * 32, s) && ensure(ctx, ctx->rec0, vcap * 16, s) &&
              ensure(ctx, ctx->rec1, vcap * 16, s) && ensure(ctx, ctx->rec2, vcap * 16, s) &&

@@ -88,8 +88,7 @@ struct ChunkWS {
   uint2* rect;          // (x0 | x1<<16, y0 | y1<<16)
   uint32_t* rmask;      // [V] R37 kept-tile masks of <= 32-tile rects (null: variant off)
   uint32_t* zkey;       // f32 bits of z
-  uint32_t* zmin;       // [Ec] min / max depth bits per env (depth-sort key offset)
-  uint32_t* zmax;
+  uint32_t zbase;       // f32 bits of the near plane: depth-sort key = z bits - zbase, in (0, bits(far) - zbase]
   uint32_t* gid;        // Gaussian index (debug dumps only; may be null)
   // depth-sort scratch [V]: packed (key - zmin) << 32 | record ping-pong, and
   // the last pass's output (records in depth order)

@@ -111,12 +111,10 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 
 // conservative footprint test (DESIGN.md §4 K1a): lambda1 <= a + c + sqrt(0.1)
 // and a + c <= s_max^2 |T|_F^2 + 0.6; generous margins absorb f32 rounding.
-__device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float smax2, const RenderParams& rp,
-                                              uint32_t& zbits) {
+__device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float smax2, const RenderParams& rp) {
   // p_z in the canonical order (it decides near/far exactly); p_x, p_y only
   // feed the margin-protected footprint test
   const float pz = fa(dot3(c.R[6], g.x, c.R[7], g.y, c.R[8], g.z), c.t[2]);
-  zbits = __float_as_uint(pz);
   if (!(pz > rp.near_p && pz <= rp.far_p)) return false;
   const float px = fmaf(c.R[2], g.z, fmaf(c.R[1], g.y, fmaf(c.R[0], g.x, c.t[0])));
   const float py = fmaf(c.R[5], g.z, fmaf(c.R[4], g.y, fmaf(c.R[3], g.x, c.t[1])));
@@ -139,11 +137,9 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
                   const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
   __shared__ EnvConst cams[ENV_GROUP];
   __shared__ uint32_t wc[ENV_GROUP][PROJ_BLOCK / 32];
-  __shared__ uint32_t szmn[ENV_GROUP], szmx[ENV_GROUP];   // the CTA's depth-key range per env
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0) return;
   load_group_cams(cams, envs, e0, grp);
-  if (threadIdx.x < ENV_GROUP) { szmn[threadIdx.x] = 0xffffffffu; szmx[threadIdx.x] = 0u; }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.y * PROJ_BLOCK + threadIdx.x;
@@ -151,9 +147,9 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
   float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
   float smax2 = 0.f;
   const int wi = blockIdx.y * (PROJ_BLOCK / 32) + warp;
-  // lane k keeps env k's visibility word and depth-key range (no per-env
-  // branch in the loop; ENV_GROUP <= 32)
-  uint32_t my_word = 0u, my_zmn = 0xffffffffu, my_zmx = 0u;
+  // lane k keeps env k's visibility word (no per-env branch in the loop;
+  // ENV_GROUP <= 32)
+  uint32_t my_word = 0u;
   for (int k = 0; k < grp.cnt; ++k) {
     const EnvConst c = load_cam(&cams[k]);
     if (c.scene != cur) {             // uniform across the CTA
@@ -164,21 +160,13 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
         smax2 = __ldg(&sc.aux[i]).y;
       }
     }
-    uint32_t zb = 0;
-    const bool keep = i < c.n && maybe_visible(c, g, smax2, rp, zb);
+    const bool keep = i < c.n && maybe_visible(c, g, smax2, rp);
     const uint32_t word = __ballot_sync(0xffffffffu, keep);
-    // depth-key range of the kept records (= the env's record set): sort key offset
-    const uint32_t zmn = __reduce_min_sync(0xffffffffu, keep ? zb : 0xffffffffu);
-    const uint32_t zmx = __reduce_max_sync(0xffffffffu, keep ? zb : 0u);
-    if (lane == k) { my_word = word; my_zmn = zmn; my_zmx = zmx; }
+    if (lane == k) my_word = word;
   }
   if (lane < grp.cnt) {
     ws.flags[(size_t)(grp.elo + lane) * ws.nwords + wi] = my_word;
     wc[lane][warp] = __popc(my_word);
-    if (my_word) {
-      atomicMin(&szmn[lane], my_zmn);
-      atomicMax(&szmx[lane], my_zmx);
-    }
   }
   __syncthreads();
   if (threadIdx.x < grp.cnt) {
@@ -186,10 +174,6 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
 #pragma unroll
     for (int w = 0; w < PROJ_BLOCK / 32; ++w) s += wc[threadIdx.x][w];
     ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blockIdx.y] = s;
-    if (s) {
-      atomicMin(&ws.zmin[grp.elo + threadIdx.x], szmn[threadIdx.x]);
-      atomicMax(&ws.zmax[grp.elo + threadIdx.x], szmx[threadIdx.x]);
-    }
   }
 }
 

@@ -117,13 +117,14 @@ __device__ __forceinline__ void unpack_rect(uint2 r, uint32_t& x0, uint32_t& x1,
 }
 
 // Input / output arrays of depth pass p (all indexed rec_base[e] + j).  The
-// sort key is the f32 depth bits minus the env's minimum (a monotone map of
-// the positive f32 bits), so a typical ~27-bit span needs 3 passes of 10 bits.
+// sort key is the f32 depth bits minus those of the near plane (a monotone map
+// of the positive f32 bits; every record has near < z <= far), so the default
+// [0.01, 1e10] span (29 bits) needs 3 passes of 10 bits.
 // Between passes key and record travel as one 64-bit word (key << 32 |
 // record): one load, one staging store and one scattered store per element.
 struct DepthIO {
   const uint32_t* zin;   // first pass: f32 depth bits (records = identity j)
-  const uint64_t* pin;   // later passes: packed (key - zmin) << 32 | record
+  const uint64_t* pin;   // later passes: packed (z bits - zbase) << 32 | record
   uint64_t* pout;        // packed out (null on the last pass)
   uint32_t* vout;        // last pass: records in depth order
 };
@@ -132,7 +133,7 @@ __device__ __forceinline__ uint32_t depth_digit(uint32_t key, int shift) {
   return (key >> shift) & (DS_RADIX - 1);
 }
 
-// element i of the block as (key - zmin) << 32 | record
+// element i of the block as (z bits - zbase) << 32 | record
 __device__ __forceinline__ uint64_t depth_elem(const DepthIO& io, uint64_t at, uint32_t j, uint32_t zmin) {
   return io.zin ? ((uint64_t)(io.zin[at] - zmin) << 32) | j : io.pin[at];
 }
@@ -143,7 +144,7 @@ __device__ __forceinline__ void depth_upsweep_block(uint32_t b, const BlockTable
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
   const uint64_t rb = ws.rec_base[e];
-  const uint32_t zmin = ws.zmin[e];
+  const uint32_t zmin = ws.zbase;
   for (int i = threadIdx.x; i < DS_RADIX; i += DS_THREADS) h[i] = 0;
   __syncthreads();
   uint32_t k[DS_IPT];                              // all of this thread's keys in flight first
@@ -286,7 +287,7 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
   const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
   const uint32_t n = min((uint32_t)SORT_BLK, ws.vcnt[e] - j0);
   const uint64_t rb = ws.rec_base[e];
-  const uint32_t zmin = ws.zmin[e];
+  const uint32_t zmin = ws.zbase;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < DS_WARPS * DS_RADIX / 2; i += DS_THREADS) (&sm.u.r.wcnt[0][0])[i] = 0u;
   for (int i = tid; i < DS_WARPS * 32; i += DS_THREADS) (&sm.u.r.pm[0][0])[i] = 0u;
@@ -659,7 +660,7 @@ uint32_t sort_blocks(uint32_t V) { return (V + SORT_BLK - 1) / SORT_BLK; }
 int sort_block_size() { return SORT_BLK; }
 size_t sort_ghist_words() { return DS_RADIX; }
 
-// number of depth passes for a key span (max over the chunk's envs of zmax - zmin)
+// number of depth passes for a key span (bits(far) - bits(near))
 int depth_passes(uint32_t span) {
   int bits = 0;
   while (bits < 32 && (span >> bits) != 0) ++bits;
