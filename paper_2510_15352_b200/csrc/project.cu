@@ -322,8 +322,22 @@ __device__ __forceinline__ bool tile_keeps(float u, float v, float A, float B, f
 
 constexpr int SH_MAX = 48;              // floats per Gaussian at degree 3
 
+// Cameras stored field-major (float2 pair q of env k at camT[q][k]): the lanes
+// of a warp read the cameras of several envs at once, and a field-major
+// 64-bit load of up to 16 envs is one contiguous 128-B row (no bank
+// conflicts), where 128-bit loads of whole 112-B records conflicted.
+typedef float2 CamWord;
+constexpr int CAM_F2 = (int)(sizeof(EnvConst) / sizeof(CamWord));
+__device__ __forceinline__ EnvConst load_cam_t(const CamWord (*camT)[ENV_GROUP], int k) {
+  EnvConst c;
+  CamWord* d = reinterpret_cast<CamWord*>(&c);
+#pragma unroll
+  for (int q = 0; q < CAM_F2; ++q) d[q] = camT[q][k];
+  return c;
+}
+
 struct ProjSmem {
-  EnvConst cams[ENV_GROUP];
+  CamWord camT[CAM_F2][ENV_GROUP];
   uint32_t fw[ENV_GROUP * 8];        // visibility words (env, word)
   uint32_t cnt[ENV_GROUP * 8];       // popc per (env, word), then exclusive prefix within the env
   uint32_t wsum[PROJ_BLOCK / 32];
@@ -342,7 +356,10 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   const int tid = threadIdx.x;
   const int gblk = blockIdx.y;
   const int i0 = gblk * PROJ_BLOCK;
-  load_group_cams(sm.cams, envs, e0, grp);
+  {
+    const CamWord* src = reinterpret_cast<const CamWord*>(envs + e0 + grp.elo);
+    for (int i = threadIdx.x; i < grp.cnt * CAM_F2; i += blockDim.x) sm.camT[i % CAM_F2][i / CAM_F2] = src[i];
+  }
   // visibility words of the group -> (Gaussian, env) pair list in (gid, env)
   // order: lanes that share a Gaussian read the same scene lines (L1
   // broadcast) and a warp touches only a few adjacent Gaussians.  A record's index is its rank within its env (gid order),
@@ -408,7 +425,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   for (uint32_t s = tid; s < total; s += PROJ_BLOCK) {
     const uint32_t ent = sm.list[s];
     const int k = ent >> 8, l = ent & 255;
-    const EnvConst c = load_cam(&sm.cams[k]);
+    const EnvConst c = load_cam_t(sm.camT, k);
     const int eloc = grp.elo + k;
     const uint32_t rank = sm.cnt[k * 8 + (l >> 5)] + __popc(sm.fw[k * 8 + (l >> 5)] & ((1u << (l & 31)) - 1u));
     const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + rank;
