@@ -569,8 +569,15 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   if (keep && !ensure(ctx, ctx->gid, 16, s)) return fail(ctx, GG_E_OOM, "alloc");
 
   float ms[3] = {0, 0, 0};
-  for (int e0 = 0; e0 < E; e0 += chunk) {
-    const int ec = std::min(chunk, E - e0);
+  for (int e0 = 0, ec = 0; e0 < E; e0 += ec) {
+    ec = std::min(chunk, E - e0);
+    if (cb && chunk >= 64) {
+      // host path: a short first chunk gets frames onto the copy engine early,
+      // a short last chunk leaves little of the copy backlog after the render
+      const int q = chunk / 4, rem = E - e0;
+      if (e0 == 0 && rem > q) ec = q;
+      else if (rem > q && rem <= chunk + q) ec = rem - q;
+    }
     // env groups: runs of one scene, <= ENV_GROUP envs
     int ngroups = 0, max_deg = 0;
     for (int i = 0; i < ec;) {
