@@ -81,14 +81,25 @@ def _room(args3):
 
 
 def make_scenes(args, c):
-    """The config's scene, or S seeded rooms (generated in parallel on the host)."""
+    """The config's scene, or an iterator over S seeded rooms generated in parallel on the host (streamed: each
+    room is loaded onto the GPU and dropped, so c5's 2,500 rooms never sit in host memory at once)."""
     S = c["n_scenes"]
     if S == 1:
         return [gi.config_scene(args.config, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])]
     import concurrent.futures as cf
     n_proc = max(1, min(16, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 4))
-    with cf.ProcessPoolExecutor(n_proc) as ex:
-        return list(ex.map(_room, [(k, c["n_gauss"], c["sh_degree"]) for k in range(S)]))
+    ex = cf.ProcessPoolExecutor(n_proc)
+    futs = [ex.submit(_room, (k, c["n_gauss"], c["sh_degree"])) for k in range(min(S, 2 * n_proc))]
+
+    def gen():
+        for k in range(S):
+            sc_ = futs[k].result()
+            futs[k] = None
+            if k + 2 * n_proc < S:
+                futs.append(ex.submit(_room, (k + 2 * n_proc, c["n_gauss"], c["sh_degree"])))
+            yield sc_
+        ex.shutdown()
+    return gen()
 
 
 def workload(args):
@@ -252,14 +263,24 @@ def main():
     want_rgb = args.outputs != "depth"
 
     # ---- inputs: scene replica + pre-generated pose sets, resident in HBM
-    scenes = make_scenes(args, c)
-    S = len(scenes)
-    scene = scenes[0]
+    S = c["n_scenes"]
     R = gg.Renderer(gpu)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    sids = [R.load_scene(t(sc_.means), t(sc_.scales), t(sc_.quats), t(sc_.opacities), t(sc_.sh), sc_.sh_degree)
-            for sc_ in scenes]
     binding = gi.scene_binding(7 + rank, E, S) if S > 1 else np.zeros(E, np.int32)
+    n_sets = args.warmup + args.steps
+    # a fresh, seeded pose set for every step, all resident in HBM; each env's camera
+    # lives in its own scene, drawn while that scene is at hand
+    vm = np.empty((n_sets, E, 4, 4), np.float32)
+    sids, scene = [], None
+    for k, sc_ in enumerate(make_scenes(args, c)):
+        sids.append(R.load_scene(t(sc_.means), t(sc_.scales), t(sc_.quats), t(sc_.opacities), t(sc_.sh),
+                                 sc_.sh_degree))
+        if k == int(binding[0]):
+            scene = sc_                          # kept for the CPU baseline's sample
+        idx = np.flatnonzero(binding == k)
+        for s_ in range(n_sets if idx.size else 0):
+            seed = 10_000 * (rank + 1) + s_ if S == 1 else 10_000 * (rank + 1) + 4096 * s_ + k
+            vm[s_, idx] = gi.cameras(seed, idx.size, W, H, sc_).viewmats
     ids_np = np.asarray(sids, np.int32)[binding]
     gg.gg_reserve(R.ctx, E, W, H, args.chunk)
     use_async = args.mode in ("async", "graph") and not args.blur
@@ -267,18 +288,6 @@ def main():
         gg.gg_reserve_async(R.ctx, E, W, H, args.chunk, 0.7, 4.0)
     tiles_flag = {"paper": 0, "tight": gg.GG_TIGHT_TILES, "ellipse": gg.GG_ELLIPSE_TILES}[args.tiles]
     mflag = (gg.GG_ASYNC if use_async else 0) | tiles_flag
-    n_sets = args.warmup + args.steps
-    # a fresh, seeded pose set for every step, all resident in HBM
-    def pose_set(s):
-        if S == 1:
-            return gi.cameras(10_000 * (rank + 1) + s, E, W, H, scene).viewmats
-        V = np.empty((E, 4, 4), np.float32)
-        for k in range(S):                       # each env's camera lives in its own scene
-            idx = np.flatnonzero(binding == k)
-            if idx.size:
-                V[idx] = gi.cameras(10_000 * (rank + 1) + 4096 * s + k, idx.size, W, H, scenes[k]).viewmats
-        return V
-    vm = np.stack([pose_set(s) for s in range(n_sets)])
     intr = t(np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1)))
     vm_d = t(vm)
     ids = t(ids_np)
@@ -478,7 +487,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         cams0 = gi.Cameras(vm[0], np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1)), W, H)
         envs = [int(e) for e in np.flatnonzero(binding == binding[0])[: max(1, min(args.cpu_envs, E))]]
-        dt, cores = oracle_sample(scenes[int(binding[0])], cams0, envs, -1)
+        dt, cores = oracle_sample(scene, cams0, envs, -1)
         cpu = {"value": len(envs) / dt, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"{len(envs)} envs of pose set 0 (full {W}x{H} frames, {scene.n:,} Gaussians "
                          f"SH{scene.sh_degree}), incl. O1 preprocessing"}
