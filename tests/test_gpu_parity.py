@@ -67,7 +67,8 @@ def parity_envs(gg, r, scenes, sids, cams, envs, tally, ints=True, sh_degree=-1,
             oscenes[s] = oracle.OracleScene.from_inputs(scenes[s])
         o = oracle.render_env(oscenes[s], cams.viewmats[e], cams.intrinsics[e], cams.width, cams.height,
                               sh_degree=sh_degree, background=tuple(float(np.float32(b)) for b in background),
-                              flags=oflag)
+                              flags=oflag, near=float(np.float32(kw.get("near_plane", 0.01))),
+                              far=float(np.float32(kw.get("far_plane", 1e10))))
         tally.add(rgb[e], depth[e], alpha[e], o)
         if ints:
             render(gg, r, sids, cams, sh_degree=sh_degree,
@@ -87,6 +88,22 @@ def test_c1_full(gg, R):
     parity_envs(gg, R, {sid: sc}, [sid] * cams.n, cams, range(cams.n), t)
     t.check()
     print(t)
+
+
+@pytest.mark.parametrize("near,far,passes", [(4.0, 4.4, 2), (0.01, 1e10, 3), (1e-30, 1e10, 4)])
+def test_depth_pass_counts(gg, R, near, far, passes):
+    """The depth-sort key is z bits - bits(near) (every record has near < z <= far),
+    so [near, far] fixes the number of 10-bit passes: a thin slab of the cloud
+    sorts in 2 passes, an extreme span in 4.  Lists and images match the
+    oracle run with the same planes."""
+    span = int(np.float32(far).view(np.uint32)) - int(np.float32(near).view(np.uint32))
+    assert (span.bit_length() + 9) // 10 == passes
+    sc = gi.random_cloud(1500, 400, sh_degree=1)
+    cams = gi.cloud_cameras(1500, 3)
+    sid = load(R, sc)
+    t = Tally()
+    parity_envs(gg, R, {sid: sc}, [sid] * 3, cams, range(3), t, near_plane=near, far_plane=far)
+    t.check()
 
 
 @pytest.mark.parametrize("seed", range(12))
