@@ -230,13 +230,11 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
 // the loader was measured slower: 87.9 vs 85.5 ms per c3 step).
 constexpr int RW_THREADS = 128;
 
-// The next batch's records are prefetched into registers while the current
-// batch is walked (the record gathers' latency hides behind the blend).  The
-// stop test looks at T' alone: a non-passing pixel has w = 0 and T' = T >=
+// The stop test looks at T' alone: a non-passing pixel has w = 0 and T' = T >=
 // 1e-4, so only a passing pixel can stop; its weight is zeroed by a select.
 template <bool RGB>   // false: depth-only render (no colour accumulation)
 #ifndef GG_RW_MINB
-#define GG_RW_MINB 10   // 48 registers, 40 warps/SM: measured best (8: 91.4, 9: 95.6, 10: 87.9, 11: 94.1 ms per c3 step)
+#define GG_RW_MINB 12   // 40 registers, 48 warps/SM: measured best (10: 82.2, 11-12: 81.5, 14: 90.2 ms per c3 step)
 #endif
 __global__ void __launch_bounds__(RW_THREADS, GG_RW_MINB)
 raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
@@ -268,16 +266,14 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
   float cut0 = in0 ? LOG2_CUTOFF : INF, cut1 = in1 ? LOG2_CUTOFF : INF;
   const uint32_t lt = (1u << lane) - 1u;
 
-  // records of the current batch in registers, the next batch's indices
-  float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
-  if (rg.x + lane < rg.y) {
-    const uint32_t i0 = __ldg(&list[rg.x + lane]);
-    a0 = __ldg(&R0[i0]); a1 = __ldg(&R1[i0]); a2 = __ldg(&R2[i0]);
-  }
-  uint32_t nidx = rg.x + 32 + lane < rg.y ? __ldg(&list[rg.x + 32 + lane]) : 0u;
+  // this batch's list entries are loaded one batch ahead
+  uint32_t nidx = rg.x + lane < rg.y ? __ldg(&list[rg.x + lane]) : 0u;
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
     if (__all_sync(0xffffffffu, cut0 == INF && cut1 == INF)) break;
     const bool valid = b + lane < rg.y;
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
+    if (valid) { a0 = __ldg(&R0[nidx]); a1 = __ldg(&R1[nidx]); a2 = __ldg(&R2[nidx]); }
+    nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
     const float lx0 = bx0, lx1 = bx0 + 7.f, ly0 = by0, ly1 = by0 + 7.f;
     bool mine = false;
     if (valid && a1.w >= 0.f && a0.z >= LOG2_CUTOFF) {
@@ -291,11 +287,6 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
       srec[warp][3 * pos + 1] = make_float4(a1.x, a1.y, a1.z, a0.w);
       srec[warp][3 * pos + 2] = a2;
     }
-    // prefetch: the next batch's records, the batch after's indices
-    if (b + 32 + lane < rg.y) {
-      a0 = __ldg(&R0[nidx]); a1 = __ldg(&R1[nidx]); a2 = __ldg(&R2[nidx]);
-    }
-    nidx = b + 64 + lane < rg.y ? __ldg(&list[b + 64 + lane]) : 0u;
     __syncwarp();
     const uint32_t cnt = __popc(m);
     for (uint32_t i = 0; i < cnt; ++i) {
