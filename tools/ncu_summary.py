@@ -21,6 +21,9 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
            "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
            "sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+           "l1tex__throughput.avg.pct_of_peak_sustained_active",
+           "lts__throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__warps_active.avg.pct_of_peak_sustained_active",
            "dram__throughput.avg.pct_of_peak_sustained_elapsed",
            "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size"]
@@ -97,13 +100,16 @@ with open(os.path.join(DST, "ncu_summary.md"), "w") as f:
     for k, a in sorted(agg.items(), key=lambda x: -x[1]["seconds"]):
         f.write(f"| {k} | {a['launches']} | {a['seconds']*1e3:.2f} | {a['share']*100:.1f}% |\n")
     f.write("\nFull captures (one launch = one 512-env chunk):\n\n| kernel | ms | DRAM read GB | DRAM write GB | "
-            "issue % | FMA pipe % | ALU pipe % | XU pipe % | warps active % | regs |\n|---|---|---|---|---|---|---|---|---|---|\n")
+            "issue % | FMA pipe % | ALU pipe % | XU (MUFU) inst % | L1 % | L2 % | warps active % | regs |\n"
+            "|---|---|---|---|---|---|---|---|---|---|---|---|\n")
     for k, r in kern.items():
         f.write(f"| {k} | {r.get('gpu__time_duration.sum', 0)*1e3:.2f} | {r.get('dram__bytes_read.sum', 0)/1e9:.2f} | "
                 f"{r.get('dram__bytes_write.sum', 0)/1e9:.2f} | {r.get('sm__issue_active.avg.pct_of_peak_sustained_elapsed', 0):.0f} | "
                 f"{r.get('sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active', 0):.0f} | "
                 f"{r.get('sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active', 0):.0f} | "
-                f"{r.get('sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active', 0):.0f} | "
+                f"{r.get('sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active', r.get('sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active', 0)):.0f} | "
+                f"{r.get('l1tex__throughput.avg.pct_of_peak_sustained_active', 0):.0f} | "
+                f"{r.get('lts__throughput.avg.pct_of_peak_sustained_elapsed', 0):.0f} | "
                 f"{r.get('sm__warps_active.avg.pct_of_peak_sustained_active', 0):.0f} | "
                 f"{r.get('launch__registers_per_thread', 0):.0f} |\n")
 import shutil
