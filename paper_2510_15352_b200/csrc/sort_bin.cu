@@ -329,7 +329,7 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
 
 template <bool LOOP>
 #ifndef GG_DS_MINB
-#define GG_DS_MINB 3   // 40 registers: the packed elements stay (mostly) in registers
+#define GG_DS_MINB 2   // 64 registers, no spills: measured best (2: 4.69, 3: 5.05, 4: 5.51 ms per 1024 envs)
 #endif
 __global__ void __launch_bounds__(DS_THREADS, GG_DS_MINB)
 depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const uint32_t* ghist) {
