@@ -650,7 +650,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       return fail(ctx, GG_E_OOM, "gg_render: key workspace (%llu keys) allocation failed", (unsigned long long)K);
     ctx->launches += launch_copy_words(ctx->kbase.p, ctx->h_kbase, ec * 8, s);
     ws.sorted = P<uint32_t>(ctx->sorted);
-    // K3-K5: sort blocks of 4096 records, never straddling an env
+    // K3-K5: sort blocks of sort_block_size() records, never straddling an env
     uint32_t nb = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_blkbase[i] = nb; nb += sort_blocks(ctx->h_vcnt[i]); }
     ctx->h_blkbase[ec] = nb;
