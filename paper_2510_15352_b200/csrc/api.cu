@@ -446,7 +446,7 @@ gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t W, int32_t H, in
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   const int ntiles = ((W + TILE - 1) / TILE) * ((H + TILE - 1) / TILE);
   bool ok = ensure(ctx, ctx->envc, sizeof(EnvConst) * max_envs, s) &&
-            ensure(ctx, ctx->flags, (size_t)ec * nblk * 8 * 4, s) &&
+            ensure(ctx, ctx->flags, (size_t)ec * nblk * PROJ_WPB * 4, s) &&
             ensure(ctx, ctx->blkcnt, (size_t)ec * nblk * 4, s) && ensure(ctx, ctx->vcnt, ec * 4, s) &&
             ensure(ctx, ctx->kcnt, ec * 4, s) && ensure(ctx, ctx->rbase, ec * 8, s) &&
             ensure(ctx, ctx->kbase, ec * 8, s) && ensure(ctx, ctx->ranges, (size_t)ec * ntiles * 8, s) &&
@@ -878,7 +878,7 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
   const uint64_t kcap = (uint64_t)((double)vcap * keys_per_visible) + 1;
   const uint64_t nbcap = vcap / (uint64_t)sort_block_size() + ch + 1;
   bool okb = ensure(ctx, ctx->envc, sizeof(EnvConst) * max_envs, s) &&
-             ensure(ctx, ctx->flags, (size_t)ch * nblk * 8 * 4, s) && ensure(ctx, ctx->blkcnt, (size_t)ch * nblk * 4, s) &&
+             ensure(ctx, ctx->flags, (size_t)ch * nblk * PROJ_WPB * 4, s) && ensure(ctx, ctx->blkcnt, (size_t)ch * nblk * 4, s) &&
              ensure(ctx, ctx->vcnt, ch * 4, s) && ensure(ctx, ctx->kcnt, ch * 4, s) && ensure(ctx, ctx->rbase, ch * 8, s) &&
              ensure(ctx, ctx->kbase, ch * 8, s) &&
              ensure(ctx, ctx->ranges, (size_t)ch * ntiles * 8, s) && ensure(ctx, ctx->okflag, 16, s) &&

@@ -338,16 +338,16 @@ __device__ __forceinline__ EnvConst load_cam_t(const CamWord (*camT)[ENV_GROUP],
 
 struct ProjSmem {
   CamWord camT[CAM_F2][ENV_GROUP];
-  uint32_t fw[ENV_GROUP * 8];        // visibility words (env, word)
-  uint32_t cnt[ENV_GROUP * 8];       // popc per (env, word), then exclusive prefix within the env
+  uint32_t fw[ENV_GROUP * PROJ_WPB];   // visibility words (env, word)
+  uint32_t cnt[ENV_GROUP * PROJ_WPB];  // popc per (env, word), then exclusive prefix within the env
   uint32_t wsum[PROJ_BLOCK / 32];
   uint32_t kacc[ENV_GROUP];
   uint32_t total;
-  uint16_t list[ENV_GROUP * PROJ_BLOCK];   // (k << 8) | local
+  uint16_t list[ENV_GROUP * PROJ_BLOCK];   // (k << PROJ_LB) | local
 };
 
 template <bool ELL>   // GG_ELLIPSE_TILES (reading R37): per-record tile masks
-__global__ void __launch_bounds__(PROJ_BLOCK, 4)
+__global__ void __launch_bounds__(PROJ_BLOCK, 1024 / PROJ_BLOCK)
 project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
                const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
   __shared__ ProjSmem sm;
@@ -364,21 +364,21 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   // order: lanes that share a Gaussian read the same scene lines (L1
   // broadcast) and a warp touches only a few adjacent Gaussians.  A record's index is its rank within its env (gid order),
   // which does not depend on which thread computes it.
-  if (tid < ENV_GROUP * 8) {
-    const int k = tid >> 3, w = tid & 7;
+  for (int q = tid; q < ENV_GROUP * PROJ_WPB; q += PROJ_BLOCK) {
+    const int k = q / PROJ_WPB, w = q % PROJ_WPB;
     uint32_t word = 0;
-    if (k < grp.cnt) word = ws.flags[(size_t)(grp.elo + k) * ws.nwords + gblk * 8 + w];
-    sm.fw[tid] = word;
-    sm.cnt[tid] = __popc(word);
+    if (k < grp.cnt) word = ws.flags[(size_t)(grp.elo + k) * ws.nwords + gblk * PROJ_WPB + w];
+    sm.fw[q] = word;
+    sm.cnt[q] = __popc(word);
   }
   if (tid < ENV_GROUP) sm.kacc[tid] = 0;
   __syncthreads();
   if (tid < ENV_GROUP) {   // per env: exclusive prefix of its 8 word counts
     uint32_t run = 0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const uint32_t c = sm.cnt[tid * 8 + w];
-      sm.cnt[tid * 8 + w] = run;
+    for (int w = 0; w < PROJ_WPB; ++w) {
+      const uint32_t c = sm.cnt[tid * PROJ_WPB + w];
+      sm.cnt[tid * PROJ_WPB + w] = run;
       run += c;
     }
   }
@@ -387,7 +387,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   {
     const int w = tid >> 5, b = tid & 31;
 #pragma unroll
-    for (int k = 0; k < ENV_GROUP; ++k) emask |= ((sm.fw[k * 8 + w] >> b) & 1u) << k;
+    for (int k = 0; k < ENV_GROUP; ++k) emask |= ((sm.fw[k * PROJ_WPB + w] >> b) & 1u) << k;
   }
   const uint32_t ecnt = __popc(emask);
   {
@@ -416,7 +416,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     while (m) {
       const int k = __ffs(m) - 1;
       m &= m - 1;
-      sm.list[o++] = (uint16_t)((k << 8) | tid);
+      sm.list[o++] = (uint16_t)((k << PROJ_LB) | tid);
     }
   }
   const uint32_t total = sm.total;
@@ -424,10 +424,10 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   __syncthreads();   // the pair list is complete
   for (uint32_t s = tid; s < total; s += PROJ_BLOCK) {
     const uint32_t ent = sm.list[s];
-    const int k = ent >> 8, l = ent & 255;
+    const int k = ent >> PROJ_LB, l = ent & (PROJ_BLOCK - 1);
     const EnvConst c = load_cam_t(sm.camT, k);
     const int eloc = grp.elo + k;
-    const uint32_t rank = sm.cnt[k * 8 + (l >> 5)] + __popc(sm.fw[k * 8 + (l >> 5)] & ((1u << (l & 31)) - 1u));
+    const uint32_t rank = sm.cnt[k * PROJ_WPB + (l >> 5)] + __popc(sm.fw[k * PROJ_WPB + (l >> 5)] & ((1u << (l & 31)) - 1u));
     const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + rank;
     const DevScene& scn = scenes[c.scene];
     const int gi = i0 + l;
