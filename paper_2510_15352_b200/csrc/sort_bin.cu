@@ -35,7 +35,12 @@ namespace gg {
 
 constexpr int SB_THREADS = 1024;                // placement kernels
 constexpr int SB_WARPS = 32;
-constexpr int PD_THREADS = 512;                 // placement downsweep: 16 warps = up to 16 segments
+#ifndef GG_PD_THREADS
+#define GG_PD_THREADS 512   // measured: 256 threads (8 longer segments) 11.5 vs 6.3 ms per 1024 envs
+#endif
+constexpr int PD_THREADS = GG_PD_THREADS;        // placement downsweep: 16 warps = up to 16 segments
+constexpr int PD_MINB = 1536 / PD_THREADS;       // resident CTAs per SM the smem budget below allows
+constexpr int PD_SMEM = 216 * 1024 / PD_MINB;    // shared-memory budget per CTA
 constexpr int PD_WARPS = PD_THREADS / 32;
 #ifndef GG_SORT_BLK
 #define GG_SORT_BLK 6144   // measured: sort stage 56.4 (4096), 54.9 (5120), 53.4 (6144), 53.7 (7168), 59.9 (8192) ms per c3 step
@@ -592,7 +597,7 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
 }
 
 template <int TB, bool LOOP, bool MASK>
-__global__ void __launch_bounds__(PD_THREADS, 3)
+__global__ void __launch_bounds__(PD_THREADS, PD_MINB)
 place_downsweep_kernel(BlockTable bt, ChunkWS ws, const uint32_t* order, RenderParams rp, const uint32_t* thist,
                        int S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -619,7 +624,7 @@ static size_t place_seg_bytes(int ntiles) {
   return ntiles <= 2048 ? w + 128 + (size_t)ntiles : w;
 }
 int place_segments(int ntiles) {
-  const size_t budget = 72 * 1024 - (size_t)ntiles * 4;
+  const size_t budget = PD_SMEM - (size_t)ntiles * 4;
   const int s = (int)(budget / place_seg_bytes(ntiles));
   return s < 1 ? 1 : (s > PD_WARPS ? PD_WARPS : s);
 }
@@ -630,13 +635,13 @@ size_t place_down_smem(int ntiles) {
 template <bool LOOP, bool MASK>
 static cudaError_t place_init_variant() {
   cudaError_t e = cudaFuncSetAttribute(place_downsweep_kernel<8, LOOP, MASK>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, PD_SMEM);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(place_downsweep_kernel<11, LOOP, MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           72 * 1024);
+                           PD_SMEM);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(place_downsweep_kernel<13, LOOP, MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           72 * 1024);
+                           PD_SMEM);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(place_upsweep_kernel<LOOP, MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(MAX_TILES * 4));
