@@ -194,7 +194,10 @@ def use_all_cores() -> int:
 # R32-R34: t_i = shutter ((i + 0.5)/K - 0.5); sample pose i
 # rotates the camera about its centre by the world-frame axis-angle vector
 # w t_i and moves the centre by v t_i; uniform 1/K average of the linear
-# colours (and alphas); depth from sample floor(K/2).
+# colours (and alphas); depth from the centre sample, i.e. the nominal pose
+# t = 0 the offsets are centred on ("depth taken from the center
+# sample", "offsets centered on the nominal pose") = the caller's
+# view matrix, for odd and even K alike.
 
 def _rodrigues(rv):
     rv = np.asarray(rv, np.float64)
@@ -228,7 +231,7 @@ def blur_poses(viewmat, lin_vel, ang_vel, shutter: float, K: int) -> np.ndarray:
 class BlurResult:
     rgb: np.ndarray      # [H,W,3] f64 uniform average of the samples' linear colours
     rgb8: np.ndarray     # [H,W,3] u8
-    depth: np.ndarray    # [H,W] depth of sample floor(K/2)
+    depth: np.ndarray    # [H,W] depth of the nominal pose (t = 0)
     alpha: np.ndarray    # [H,W] average alpha
     exempt: np.ndarray   # [H,W] any sample's near-miss flag
     depth_alpha: np.ndarray   # [H,W] alpha of the depth's sample
@@ -244,8 +247,9 @@ def render_blur_env(scene: OracleScene, viewmat, intr, width: int, height: int, 
     rgb = np.mean([s.rgb for s in samples], axis=0)
     alpha = np.mean([s.alpha for s in samples], axis=0)
     rgb8 = np.rint(np.clip(rgb, 0.0, 1.0) * 255.0).astype(np.uint8)   # numpy rint = half-to-even
-    exempt = np.any([s.exempt for s in samples], axis=0)
-    return BlurResult(rgb, rgb8, samples[K // 2].depth, alpha, exempt, samples[K // 2].alpha, samples)
+    nominal = render_env(scene, np.asarray(viewmat, np.float32), intr, width, height, **kw)   # t = 0
+    exempt = np.any([s.exempt for s in samples] + [nominal.exempt], axis=0)
+    return BlurResult(rgb, rgb8, nominal.depth, alpha, exempt, nominal.alpha, samples)
 
 
 # ---------------------------------------------------------------- DinoV2 input

@@ -40,15 +40,15 @@ int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, uint32_t* blk
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s);
-void launch_blur_poses(int E, int K, const float* viewmats, const float* lin, const float* ang, float shutter,
-                       float* out, cudaStream_t s);
-void launch_blur_average(int ec, int e0, int K, size_t P, const float* srgb, const float* sdepth,
+void launch_blur_poses(int E, int K, int Kc, const float* viewmats, const float* lin, const float* ang,
+                       float shutter, float* out, cudaStream_t s);
+void launch_blur_average(int ec, int e0, int K, int Kc, int dk, size_t P, const float* srgb, const float* sdepth,
                          const float* salpha, int rgb_format, void* rgb, float* depth, float* alpha, cudaStream_t s);
 void launch_blur_expand(int ec, int K, const int32_t* ids, const float* intr, int32_t* ids_k, float* intr_k,
                         cudaStream_t s);
 void launch_tables_v(int ec, const uint32_t* vcnt, uint64_t* rbase, uint64_t vcap, uint32_t* ok, uint32_t* err,
                      cudaStream_t s);
-void launch_tables_k(int ec, const uint32_t* vcnt, const uint32_t* kcnt, uint64_t* kbase, uint32_t* blkbase,
+void launch_tables_k(int ec, const uint32_t* vcnt, const unsigned long long* kcnt, uint64_t* kbase, uint32_t* blkbase,
                      int sort_blk, uint64_t kcap, uint64_t nbcap, uint32_t* ok, uint32_t* err, cudaStream_t s);
 void launch_checksum(int E, int W, int H, const uint8_t* rgb8, const float* rgbf, const float* depth,
                      unsigned long long* out, cudaStream_t s);
@@ -69,6 +69,19 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+// Per-call workspace.  The sync path and the sync-free (GG_ASYNC) path own
+// separate sets: a CUDA graph captured over a GG_ASYNC render holds the
+// addresses of `aw`, which only gg_reserve_async (re)allocates, so a later
+// sync render that grows its own buffers never frees memory a graph uses.
+struct Work {
+  DevBuf envc, flags, blkcnt, vcnt, kcnt, rbase, kbase;
+  DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, rmask, dconic;
+  DevBuf sorted, ranges, counters, perm, groups, blkbase, blkenv, ghist, thist, qctr, okflag;
+  DevBuf* all() { return &envc; }
+  static constexpr int count = 29;
+};
+static_assert(sizeof(Work) == Work::count * sizeof(DevBuf), "Work::count");
+
 struct SceneSlot {
   DevScene d{};
   DevBuf pos_op, cov_a, cov_b, aux, qmax, sh;
@@ -76,6 +89,7 @@ struct SceneSlot {
 };
 
 constexpr int DEFAULT_CHUNK = 1024;
+constexpr int SCENE_TABLE_MIN = 4096;   // scene-table slots allocated up front
 
 }  // namespace
 
@@ -90,16 +104,16 @@ struct gg_context {
   DevBuf scene_table;
   int scene_table_cap = 0;
   int chunk = DEFAULT_CHUNK;
-  // workspace
-  DevBuf envc, errflag, flags, blkcnt, vcnt, kcnt, rbase, kbase;
-  DevBuf rec0, rec1, rec2, rect, zkey, gid, dk0, dv0, dk1, dv1, rmask;
-  DevBuf sorted, ranges, counters, valid_out, perm, groups, blkbase, blkenv, ghist, thist, qctr;
-  DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval, dconic;
+  // workspace: sync path (sw) and sync-free path (aw), see Work
+  Work sw, aw;
+  const DevBuf* last_counters = nullptr;   // counters buffer of the last render
+  DevBuf errflag, valid_out;
+  DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval;
   DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
   DevBuf blur_vm, blur_ids, blur_intr, blur_rgb, blur_depth, blur_alpha;   // gg_render_blur
   // pinned host mirrors
   uint32_t* h_vcnt = nullptr;
-  uint32_t* h_kcnt = nullptr;
+  uint64_t* h_kcnt = nullptr;
   uint64_t* h_rbase = nullptr;
   uint64_t* h_kbase = nullptr;
   uint32_t* h_err = nullptr;
@@ -183,19 +197,29 @@ bool ensure(gg_context* ctx, DevBuf& b, size_t bytes, cudaStream_t s) {
   return true;
 }
 
+// Pinned host mirrors of the per-chunk tables.  All-or-nothing: the new set
+// is allocated into temporaries and swapped in only when every allocation
+// succeeded, so a failure leaves the old (valid) set and h_cap untouched.
 bool ensure_host(gg_context* ctx, int n) {
   if (ctx->h_cap >= n) return true;
-  cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase); cudaFreeHost(ctx->h_kbase);
-  cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
-  int cap = std::max(n, 1024);
-  if (cudaMallocHost(&ctx->h_blkbase, (cap + 1) * 4) != cudaSuccess) return false;
-  if (cudaMallocHost(&ctx->h_ids, cap * 4) != cudaSuccess) return false;
-  if (cudaMallocHost(&ctx->h_perm, cap * 4) != cudaSuccess) return false;
-  if (cudaMallocHost(&ctx->h_groups, cap * sizeof(EnvGroup)) != cudaSuccess) return false;
-  if (cudaMallocHost(&ctx->h_vcnt, cap * 4) != cudaSuccess) return false;
-  if (cudaMallocHost(&ctx->h_kcnt, cap * 4) != cudaSuccess) return false;
-  if (cudaMallocHost(&ctx->h_rbase, cap * 8) != cudaSuccess) return false;
-  if (cudaMallocHost(&ctx->h_kbase, cap * 8) != cudaSuccess) return false;
+  cudaDeviceSynchronize();   // in-flight copy kernels may still read/write the old mirrors
+  const int cap = std::max(n, 1024);
+  void* p[8] = {};
+  const size_t sz[8] = {(size_t)(cap + 1) * 4, (size_t)cap * 4, (size_t)cap * 4, (size_t)cap * sizeof(EnvGroup),
+                        (size_t)cap * 4, (size_t)cap * 8, (size_t)cap * 8, (size_t)cap * 8};
+  for (int i = 0; i < 8; ++i) {
+    if (cudaMallocHost(&p[i], sz[i]) != cudaSuccess) {
+      cudaGetLastError();
+      for (int j = 0; j < i; ++j) cudaFreeHost(p[j]);
+      return false;
+    }
+  }
+  void** cur[8] = {(void**)&ctx->h_blkbase, (void**)&ctx->h_ids, (void**)&ctx->h_perm, (void**)&ctx->h_groups,
+                   (void**)&ctx->h_vcnt, (void**)&ctx->h_kcnt, (void**)&ctx->h_rbase, (void**)&ctx->h_kbase};
+  for (int i = 0; i < 8; ++i) {
+    if (*cur[i]) cudaFreeHost(*cur[i]);
+    *cur[i] = p[i];
+  }
   ctx->h_cap = cap;
   return true;
 }
@@ -294,13 +318,11 @@ gg_status gg_destroy(gg_context* ctx) {
     dev_free(ctx, sc.aux, s); dev_free(ctx, sc.qmax, s); dev_free(ctx, sc.sh, s);
   }
   for (auto& e : ctx->a_ev) cudaEventDestroy(e);
-  DevBuf* all[] = {&ctx->scene_table, &ctx->envc, &ctx->errflag, &ctx->okflag, &ctx->flags, &ctx->blkcnt, &ctx->vcnt,
-                   &ctx->kcnt, &ctx->rbase, &ctx->kbase, &ctx->rec0, &ctx->rec1, &ctx->rec2, &ctx->rect, &ctx->rmask,
-                   &ctx->zkey, &ctx->gid, &ctx->dk0, &ctx->dv0, &ctx->dk1, &ctx->dv1, &ctx->perm, &ctx->groups,
-                   &ctx->blkbase, &ctx->blkenv, &ctx->ghist, &ctx->thist, &ctx->qctr,
-                   &ctx->sorted, &ctx->ranges, &ctx->counters, &ctx->valid_out,
+  for (Work* w : {&ctx->sw, &ctx->aw})
+    for (int i = 0; i < Work::count; ++i) dev_free(ctx, w->all()[i], s);
+  DevBuf* all[] = {&ctx->scene_table, &ctx->errflag, &ctx->valid_out,
                    &ctx->dbg_tc, &ctx->dbg_proj, &ctx->dbg_stile, &ctx->dbg_sz, &ctx->dbg_sgid,
-                   &ctx->dbg_neval, &ctx->dconic, &ctx->h_in, &ctx->blur_vm, &ctx->blur_ids,
+                   &ctx->dbg_neval, &ctx->h_in, &ctx->blur_vm, &ctx->blur_ids,
                    &ctx->blur_intr, &ctx->blur_rgb, &ctx->blur_depth, &ctx->blur_alpha};
   for (DevBuf* b : all) dev_free(ctx, *b, s);
   cudaStreamSynchronize(s);
@@ -321,8 +343,13 @@ static gg_status upload_scene_table(gg_context* ctx) {
     h[i] = ctx->scenes[i].d;
     h[i].valid = ctx->scenes[i].live ? 1 : 0;
   }
-  if (!ensure(ctx, ctx->scene_table, sizeof(DevScene) * std::max(n, 1), ctx->own))
+  // capacity for SCENE_TABLE_MIN scenes up front: the table normally never
+  // moves, so CUDA graphs captured over GG_ASYNC renders stay valid across
+  // later gg_load_scene / gg_unload_scene calls (the table is read at replay)
+  const void* before = ctx->scene_table.p;
+  if (!ensure(ctx, ctx->scene_table, sizeof(DevScene) * std::max(n, SCENE_TABLE_MIN), ctx->own))
     return fail(ctx, GG_E_OOM, "scene table alloc");
+  if (before && before != ctx->scene_table.p) ctx->async_ready = false;   // graphs over the old table are stale
   CK(cudaMemcpyAsync(ctx->scene_table.p, h.data(), sizeof(DevScene) * n, cudaMemcpyHostToDevice, ctx->own));
   CK(cudaStreamSynchronize(ctx->own));
   return GG_OK;
@@ -445,12 +472,12 @@ gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t W, int32_t H, in
   const int nmax = std::max(max_scene_n(ctx), 1);
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   const int ntiles = ((W + TILE - 1) / TILE) * ((H + TILE - 1) / TILE);
-  bool ok = ensure(ctx, ctx->envc, sizeof(EnvConst) * max_envs, s) &&
-            ensure(ctx, ctx->flags, (size_t)ec * nblk * PROJ_WPB * 4, s) &&
-            ensure(ctx, ctx->blkcnt, (size_t)ec * nblk * 4, s) && ensure(ctx, ctx->vcnt, ec * 4, s) &&
-            ensure(ctx, ctx->kcnt, ec * 4, s) && ensure(ctx, ctx->rbase, ec * 8, s) &&
-            ensure(ctx, ctx->kbase, ec * 8, s) && ensure(ctx, ctx->ranges, (size_t)ec * ntiles * 8, s) &&
-            ensure(ctx, ctx->counters, (size_t)max_envs * 32, s) && ensure_host(ctx, ec);
+  bool ok = ensure(ctx, ctx->sw.envc, sizeof(EnvConst) * max_envs, s) &&
+            ensure(ctx, ctx->sw.flags, (size_t)ec * nblk * PROJ_WPB * 4, s) &&
+            ensure(ctx, ctx->sw.blkcnt, (size_t)ec * nblk * 4, s) && ensure(ctx, ctx->sw.vcnt, ec * 4, s) &&
+            ensure(ctx, ctx->sw.kcnt, ec * 8, s) && ensure(ctx, ctx->sw.rbase, ec * 8, s) &&
+            ensure(ctx, ctx->sw.kbase, ec * 8, s) && ensure(ctx, ctx->sw.ranges, (size_t)ec * ntiles * 8, s) &&
+            ensure(ctx, ctx->sw.counters, (size_t)max_envs * 32, s) && ensure_host(ctx, ec);
   CK(cudaStreamSynchronize(s));
   return ok ? GG_OK : fail(ctx, GG_E_OOM, "gg_reserve: allocation failed");
 }
@@ -531,15 +558,18 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   const int nwords = nblk * (PROJ_BLOCK / 32);
   const int chunk = std::min(E, ctx->chunk);
 
-  if (!ensure(ctx, ctx->envc, sizeof(EnvConst) * E, s) || !ensure(ctx, ctx->perm, (size_t)E * 4, s) ||
-      !ensure(ctx, ctx->groups, sizeof(EnvGroup) * (size_t)chunk, s) ||
-      !ensure(ctx, ctx->flags, (size_t)chunk * nwords * 4, s) ||
-      !ensure(ctx, ctx->blkcnt, (size_t)chunk * nblk * 4, s) || !ensure(ctx, ctx->vcnt, chunk * 4, s) ||
-      !ensure(ctx, ctx->kcnt, chunk * 4, s) || !ensure(ctx, ctx->rbase, chunk * 8, s) ||
-      !ensure(ctx, ctx->kbase, chunk * 8, s) || !ensure(ctx, ctx->ranges, (size_t)chunk * ntiles * 8, s) ||
-      !ensure_host(ctx, std::max(E, chunk)) || (counters && !ensure(ctx, ctx->counters, (size_t)E * 32, s)))
+  if (!ensure(ctx, ctx->sw.envc, sizeof(EnvConst) * E, s) || !ensure(ctx, ctx->sw.perm, (size_t)E * 4, s) ||
+      !ensure(ctx, ctx->sw.groups, sizeof(EnvGroup) * (size_t)chunk, s) ||
+      !ensure(ctx, ctx->sw.flags, (size_t)chunk * nwords * 4, s) ||
+      !ensure(ctx, ctx->sw.blkcnt, (size_t)chunk * nblk * 4, s) || !ensure(ctx, ctx->sw.vcnt, chunk * 4, s) ||
+      !ensure(ctx, ctx->sw.kcnt, chunk * 8, s) || !ensure(ctx, ctx->sw.rbase, chunk * 8, s) ||
+      !ensure(ctx, ctx->sw.kbase, chunk * 8, s) || !ensure(ctx, ctx->sw.ranges, (size_t)chunk * ntiles * 8, s) ||
+      !ensure_host(ctx, std::max(E, chunk)) || (counters && !ensure(ctx, ctx->sw.counters, (size_t)E * 32, s)))
     return fail(ctx, GG_E_OOM, "gg_render: workspace allocation failed");
-  if (counters) CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)E * 32, s));
+  if (counters) {
+    CK(cudaMemsetAsync(ctx->sw.counters.p, 0, (size_t)E * 32, s));
+    ctx->last_counters = &ctx->sw.counters;
+  }
   CK(cudaMemsetAsync(ctx->errflag.p, 0, 4, s));
 
   // Scene-sorted env order (stable): envs bound to one scene become
@@ -561,12 +591,12 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ctx->h_perm[p] = order[p];
     if (keep && order[p] == opts.debug_env) dbg_pos = p;
   }
-  ctx->launches += launch_copy_words(ctx->perm.p, ctx->h_perm, (size_t)E * 4, s);
-  launch_setup_envs(E, P<int32_t>(ctx->perm), scene_ids, viewmats, intr, P<DevScene>(ctx->scene_table), nsc, W, H,
-                    opts.sh_degree, P<EnvConst>(ctx->envc), P<uint32_t>(ctx->errflag), s);
+  ctx->launches += launch_copy_words(ctx->sw.perm.p, ctx->h_perm, (size_t)E * 4, s);
+  launch_setup_envs(E, P<int32_t>(ctx->sw.perm), scene_ids, viewmats, intr, P<DevScene>(ctx->scene_table), nsc, W, H,
+                    opts.sh_degree, P<EnvConst>(ctx->sw.envc), P<uint32_t>(ctx->errflag), s);
   ctx->launches++;
   CK(cudaGetLastError());
-  if (keep && !ensure(ctx, ctx->gid, 16, s)) return fail(ctx, GG_E_OOM, "alloc");
+  if (keep && !ensure(ctx, ctx->sw.gid, 16, s)) return fail(ctx, GG_E_OOM, "alloc");
 
   float ms[3] = {0, 0, 0};
   for (int e0 = 0, ec = 0; e0 < E; e0 += ec) {
@@ -593,23 +623,23 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       }
       i = j;
     }
-    ctx->launches += launch_copy_words(ctx->groups.p, ctx->h_groups, sizeof(EnvGroup) * ngroups, s);
+    ctx->launches += launch_copy_words(ctx->sw.groups.p, ctx->h_groups, sizeof(EnvGroup) * ngroups, s);
     ChunkWS ws{};
-    ws.flags = P<uint32_t>(ctx->flags);
-    ws.blkcnt = P<uint32_t>(ctx->blkcnt);
-    ws.vcnt = P<uint32_t>(ctx->vcnt);
-    ws.kcnt = P<uint32_t>(ctx->kcnt);
-    ws.rec_base = P<uint64_t>(ctx->rbase);
-    ws.k_base = P<uint64_t>(ctx->kbase);
-    ws.ranges = P<uint2>(ctx->ranges);
+    ws.flags = P<uint32_t>(ctx->sw.flags);
+    ws.blkcnt = P<uint32_t>(ctx->sw.blkcnt);
+    ws.vcnt = P<uint32_t>(ctx->sw.vcnt);
+    ws.kcnt = P<unsigned long long>(ctx->sw.kcnt);
+    ws.rec_base = P<uint64_t>(ctx->sw.rbase);
+    ws.k_base = P<uint64_t>(ctx->sw.kbase);
+    ws.ranges = P<uint2>(ctx->sw.ranges);
     ws.zbase = f32_bits(opts.near_plane);
     ws.nwords = nwords;
     ws.nblk = nblk;
     ws.ec = ec;
-    const EnvGroup* groups = P<EnvGroup>(ctx->groups);
+    const EnvGroup* groups = P<EnvGroup>(ctx->sw.groups);
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], s));
     // K1a + K2
-    launch_cull_count(e0, ngroups, nblk, groups, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
+    launch_cull_count(e0, ngroups, nblk, groups, P<EnvConst>(ctx->sw.envc), P<DevScene>(ctx->scene_table), rp, ws, s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
     ctx->launches += 2;
     CK(cudaGetLastError());
@@ -617,52 +647,54 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     CK(cudaStreamSynchronize(s));
     uint64_t V = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_rbase[i] = V; V += ctx->h_vcnt[i]; }
-    if (!ensure(ctx, ctx->rec0, V * 16, s) || !ensure(ctx, ctx->rec1, V * 16, s) ||
-        !ensure(ctx, ctx->rec2, V * 16, s) || !ensure(ctx, ctx->rect, V * 8, s) ||
-        !ensure(ctx, ctx->zkey, V * 4, s) || (keep && !ensure(ctx, ctx->gid, V * 4, s)) ||
-        (rp.ellipse && !ensure(ctx, ctx->rmask, V * 4 + 4, s)) ||
-        (keep && !ensure(ctx, ctx->dconic, V * 16, s)) ||
-        !ensure(ctx, ctx->dk0, V * 8, s) || !ensure(ctx, ctx->dk1, V * 8, s) ||
-        !ensure(ctx, ctx->dv0, V * 4, s))
+    if (!ensure(ctx, ctx->sw.rec0, V * 16, s) || !ensure(ctx, ctx->sw.rec1, V * 16, s) ||
+        !ensure(ctx, ctx->sw.rec2, V * 16, s) || !ensure(ctx, ctx->sw.rect, V * 8, s) ||
+        !ensure(ctx, ctx->sw.zkey, V * 4, s) || (keep && !ensure(ctx, ctx->sw.gid, V * 4, s)) ||
+        (rp.ellipse && !ensure(ctx, ctx->sw.rmask, V * 4 + 4, s)) ||
+        (keep && !ensure(ctx, ctx->sw.dconic, V * 16, s)) ||
+        !ensure(ctx, ctx->sw.dk0, V * 8, s) || !ensure(ctx, ctx->sw.dk1, V * 8, s) ||
+        !ensure(ctx, ctx->sw.dv0, V * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: record workspace (%llu records) allocation failed",
                   (unsigned long long)V);
-    ctx->launches += launch_copy_words(ctx->rbase.p, ctx->h_rbase, ec * 8, s);
-    CK(cudaMemsetAsync(ws.kcnt, 0, ec * 4, s));
-    ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
-    ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
-    ws.rmask = rp.ellipse ? P<uint32_t>(ctx->rmask) : nullptr;
-    ws.gid = keep ? P<uint32_t>(ctx->gid) : nullptr;
-    ws.dconic = keep ? P<float4>(ctx->dconic) : nullptr;
-    ws.dp0 = P<uint64_t>(ctx->dk0); ws.dp1 = P<uint64_t>(ctx->dk1); ws.order = P<uint32_t>(ctx->dv0);
+    ctx->launches += launch_copy_words(ctx->sw.rbase.p, ctx->h_rbase, ec * 8, s);
+    CK(cudaMemsetAsync(ws.kcnt, 0, ec * 8, s));
+    ws.rec0 = P<float4>(ctx->sw.rec0); ws.rec1 = P<float4>(ctx->sw.rec1); ws.rec2 = P<float4>(ctx->sw.rec2);
+    ws.rect = P<uint2>(ctx->sw.rect); ws.zkey = P<uint32_t>(ctx->sw.zkey);
+    ws.rmask = rp.ellipse ? P<uint32_t>(ctx->sw.rmask) : nullptr;
+    ws.gid = keep ? P<uint32_t>(ctx->sw.gid) : nullptr;
+    ws.dconic = keep ? P<float4>(ctx->sw.dconic) : nullptr;
+    ws.dp0 = P<uint64_t>(ctx->sw.dk0); ws.dp1 = P<uint64_t>(ctx->sw.dk1); ws.order = P<uint32_t>(ctx->sw.dv0);
     // K1b
-    launch_project(e0, ngroups, nblk, max_deg, groups, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp,
+    launch_project(e0, ngroups, nblk, max_deg, groups, P<EnvConst>(ctx->sw.envc), P<DevScene>(ctx->scene_table), rp,
                    ws, s);
     ctx->launches++;
     CK(cudaGetLastError());
-    ctx->launches += launch_copy_words(ctx->h_kcnt, ws.kcnt, ec * 4, s);
+    ctx->launches += launch_copy_words(ctx->h_kcnt, ws.kcnt, ec * 8, s);
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], s));
     CK(cudaStreamSynchronize(s));
     uint64_t K = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_kbase[i] = K; K += ctx->h_kcnt[i]; }
     for (int i = 0; i < ec; ++i)
-      if (ctx->h_kcnt[i] >= 0xfffffff0u) return fail(ctx, GG_E_CAPACITY, "gg_render: env key overflow");
-    if (!ensure(ctx, ctx->sorted, K * 4, s))
+      if (ctx->h_kcnt[i] > 0xffffffffull)
+        return fail(ctx, GG_E_CAPACITY, "gg_render: env %d has %llu tile keys (>= 2^32)", ctx->h_perm[e0 + i],
+                    (unsigned long long)ctx->h_kcnt[i]);
+    if (!ensure(ctx, ctx->sw.sorted, K * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: key workspace (%llu keys) allocation failed", (unsigned long long)K);
-    ctx->launches += launch_copy_words(ctx->kbase.p, ctx->h_kbase, ec * 8, s);
-    ws.sorted = P<uint32_t>(ctx->sorted);
+    ctx->launches += launch_copy_words(ctx->sw.kbase.p, ctx->h_kbase, ec * 8, s);
+    ws.sorted = P<uint32_t>(ctx->sw.sorted);
     // K3-K5: sort blocks of sort_block_size() records, never straddling an env
     uint32_t nb = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_blkbase[i] = nb; nb += sort_blocks(ctx->h_vcnt[i]); }
     ctx->h_blkbase[ec] = nb;
     const int passes = depth_passes_for(opts.near_plane, opts.far_plane);
-    if (!ensure(ctx, ctx->blkbase, (size_t)(ec + 1) * 4, s) || !ensure(ctx, ctx->blkenv, (size_t)nb * 4 + 4, s) ||
-        !ensure(ctx, ctx->ghist, (size_t)nb * sort_ghist_words() * 4, s) ||
-        !ensure(ctx, ctx->thist, (size_t)nb * ntiles * 4, s))
+    if (!ensure(ctx, ctx->sw.blkbase, (size_t)(ec + 1) * 4, s) || !ensure(ctx, ctx->sw.blkenv, (size_t)nb * 4 + 4, s) ||
+        !ensure(ctx, ctx->sw.ghist, (size_t)nb * sort_ghist_words() * 4, s) ||
+        !ensure(ctx, ctx->sw.thist, (size_t)nb * ntiles * 4, s))
       return fail(ctx, GG_E_OOM, "gg_render: sort workspace allocation failed");
-    ctx->launches += launch_copy_words(ctx->blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, s);
-    ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->blkbase), P<uint32_t>(ctx->blkenv), passes, rp, ws,
-                                     P<uint32_t>(ctx->ghist),
-                                     P<uint32_t>(ctx->thist), s, false, nullptr);
+    ctx->launches += launch_copy_words(ctx->sw.blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, s);
+    ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->sw.blkbase), P<uint32_t>(ctx->sw.blkenv), passes, rp, ws,
+                                     P<uint32_t>(ctx->sw.ghist),
+                                     P<uint32_t>(ctx->sw.thist), s, false, nullptr);
     CK(cudaGetLastError());
     if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], s));
     // K6
@@ -684,8 +716,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
         wss.vcnt = ws.vcnt + s0;
         wss.kcnt = ws.kcnt + s0;
         const int dl = (dbg_eloc >= s0 && dbg_eloc < s0 + n) ? dbg_eloc - s0 : -1;
-        launch_raster(e0 + s0, n, P<EnvConst>(ctx->envc), rp, wss, rgb, depth, alpha, counters,
-                      counters ? P<unsigned long long>(ctx->counters) : nullptr, dl >= 0 ? dbg_neval : nullptr, dl,
+        launch_raster(e0 + s0, n, P<EnvConst>(ctx->sw.envc), rp, wss, rgb, depth, alpha, counters,
+                      counters ? P<unsigned long long>(ctx->sw.counters) : nullptr, dl >= 0 ? dbg_neval : nullptr, dl,
                       s);
         ctx->launches++;
         CK(cudaGetLastError());
@@ -693,8 +725,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
         if (cs != GG_OK) return cs;
       }
     } else {
-      launch_raster(e0, ec, P<EnvConst>(ctx->envc), rp, ws, rgb, depth, alpha, counters,
-                    counters ? P<unsigned long long>(ctx->counters) : nullptr, dbg_neval, dbg_eloc, s);
+      launch_raster(e0, ec, P<EnvConst>(ctx->sw.envc), rp, ws, rgb, depth, alpha, counters,
+                    counters ? P<unsigned long long>(ctx->sw.counters) : nullptr, dbg_neval, dbg_eloc, s);
       ctx->launches++;
       CK(cudaGetLastError());
     }
@@ -709,7 +741,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     }
     if (dbg_eloc >= 0) {
       // K8: snapshot the debug env's integer artefacts to host
-      const uint32_t Vd = ctx->h_vcnt[dbg_eloc], Kd = ctx->h_kcnt[dbg_eloc];
+      const uint32_t Vd = ctx->h_vcnt[dbg_eloc], Kd = (uint32_t)ctx->h_kcnt[dbg_eloc];
       const uint64_t rb = ctx->h_rbase[dbg_eloc], kb = ctx->h_kbase[dbg_eloc];
       const int n_all = nmax;
       if (!ensure(ctx, ctx->dbg_tc, (size_t)n_all * 4, s) || !ensure(ctx, ctx->dbg_proj, (size_t)n_all * 64, s) ||
@@ -724,7 +756,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       ctx->launches += 2;
       CK(cudaGetLastError());
       EnvConst hc;
-      CK(cudaMemcpyAsync(&hc, P<EnvConst>(ctx->envc) + dbg_pos, sizeof hc, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(&hc, P<EnvConst>(ctx->sw.envc) + dbg_pos, sizeof hc, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       const int nn = std::max(hc.n, 0);
       ctx->d_tc.resize(nn); ctx->d_proj.resize((size_t)nn * 16);
@@ -741,7 +773,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       ctx->d_counters[3] = Kd;
       if (counters) {
         unsigned long long c2[2];
-        CK(cudaMemcpy(c2, P<unsigned long long>(ctx->counters) + (size_t)opts.debug_env * 4, 16,
+        CK(cudaMemcpy(c2, P<unsigned long long>(ctx->sw.counters) + (size_t)opts.debug_env * 4, 16,
                       cudaMemcpyDeviceToHost));
         ctx->d_counters[0] = (int64_t)c2[0];
         ctx->d_counters[1] = (int64_t)c2[1];
@@ -773,12 +805,12 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
 static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
                               const float* intr, int32_t W, int32_t H, const gg_render_opts& opts, void* rgb,
                               float* depth, float* alpha, cudaStream_t s) {
-  if (!ctx->async_ready) return fail(ctx, GG_E_INVALID, "GG_ASYNC: call gg_reserve_async first");
+  if (!ctx->async_ready) return fail(ctx, GG_E_INVALID, "GG_ASYNC: call gg_reserve_async first (again after the scene table moved)");
   if (E > ctx->a_max_envs || W != ctx->a_W || H != ctx->a_H)
     return fail(ctx, GG_E_CAPACITY, "GG_ASYNC: render (%d envs, %dx%d) exceeds the reservation (%d, %dx%d)", E, W, H,
                 ctx->a_max_envs, ctx->a_W, ctx->a_H);
   if (opts.flags & GG_KEEP_INTERMEDIATES) return fail(ctx, GG_E_UNSUPPORTED, "GG_ASYNC: no intermediates");
-  if ((opts.flags & GG_COUNTERS) && ctx->counters.bytes < (size_t)E * 32)
+  if ((opts.flags & GG_COUNTERS) && ctx->aw.counters.bytes < (size_t)E * 32)
     return fail(ctx, GG_E_CAPACITY, "GG_ASYNC: counters not reserved");
   const int TX = (W + TILE - 1) / TILE, TY = (H + TILE - 1) / TILE;
   RenderParams rp;
@@ -795,10 +827,13 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     return fail(ctx, GG_E_CAPACITY, "GG_ASYNC: a scene larger than at gg_reserve_async time was loaded");
   const int passes = depth_passes_for(opts.near_plane, opts.far_plane);
   uint32_t* err = P<uint32_t>(ctx->errflag);
-  uint32_t* ok = P<uint32_t>(ctx->okflag);
-  if (counters) CK(cudaMemsetAsync(ctx->counters.p, 0, (size_t)E * 32, s));
+  uint32_t* ok = P<uint32_t>(ctx->aw.okflag);
+  if (counters) {
+    CK(cudaMemsetAsync(ctx->aw.counters.p, 0, (size_t)E * 32, s));
+    ctx->last_counters = &ctx->aw.counters;
+  }
   launch_setup_envs(E, nullptr, scene_ids, viewmats, intr, P<DevScene>(ctx->scene_table), (int)ctx->scenes.size(), W,
-                    H, opts.sh_degree, P<EnvConst>(ctx->envc), err, s);
+                    H, opts.sh_degree, P<EnvConst>(ctx->aw.envc), err, s);
   ctx->launches++;
   const int nchunks = (E + chunk - 1) / chunk;
   if (ctx->timing) {
@@ -812,42 +847,42 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     const int e0 = c * chunk, ec = std::min(chunk, E - e0);
     const int ngroups = (ec + ENV_GROUP - 1) / ENV_GROUP;
     ChunkWS ws{};
-    ws.flags = P<uint32_t>(ctx->flags);
-    ws.blkcnt = P<uint32_t>(ctx->blkcnt);
-    ws.vcnt = P<uint32_t>(ctx->vcnt);
-    ws.kcnt = P<uint32_t>(ctx->kcnt);
-    ws.rec_base = P<uint64_t>(ctx->rbase);
-    ws.k_base = P<uint64_t>(ctx->kbase);
-    ws.rec0 = P<float4>(ctx->rec0); ws.rec1 = P<float4>(ctx->rec1); ws.rec2 = P<float4>(ctx->rec2);
-    ws.rect = P<uint2>(ctx->rect); ws.zkey = P<uint32_t>(ctx->zkey);
-    ws.rmask = rp.ellipse ? P<uint32_t>(ctx->rmask) : nullptr;
+    ws.flags = P<uint32_t>(ctx->aw.flags);
+    ws.blkcnt = P<uint32_t>(ctx->aw.blkcnt);
+    ws.vcnt = P<uint32_t>(ctx->aw.vcnt);
+    ws.kcnt = P<unsigned long long>(ctx->aw.kcnt);
+    ws.rec_base = P<uint64_t>(ctx->aw.rbase);
+    ws.k_base = P<uint64_t>(ctx->aw.kbase);
+    ws.rec0 = P<float4>(ctx->aw.rec0); ws.rec1 = P<float4>(ctx->aw.rec1); ws.rec2 = P<float4>(ctx->aw.rec2);
+    ws.rect = P<uint2>(ctx->aw.rect); ws.zkey = P<uint32_t>(ctx->aw.zkey);
+    ws.rmask = rp.ellipse ? P<uint32_t>(ctx->aw.rmask) : nullptr;
     ws.zbase = f32_bits(opts.near_plane);
-    ws.dp0 = P<uint64_t>(ctx->dk0); ws.dp1 = P<uint64_t>(ctx->dk1); ws.order = P<uint32_t>(ctx->dv0);
-    ws.sorted = P<uint32_t>(ctx->sorted);
-    ws.ranges = P<uint2>(ctx->ranges);
+    ws.dp0 = P<uint64_t>(ctx->aw.dk0); ws.dp1 = P<uint64_t>(ctx->aw.dk1); ws.order = P<uint32_t>(ctx->aw.dv0);
+    ws.sorted = P<uint32_t>(ctx->aw.sorted);
+    ws.ranges = P<uint2>(ctx->aw.ranges);
     ws.ok = ok;
     ws.nwords = nwords;
     ws.nblk = nblk;
     ws.ec = ec;
     if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 0], s));
-    CK(cudaMemsetAsync(ws.kcnt, 0, ec * 4, s));
+    CK(cudaMemsetAsync(ws.kcnt, 0, ec * 8, s));
     CK(cudaMemsetAsync(ok, 0x01, 4, s));
-    launch_cull_count(e0, ngroups, nblk, nullptr, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table), rp, ws, s);
+    launch_cull_count(e0, ngroups, nblk, nullptr, P<EnvConst>(ctx->aw.envc), P<DevScene>(ctx->scene_table), rp, ws, s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
-    launch_tables_v(ec, ws.vcnt, P<uint64_t>(ctx->rbase), ctx->a_vcap, ok, err, s);
-    launch_project(e0, ngroups, nblk, ctx->a_maxdeg, nullptr, P<EnvConst>(ctx->envc), P<DevScene>(ctx->scene_table),
+    launch_tables_v(ec, ws.vcnt, P<uint64_t>(ctx->aw.rbase), ctx->a_vcap, ok, err, s);
+    launch_project(e0, ngroups, nblk, ctx->a_maxdeg, nullptr, P<EnvConst>(ctx->aw.envc), P<DevScene>(ctx->scene_table),
                    rp, ws, s);
-    launch_tables_k(ec, ws.vcnt, ws.kcnt, P<uint64_t>(ctx->kbase), P<uint32_t>(ctx->blkbase), sort_block_size(),
+    launch_tables_k(ec, ws.vcnt, ws.kcnt, P<uint64_t>(ctx->aw.kbase), P<uint32_t>(ctx->aw.blkbase), sort_block_size(),
                     ctx->a_kcap, ctx->a_nbcap, ok, err, s);
     ctx->launches += 5;
     if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 1], s));
-    ctx->launches += launch_sort_bin(ec, (uint32_t)ctx->a_nbcap, P<uint32_t>(ctx->blkbase), P<uint32_t>(ctx->blkenv),
+    ctx->launches += launch_sort_bin(ec, (uint32_t)ctx->a_nbcap, P<uint32_t>(ctx->aw.blkbase), P<uint32_t>(ctx->aw.blkenv),
                                      passes, rp, ws,
-                                     P<uint32_t>(ctx->ghist), P<uint32_t>(ctx->thist), s, true,
-                                     P<uint32_t>(ctx->qctr));
+                                     P<uint32_t>(ctx->aw.ghist), P<uint32_t>(ctx->aw.thist), s, true,
+                                     P<uint32_t>(ctx->aw.qctr));
     if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 2], s));
-    launch_raster(e0, ec, P<EnvConst>(ctx->envc), rp, ws, rgb, depth, alpha, counters,
-                  counters ? P<unsigned long long>(ctx->counters) : nullptr, nullptr, -1, s);
+    launch_raster(e0, ec, P<EnvConst>(ctx->aw.envc), rp, ws, rgb, depth, alpha, counters,
+                  counters ? P<unsigned long long>(ctx->aw.counters) : nullptr, nullptr, -1, s);
     ctx->launches++;
     if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 3], s));
     CK(cudaGetLastError());
@@ -877,21 +912,21 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
   const uint64_t vcap = (uint64_t)((double)ch * nmax * max_visible_frac) + 1;
   const uint64_t kcap = (uint64_t)((double)vcap * keys_per_visible) + 1;
   const uint64_t nbcap = vcap / (uint64_t)sort_block_size() + ch + 1;
-  bool okb = ensure(ctx, ctx->envc, sizeof(EnvConst) * max_envs, s) &&
-             ensure(ctx, ctx->flags, (size_t)ch * nblk * PROJ_WPB * 4, s) && ensure(ctx, ctx->blkcnt, (size_t)ch * nblk * 4, s) &&
-             ensure(ctx, ctx->vcnt, ch * 4, s) && ensure(ctx, ctx->kcnt, ch * 4, s) && ensure(ctx, ctx->rbase, ch * 8, s) &&
-             ensure(ctx, ctx->kbase, ch * 8, s) &&
-             ensure(ctx, ctx->ranges, (size_t)ch * ntiles * 8, s) && ensure(ctx, ctx->okflag, 16, s) &&
-             ensure(ctx, ctx->counters, (size_t)max_envs * 32, s) && ensure(ctx, ctx->rec0, vcap * 16, s) &&
-             ensure(ctx, ctx->rec1, vcap * 16, s) && ensure(ctx, ctx->rec2, vcap * 16, s) &&
-             ensure(ctx, ctx->rect, vcap * 8, s) && ensure(ctx, ctx->zkey, vcap * 4, s) &&
-             ensure(ctx, ctx->rmask, vcap * 4 + 4, s) &&
-             ensure(ctx, ctx->dk0, vcap * 8, s) && ensure(ctx, ctx->dk1, vcap * 8, s) &&
-             ensure(ctx, ctx->dv0, vcap * 4, s) &&
-             ensure(ctx, ctx->sorted, kcap * 4, s) && ensure(ctx, ctx->blkbase, (size_t)(ch + 1) * 4, s) &&
-             ensure(ctx, ctx->blkenv, nbcap * 4 + 4, s) && ensure(ctx, ctx->qctr, 64 * 4, s) &&
-             ensure(ctx, ctx->ghist, nbcap * sort_ghist_words() * 4, s) &&
-             ensure(ctx, ctx->thist, nbcap * ntiles * 4, s);
+  bool okb = ensure(ctx, ctx->aw.envc, sizeof(EnvConst) * max_envs, s) &&
+             ensure(ctx, ctx->aw.flags, (size_t)ch * nblk * PROJ_WPB * 4, s) && ensure(ctx, ctx->aw.blkcnt, (size_t)ch * nblk * 4, s) &&
+             ensure(ctx, ctx->aw.vcnt, ch * 4, s) && ensure(ctx, ctx->aw.kcnt, ch * 8, s) && ensure(ctx, ctx->aw.rbase, ch * 8, s) &&
+             ensure(ctx, ctx->aw.kbase, ch * 8, s) &&
+             ensure(ctx, ctx->aw.ranges, (size_t)ch * ntiles * 8, s) && ensure(ctx, ctx->aw.okflag, 16, s) &&
+             ensure(ctx, ctx->aw.counters, (size_t)max_envs * 32, s) && ensure(ctx, ctx->aw.rec0, vcap * 16, s) &&
+             ensure(ctx, ctx->aw.rec1, vcap * 16, s) && ensure(ctx, ctx->aw.rec2, vcap * 16, s) &&
+             ensure(ctx, ctx->aw.rect, vcap * 8, s) && ensure(ctx, ctx->aw.zkey, vcap * 4, s) &&
+             ensure(ctx, ctx->aw.rmask, vcap * 4 + 4, s) &&
+             ensure(ctx, ctx->aw.dk0, vcap * 8, s) && ensure(ctx, ctx->aw.dk1, vcap * 8, s) &&
+             ensure(ctx, ctx->aw.dv0, vcap * 4, s) &&
+             ensure(ctx, ctx->aw.sorted, kcap * 4, s) && ensure(ctx, ctx->aw.blkbase, (size_t)(ch + 1) * 4, s) &&
+             ensure(ctx, ctx->aw.blkenv, nbcap * 4 + 4, s) && ensure(ctx, ctx->aw.qctr, 64 * 4, s) &&
+             ensure(ctx, ctx->aw.ghist, nbcap * sort_ghist_words() * 4, s) &&
+             ensure(ctx, ctx->aw.thist, nbcap * ntiles * 4, s);
   CK(cudaStreamSynchronize(s));
   if (!okb) return fail(ctx, GG_E_OOM, "gg_reserve_async: allocation failed (%llu records, %llu keys)",
                         (unsigned long long)vcap, (unsigned long long)kcap);
@@ -993,7 +1028,7 @@ gg_status gg_blur_poses(gg_context* ctx, int32_t E, const float* viewmats, const
   if (E <= 0 || K < 1 || K > 64 || !(shutter >= 0.f) || !viewmats || !lin || !ang || !out)
     return fail(ctx, GG_E_INVALID, "gg_blur_poses: bad arguments");
   CK(cudaSetDevice(ctx->device));
-  launch_blur_poses(E, K, viewmats, lin, ang, shutter, out, (cudaStream_t)stream);
+  launch_blur_poses(E, K, K, viewmats, lin, ang, shutter, out, (cudaStream_t)stream);
   ctx->launches++;
   CK(cudaGetLastError());
   return GG_OK;
@@ -1014,30 +1049,35 @@ gg_status gg_render_blur(gg_context* ctx, int32_t E, const int32_t* scene_ids, c
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
   const size_t npx = (size_t)W * H;
-  const int ecb = std::max(1, std::min(E, ctx->chunk / K));
-  const size_t nk = (size_t)ecb * K;
+  // Kc cameras per env: the K colour samples, plus the nominal pose (t = 0)
+  // for the depth when K is even (odd K: sample (K-1)/2 is at t = 0; R34)
+  const bool need_depth = depth != nullptr;
+  const int Kc = K + ((K % 2 == 0 && need_depth) ? 1 : 0);
+  const int dk = (K % 2 == 1) ? (K - 1) / 2 : K;
+  const int ecb = std::max(1, std::min(E, ctx->chunk / Kc));
+  const size_t nk = (size_t)ecb * Kc;
   if (!ensure(ctx, ctx->blur_vm, nk * 64, s) || !ensure(ctx, ctx->blur_ids, nk * 4, s) ||
       !ensure(ctx, ctx->blur_intr, nk * 16, s) || (rgb && !ensure(ctx, ctx->blur_rgb, nk * npx * 12, s)) ||
       (depth && !ensure(ctx, ctx->blur_depth, nk * npx * 4, s)) || (alpha && !ensure(ctx, ctx->blur_alpha, nk * npx * 4, s)))
     return fail(ctx, GG_E_OOM, "gg_render_blur: sample buffers");
   gg_render_opts sub = opts;
   sub.rgb_format = 1;   // linear f32 samples, averaged before quantisation
-  sub.flags = 0;
+  sub.flags = opts.flags & (GG_TIGHT_TILES | GG_ELLIPSE_TILES);   // tile-list variants apply per sample
   sub.debug_env = -1;
   for (int e0 = 0; e0 < E; e0 += ecb) {
     const int ec = std::min(ecb, E - e0);
-    launch_blur_poses(ec, K, viewmats + (size_t)e0 * 16, lin + (size_t)e0 * 3, ang + (size_t)e0 * 3, shutter,
+    launch_blur_poses(ec, K, Kc, viewmats + (size_t)e0 * 16, lin + (size_t)e0 * 3, ang + (size_t)e0 * 3, shutter,
                       P<float>(ctx->blur_vm), s);
-    launch_blur_expand(ec, K, scene_ids + e0, intr + (size_t)e0 * 4, P<int32_t>(ctx->blur_ids),
+    launch_blur_expand(ec, Kc, scene_ids + e0, intr + (size_t)e0 * 4, P<int32_t>(ctx->blur_ids),
                        P<float>(ctx->blur_intr), s);
     ctx->launches += 2;
     CK(cudaGetLastError());
-    gg_status st = render_impl(ctx, ec * K, P<int32_t>(ctx->blur_ids), P<float>(ctx->blur_vm),
+    gg_status st = render_impl(ctx, ec * Kc, P<int32_t>(ctx->blur_ids), P<float>(ctx->blur_vm),
                                P<float>(ctx->blur_intr), W, H, &sub, rgb ? ctx->blur_rgb.p : nullptr,
                                depth ? P<float>(ctx->blur_depth) : nullptr, alpha ? P<float>(ctx->blur_alpha) : nullptr,
                                s, nullptr, nullptr);
     if (st != GG_OK) return st;
-    launch_blur_average(ec, e0, K, npx, rgb ? P<float>(ctx->blur_rgb) : nullptr,
+    launch_blur_average(ec, e0, K, Kc, dk, npx, rgb ? P<float>(ctx->blur_rgb) : nullptr,
                         depth ? P<float>(ctx->blur_depth) : nullptr, alpha ? P<float>(ctx->blur_alpha) : nullptr,
                         opts.rgb_format, rgb, depth, alpha, s);
     ctx->launches++;
@@ -1086,11 +1126,12 @@ gg_status gg_check_errors(gg_context* ctx, void* stream) {
 
 gg_status gg_get_counters(gg_context* ctx, int32_t E, int64_t* dst) {
   if (!ctx || !dst || E <= 0) return GG_E_INVALID;
-  if (E > ctx->last_E || !ctx->counters.p || ctx->counters.bytes < (size_t)E * 32)
+  const DevBuf* cb = ctx->last_counters;
+  if (E > ctx->last_E || !cb || !cb->p || cb->bytes < (size_t)E * 32)
     return fail(ctx, GG_E_INVALID, "gg_get_counters: no counters for %d envs", E);
   CK(cudaSetDevice(ctx->device));
   CK(cudaDeviceSynchronize());
-  CK(cudaMemcpy(dst, ctx->counters.p, (size_t)E * 32, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(dst, cb->p, (size_t)E * 32, cudaMemcpyDeviceToHost));
   return GG_OK;
 }
 

@@ -60,14 +60,18 @@ tables_v_kernel(int ec, const uint32_t* __restrict__ vcnt, uint64_t* __restrict_
 
 // k_base = excl-scan(kcnt); blk_base = excl-scan(ceil(vcnt / sort_blk)) (ec+1 entries)
 __global__ void __launch_bounds__(TB_THREADS)
-tables_k_kernel(int ec, const uint32_t* __restrict__ vcnt, const uint32_t* __restrict__ kcnt,
+tables_k_kernel(int ec, const uint32_t* __restrict__ vcnt, const unsigned long long* __restrict__ kcnt,
                 uint64_t* __restrict__ kbase, uint32_t* __restrict__ blkbase, int sort_blk, uint64_t kcap,
                 uint64_t nbcap, uint32_t* ok, uint32_t* err) {
   __shared__ uint64_t wsum[32];
   uint64_t ck = 0, cb = 0;
+  __shared__ uint32_t wide;   // an env with >= 2^32 keys (u32 list offsets)
+  if (threadIdx.x == 0) wide = 0u;
+  __syncthreads();
   for (int base = 0; base < ec; base += TB_THREADS) {
     const int e = base + threadIdx.x;
     const uint64_t k = e < ec ? kcnt[e] : 0ull;
+    if (k > 0xffffffffull) wide = 1u;
     const uint64_t nb = e < ec ? (vcnt[e] + (uint64_t)sort_blk - 1) / (uint64_t)sort_blk : 0ull;
     uint64_t tk, tb;
     const uint64_t exk = ck + block_excl_scan64(k, wsum, &tk);
@@ -81,7 +85,7 @@ tables_k_kernel(int ec, const uint32_t* __restrict__ vcnt, const uint32_t* __res
   }
   if (threadIdx.x == 0) {
     blkbase[ec] = (uint32_t)(cb <= nbcap ? cb : nbcap);
-    if (ck > kcap || cb > nbcap) {
+    if (ck > kcap || cb > nbcap || wide) {
       *ok = 0u;
       atomicOr(err, (uint32_t)ERR_CAPACITY);
     }
@@ -93,7 +97,7 @@ void launch_tables_v(int ec, const uint32_t* vcnt, uint64_t* rbase, uint64_t vca
   tables_v_kernel<<<1, TB_THREADS, 0, s>>>(ec, vcnt, rbase, vcap, ok, err);
 }
 
-void launch_tables_k(int ec, const uint32_t* vcnt, const uint32_t* kcnt, uint64_t* kbase, uint32_t* blkbase,
+void launch_tables_k(int ec, const uint32_t* vcnt, const unsigned long long* kcnt, uint64_t* kbase, uint32_t* blkbase,
                      int sort_blk, uint64_t kcap, uint64_t nbcap, uint32_t* ok, uint32_t* err, cudaStream_t s) {
   tables_k_kernel<<<1, TB_THREADS, 0, s>>>(ec, vcnt, kcnt, kbase, blkbase, sort_blk, kcap, nbcap, ok, err);
 }

@@ -8,12 +8,16 @@ namespace gg {
 // rotated by the axis-angle vector w*t_i (Rodrigues), centre C = -Rcw^T t
 // moved by v*t_i.  Evaluated in f64 (a few hundred flops per env) so the f32
 // view matrices are reproducible by an independent f64 implementation.
-__global__ void blur_poses_kernel(int E, int K, const float* __restrict__ viewmats, const float* __restrict__ lin,
-                                  const float* __restrict__ ang, float shutter, float* __restrict__ out) {
+// Kc >= K poses per env: sample K (present when Kc > K) is the nominal pose
+// t = 0, the depth sample of an even K (R34).  At t = 0 the pose is the
+// input view matrix exactly (the translation-only branch subtracts R 0).
+__global__ void blur_poses_kernel(int E, int K, int Kc, const float* __restrict__ viewmats,
+                                  const float* __restrict__ lin, const float* __restrict__ ang, float shutter,
+                                  float* __restrict__ out) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= E * K) return;
-  const int e = idx / K, i = idx - e * K;
-  const double t = (double)shutter * (((double)i + 0.5) / (double)K - 0.5);
+  if (idx >= E * Kc) return;
+  const int e = idx / Kc, i = idx - e * Kc;
+  const double t = i >= K ? 0.0 : (double)shutter * (((double)i + 0.5) / (double)K - 0.5);
   const float* V = viewmats + (size_t)e * 16;
   double Rcw[3][3], tc[3];
   for (int r = 0; r < 3; ++r) {
@@ -52,16 +56,17 @@ __global__ void blur_poses_kernel(int E, int K, const float* __restrict__ viewma
   O[12] = 0.f; O[13] = 0.f; O[14] = 0.f; O[15] = 1.f;
 }
 
-// Average K consecutive f32 sample frames of each env (R34):
+// Average the K colour samples of each env (R34; frames e*Kc + i, i < K):
 // m = x0 + (sum_{i>=1} (x_i - x0)) / K, then u8 round-half-even or f32.
-__global__ void blur_average_kernel(int ec, int e0, int K, size_t P, const float* __restrict__ srgb,
+// Depth comes from the nominal-pose sample dk (t = 0).
+__global__ void blur_average_kernel(int ec, int e0, int K, int Kc, int dk, size_t P, const float* __restrict__ srgb,
                                     const float* __restrict__ sdepth, const float* __restrict__ salpha,
                                     int rgb_format, void* __restrict__ rgb, float* __restrict__ depth,
                                     float* __restrict__ alpha) {
   const size_t n = (size_t)ec * P;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
     const size_t e = q / P, p = q - e * P;
-    const size_t base = e * K * P + p;     // sample i of env e at frame e*K + i
+    const size_t base = e * Kc * P + p;    // sample i of env e at frame e*Kc + i
     const size_t out = (size_t)(e0 + e) * P + p;
     if (rgb) {
       for (int ch = 0; ch < 3; ++ch) {
@@ -81,7 +86,7 @@ __global__ void blur_average_kernel(int ec, int e0, int K, size_t P, const float
       for (int i = 1; i < K; ++i) s += salpha[base + (size_t)i * P] - a0;
       alpha[out] = a0 + s / (float)K;
     }
-    if (depth) depth[out] = sdepth[base + (size_t)(K / 2) * P];
+    if (depth) depth[out] = sdepth[base + (size_t)dk * P];
   }
 }
 
@@ -95,14 +100,15 @@ __global__ void blur_expand_kernel(int ec, int K, const int32_t* __restrict__ id
   for (int k = 0; k < 4; ++k) intr_k[idx * 4 + k] = intr[e * 4 + k];
 }
 
-void launch_blur_poses(int E, int K, const float* viewmats, const float* lin, const float* ang, float shutter,
-                       float* out, cudaStream_t s) {
-  blur_poses_kernel<<<(E * K + 127) / 128, 128, 0, s>>>(E, K, viewmats, lin, ang, shutter, out);
+void launch_blur_poses(int E, int K, int Kc, const float* viewmats, const float* lin, const float* ang,
+                       float shutter, float* out, cudaStream_t s) {
+  blur_poses_kernel<<<(E * Kc + 127) / 128, 128, 0, s>>>(E, K, Kc, viewmats, lin, ang, shutter, out);
 }
 
-void launch_blur_average(int ec, int e0, int K, size_t P, const float* srgb, const float* sdepth,
+void launch_blur_average(int ec, int e0, int K, int Kc, int dk, size_t P, const float* srgb, const float* sdepth,
                          const float* salpha, int rgb_format, void* rgb, float* depth, float* alpha, cudaStream_t s) {
-  blur_average_kernel<<<148 * 8, 256, 0, s>>>(ec, e0, K, P, srgb, sdepth, salpha, rgb_format, rgb, depth, alpha);
+  blur_average_kernel<<<148 * 8, 256, 0, s>>>(ec, e0, K, Kc, dk, P, srgb, sdepth, salpha, rgb_format, rgb, depth,
+                                               alpha);
 }
 
 void launch_blur_expand(int ec, int K, const int32_t* ids, const float* intr, int32_t* ids_k, float* intr_k,

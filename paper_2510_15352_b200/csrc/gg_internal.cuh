@@ -86,7 +86,7 @@ struct ChunkWS {
   uint32_t* flags;      // [Ec][nwords]
   uint32_t* blkcnt;     // [Ec][nblk] -> exclusive offsets in place
   uint32_t* vcnt;       // [Ec]
-  uint32_t* kcnt;       // [Ec]
+  unsigned long long* kcnt;   // [Ec] keys per env (64-bit: a per-env total >= 2^32 is detected, not wrapped)
   // records (global index = rec_base[e] + local)
   const uint64_t* rec_base;  // [Ec]
   const uint64_t* k_base;    // [Ec]

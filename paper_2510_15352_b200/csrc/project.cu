@@ -543,7 +543,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     if (ntiles) atomicAdd(&sm.kacc[k], ntiles);
   }
   __syncthreads();
-  if (tid < grp.cnt && sm.kacc[tid]) atomicAdd(&ws.kcnt[grp.elo + tid], sm.kacc[tid]);
+  if (tid < grp.cnt && sm.kacc[tid]) atomicAdd(&ws.kcnt[grp.elo + tid], (unsigned long long)sm.kacc[tid]);
 }
 
 cudaError_t project_init() { return cudaSuccess; }

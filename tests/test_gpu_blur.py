@@ -81,7 +81,7 @@ def test_static_cases_bit_exact(gg):
 
 def test_average_of_sample_renders_bit_exact(gg):
     """the K=4 blend equals the float mean of the four offset renders
-    (in the R34 order: m = x0 + ((x1-x0) + (x2-x0) + (x3-x0)) / 4), depth from sample 2."""
+    (in the R34 order: m = x0 + ((x1-x0) + (x2-x0) + (x3-x0)) / 4), depth from the nominal pose (t = 0)."""
     sc, cams, r, sid, lin, ang = _setup(gg)
     K, E = 4, cams.n
     poses = torch.zeros((E, K, 4, 4), device="cuda")
@@ -97,15 +97,17 @@ def test_average_of_sample_renders_bit_exact(gg):
                 acc = acc + (x[i] - x[0])
             m = x[0] + acc / np.float32(K)
             assert np.array_equal(out, m)
-        assert np.array_equal(dep_b[e], s_dep[K // 2])
         lo, hi = s_rgb.min(axis=0), s_rgb.max(axis=0)
         assert np.all(rgb_b[e] >= lo) and np.all(rgb_b[e] <= hi)    # convex combination
+    base = _plain(gg, r, sid, cams.viewmats, cams, fmt=1)
+    assert np.array_equal(dep_b, base[1])        # depth of the nominal pose t = 0, even K
     r.close()
 
 
-def test_blur_oracle_parity(gg):
+@pytest.mark.parametrize("K", [3, 4])
+def test_blur_oracle_parity(gg, K):
     sc, cams, r, sid, lin, ang = _setup(gg, seed=9, E=4)
-    K, shutter = 4, 0.02
+    shutter = 0.02
     rgb, dep, al = _blur(gg, r, sid, cams, lin, ang, shutter, K)
     osc = oracle.OracleScene.from_inputs(sc)
     t = Tally()

@@ -53,4 +53,8 @@ def test_blur_is_convex_combination_and_blurs():
     assert np.all(b.rgb >= lo - 1e-12) and np.all(b.rgb <= hi + 1e-12)
     base = oracle.render_env(osc, cams.viewmats[0], cams.intrinsics[0], 64, 64)
     assert np.abs(b.rgb - base.rgb).max() > 1e-3       # motion changes the image
-    assert np.array_equal(b.depth, b.samples[2].depth)  # depth from sample floor(K/2)
+    # depth from the nominal pose t = 0 ("center sample"), not from an offset sample of even K
+    assert np.array_equal(b.depth, base.depth)
+    assert not np.array_equal(b.depth, b.samples[2].depth)
+    b5 = oracle.render_blur_env(osc, cams.viewmats[0], cams.intrinsics[0], 64, 64, [2.0, 0, 0], [0, 0, 3.0], 0.05, 5)
+    assert np.array_equal(b5.depth, base.depth)
