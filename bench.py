@@ -33,10 +33,6 @@ import gg_inputs as gi  # noqa: E402
 METRIC = "rendered env-frames/sec at 640×480 RGB+depth, 1/2/4/8 B200 (vs roofline)"
 UNIT = "env-frames/s"
 
-# FP32 work per pixel-Gaussian pair of the definition:
-# flops with FFMA = 2, per evaluated pair and extra per blended pair.
-FLOP_EVAL = 14
-FLOP_CONTRIB = 14
 SM_COUNT = 148
 FP32_LANES = 128
 
@@ -73,33 +69,6 @@ def parse():
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo only to exercise the multi-rank path on a single-GPU box")
     return p.parse_args()
-
-
-def _room(args3):
-    k, n, d = args3
-    return gi.room_scene(100 + k, n, d)
-
-
-def make_scenes(args, c):
-    """The config's scene, or an iterator over S seeded rooms generated in parallel on the host (streamed: each
-    room is loaded onto the GPU and dropped, so c5's 2,500 rooms never sit in host memory at once)."""
-    S = c["n_scenes"]
-    if S == 1:
-        return [gi.config_scene(args.config, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])]
-    import concurrent.futures as cf
-    n_proc = max(1, min(16, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 4))
-    ex = cf.ProcessPoolExecutor(n_proc)
-    futs = [ex.submit(_room, (k, c["n_gauss"], c["sh_degree"])) for k in range(min(S, 2 * n_proc))]
-
-    def gen():
-        for k in range(S):
-            sc_ = futs[k].result()
-            futs[k] = None
-            if k + 2 * n_proc < S:
-                futs.append(ex.submit(_room, (k + 2 * n_proc, c["n_gauss"], c["sh_degree"])))
-            yield sc_
-        ex.shutdown()
-    return gen()
 
 
 def workload(args):
@@ -203,6 +172,114 @@ def oracle_sample(scene, cams, envs, sh_degree):
     return time.perf_counter() - t0, oracle.num_threads()
 
 
+# FP32 lane-operations (FFMA = 1) per pixel-Gaussian pair that compositing
+# (O4) executes, in the minimal form the timed kernel uses
+# (DESIGN.md §6): evaluating a pair = the exponent x = c0 + lx (c1 + A lx) +
+# ly (c2 + B lx + C ly) (5 FMA), the 0.99 cap (1 min) and the 1/255 cutoff
+# compare (1) = 7; blending it adds w = a T, T' = T - w, the stop compare,
+# 3 colour FFMA and 1 depth FFMA = 7 (the ex2 runs on MUFU, counted apart).
+OPS_EVAL = 7
+OPS_BLEND = 7
+OPS_BLEND_DEPTH_ONLY = 4
+OPS_CULL = 25           # per (env, Gaussian) candidate: SURVEY §8(d).2's conservative pre-test budget
+STAGES = ("cull", "project", "depth_sort", "placement", "raster")
+
+
+def alu_peak_measured(clock_mhz):
+    """FP32 lane-ops/s measured by tools/ubench/alu_peak (profiles/round2/alu_peak.json), scaled to the run's
+    SM clock; None if absent."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "round2", "alu_peak.json")))
+        best = max(d["ffma"]["lane_ops_per_s"] / d["ffma"]["sm_mhz_est"], d["ffma2"]["lane_ops_per_s"] / d["ffma2"]["sm_mhz_est"])
+        return {"lane_ops_per_s": best * clock_mhz, "ex2_per_s": d["ex2"]["lane_ops_per_s"] / d["ex2"]["sm_mhz_est"] * clock_mhz,
+                "source": "profiles/round2/alu_peak.json (FFMA / FFMA2 / MUFU.EX2 microbenchmark)"}
+    except Exception:
+        return None
+
+
+def roofline(args, c, E, W, H, S, scene, want_rgb, want_depth, stage_ms, clocks, kb, paper_counts, run_counts):
+    """The dominant kernel's roofline (bench JSON `roofline`) and every stage's (`roofline_path`).
+
+    Work is counted on what the timed render executes: the tile lists it walks (r_*: tight by default), the
+    records and keys it sorts.  The raster's count on the paper's 3-sigma lists is reported beside it."""
+    n_eval, n_contrib, n_vis, n_keys = paper_counts
+    r_eval, r_contrib, r_vis, r_keys = run_counts
+    peaks = measured_peaks()
+    clock_mhz = clocks.get("sm_mhz") or 1965.0
+    lane_peak = SM_COUNT * FP32_LANES * clock_mhz * 1e6            # FP32 lane-ops/s (derived: 148 SM x 128 lanes)
+    ex2_peak = SM_COUNT * 16 * clock_mhz * 1e6                      # MUFU ex2/s (16 per SM per clock)
+    meas = alu_peak_measured(clock_mhz)
+    hbm_peak = (peaks or {}).get("hbm_gbs", 6650.0)
+    hbm = hbm_peak * 1e9
+    ops_blend = OPS_BLEND if want_rgb else OPS_BLEND_DEPTH_ONLY
+    passes = 3                                                      # 10-bit digits over the [0.01, 1e10] key span
+    ntiles = ((W + 15) // 16) * ((H + 15) // 16)
+    sh_eff = scene.sh_degree if want_rgb else 0
+    b_g = 60 + (4 * 3 * (sh_eff + 1) ** 2 if sh_eff > 0 else 0)   # scene bytes per Gaussian (SoA store)
+    by_out = E * W * H * ((3 if want_rgb else 0) + (4 if want_depth else 0)) * kb
+    work = {
+        # stage: (bound, algorithmic amount, unit scale, peak per s, description)
+        "cull": ("alu", E * kb * scene.n * OPS_CULL, lane_peak,
+                 f"{E * kb:,} envs x {scene.n:,} Gaussians x {OPS_CULL} lane-ops (SURVEY §8(d).2 pre-test)"),
+        "project": ("hbm", S * scene.n * b_g + r_vis * 60, hbm,
+                    f"scene {b_g} B/Gaussian once per scene + 60 B per visible record ({r_vis:,})"),
+        "depth_sort": ("hbm", r_vis * 16 * passes, hbm, f"16 B per record per pass x {passes} passes"),
+        "placement": ("hbm", r_vis * 12 + r_keys * 4 + E * kb * ntiles * 8, hbm,
+                      f"12 B per record + 4 B per key ({r_keys:,}) + 8 B per tile range"),
+        "raster": ("alu", r_eval * OPS_EVAL + r_contrib * ops_blend, lane_peak,
+                   f"{r_eval:,} evaluated x {OPS_EVAL} + {r_contrib:,} blended x {ops_blend} FP32 lane-ops "
+                   f"({args.tiles} lists, the ones the timed kernel walks)"),
+    }
+    kernels = {}
+    for i, n_ in enumerate(STAGES):
+        bound, amount, peak, desc = work[n_]
+        t = float(stage_ms[i]) / 1000.0
+        alg_s = amount / peak
+        ach = amount / max(t, 1e-12)
+        unit = "GB/s" if bound == "hbm" else "T lane-ops/s"
+        scale = 1e9 if bound == "hbm" else 1e12
+        kernels[n_] = {"bound": bound, "achieved": ach / scale, "peak": peak / scale, "unit": unit,
+                       "frac": ach / peak, "ms": float(stage_ms[i]), "alg_ms": alg_s * 1e3, "work": desc}
+    # raster: MUFU and output-write bounds beside the FP32 one
+    t_r = float(stage_ms[4]) / 1000.0
+    kernels["raster"]["mufu_frac"] = (r_contrib / ex2_peak) / max(t_r, 1e-12)
+    kernels["raster"]["writes_frac"] = (by_out / hbm) / max(t_r, 1e-12)
+    kernels["raster"]["frac_paper_lists"] = (n_eval * OPS_EVAL + n_contrib * ops_blend) / lane_peak / max(t_r, 1e-12)
+    dom = STAGES[int(np.argmax(stage_ms))]
+    k = kernels[dom]
+    roof = {"kernel": {"raster": "raster_warp_kernel (K6)", "cull": "cull_count_kernel (K1a)",
+                       "project": "project_kernel (K1b)", "depth_sort": "depth passes (K3/K4)",
+                       "placement": "placement passes (K4/K5)"}[dom],
+            "bound": k["bound"], "achieved": k["achieved"], "peak": k["peak"], "unit": k["unit"], "frac": k["frac"],
+            "work": k["work"], "traffic": None}
+    if dom == "raster":
+        tr, src, cap_envs = ncu_traffic("raster_warp_kernel")
+        launch_envs = min(E, args.chunk or 1024)
+        if tr and cap_envs:
+            tr = tr * launch_envs / cap_envs          # per launch of this run (DRAM bytes scale with envs)
+        roof["traffic"] = tr
+        roof["traffic_note"] = ((f"DRAM bytes per launch ({launch_envs} envs), scaled from the {cap_envs}-env ncu "
+                                 f"--set full capture in {src}") if tr else None)
+        roof["frac_paper_lists"] = k["frac_paper_lists"]
+        roof["peak_basis"] = (f"148 SM x 128 FP32 lanes x {clock_mhz:.0f} MHz median SM clock under load "
+                              f"(derived, DESIGN.md §6)")
+        if meas:
+            roof["peak_measured"] = meas["lane_ops_per_s"] / 1e12
+            roof["frac_of_measured"] = k["achieved"] * 1e12 / meas["lane_ops_per_s"]
+            roof["peak_measured_source"] = meas["source"]
+    else:
+        roof["peak_basis"] = "MEASURED_PEAKS.json hbm_gbs" if k["bound"] == "hbm" else "148 x 128 lanes x clock"
+    roof["stage_ms_per_step"] = {n_: float(v) for n_, v in zip(STAGES, stage_ms)}
+    roof["stage_share"] = {n_: float(v / max(stage_ms.sum(), 1e-9)) for n_, v in zip(STAGES, stage_ms)}
+    t_roof = sum(max(v["alg_ms"], kernels["raster"]["writes_frac"] * v["ms"] if n_ == "raster" else 0.0)
+                 for n_, v in kernels.items())
+    roof_path = {"kernels": kernels, "t_roof_ms": t_roof, "measured_ms": float(stage_ms.sum()),
+                 "frac": t_roof / max(float(stage_ms.sum()), 1e-9),
+                 "basis": "each stage's algorithmic work on its bounding resource (work strings), summed, against "
+                          "the summed stage times (CUDA events on the render stream)"}
+    return roof, roof_path
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on the box's host cores, same metric/config."""
     from paper_2510_15352_b200.dist import dist_env
@@ -266,21 +343,20 @@ def main():
     S = c["n_scenes"]
     R = gg.Renderer(gpu)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    binding = gi.scene_binding(7 + rank, E, S) if S > 1 else np.zeros(E, np.int32)
     n_sets = args.warmup + args.steps
     # a fresh, seeded pose set for every step, all resident in HBM; each env's camera
-    # lives in its own scene, drawn while that scene is at hand
-    vm = np.empty((n_sets, E, 4, 4), np.float32)
+    # lives in its own scene, drawn while that scene is at hand (gg_inputs.Workload, shared with the
+    # full-size parity tests)
+    wl = gi.Workload(args.config, n_envs=E, n_sets=n_sets, rank=rank, n_scenes=S, n_gauss=c["n_gauss"],
+                     sh_degree=c["sh_degree"])
+    binding = wl.binding
     sids, scene = [], None
-    for k, sc_ in enumerate(make_scenes(args, c)):
+    for k, sc_ in wl.scenes():
         sids.append(R.load_scene(t(sc_.means), t(sc_.scales), t(sc_.quats), t(sc_.opacities), t(sc_.sh),
                                  sc_.sh_degree))
         if k == int(binding[0]):
             scene = sc_                          # kept for the CPU baseline's sample
-        idx = np.flatnonzero(binding == k)
-        for s_ in range(n_sets if idx.size else 0):
-            seed = 10_000 * (rank + 1) + s_ if S == 1 else 10_000 * (rank + 1) + 4096 * s_ + k
-            vm[s_, idx] = gi.cameras(seed, idx.size, W, H, sc_).viewmats
+    vm = wl.viewmats
     ids_np = np.asarray(sids, np.int32)[binding]
     gg.gg_reserve(R.ctx, E, W, H, args.chunk)
     use_async = args.mode in ("async", "graph") and not args.blur
@@ -358,12 +434,12 @@ def main():
     time.sleep(0.3)
     launches0 = gg.gg_launch_count(R.ctx)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stage = np.zeros(3)
+    stage = np.zeros(5)
     ev0.record(stream)
     for k in range(args.steps):
         step(args.warmup + k)
         if graph is None:
-            stage += np.array(gg.gg_get_stage_ms(R.ctx))
+            stage += np.array(gg.gg_get_stage_times(R.ctx))
     ev1.record(stream)
     torch.cuda.synchronize()
     gg.gg_check_errors(R.ctx)          # async mode reports capacity overflow here
@@ -379,7 +455,7 @@ def main():
         gg.gg_set_timing(R.ctx, True)
         for k in range(args.steps):
             step(args.warmup + k)
-            stage += np.array(gg.gg_get_stage_ms(R.ctx))
+            stage += np.array(gg.gg_get_stage_times(R.ctx))
         torch.cuda.synchronize()                # (its last render is the last timed pose set)
     gg.gg_set_timing(R.ctx, False)
 
@@ -419,68 +495,9 @@ def main():
                "note": "gg_render_host: pinned host inputs -> device, frames -> pinned host, every step"}
         del h_rgb, h_depth
 
-    # ---- roofline of the dominant kernel (live CUDA-event stage times)
-    peaks = measured_peaks()
-    clock_mhz = clocks.get("sm_mhz") or 1965.0
-    alu_peak = SM_COUNT * FP32_LANES * 2 * clock_mhz * 1e6 / 1e12      # TFLOP/s (FFMA = 2)
-    hbm_peak = (peaks or {}).get("hbm_gbs", 6650.0)
-    names = ["project", "sort_bin", "raster"]
-    dom = int(np.argmax(stage_ms))
-    flops = (n_eval * FLOP_EVAL + n_contrib * FLOP_CONTRIB) * (args.steps and 1)
-    bytes_sort = n_vis * (4 + 8) + n_keys * 4 + E * (W // 16) * (H // 16) * 8
-    bytes_proj = scene.n * 56 + n_vis * 64
-    if names[dom] == "raster":
-        ach = flops / (stage_ms[2] / 1000.0) / 1e12
-        tr, src, cap_envs = ncu_traffic("raster_warp_kernel")
-        launch_envs = min(E, args.chunk or 1024)
-        if tr and cap_envs:
-            tr = tr * launch_envs / cap_envs          # per launch of this run (DRAM bytes scale with envs)
-        roof = {"kernel": "raster_warp_kernel (K6)", "bound": "alu", "achieved": ach, "peak": alu_peak,
-                "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": tr,
-                "traffic_note": (f"DRAM bytes per launch ({launch_envs} envs), scaled from the {cap_envs}-env ncu "
-                                 f"--set full capture in {src}") if tr else None,
-                "peak_basis": f"148 SM x 128 FP32 lanes x 2 (FFMA) x {clock_mhz:.0f} MHz median SM clock under load",
-                "work": (f"{n_eval:,} evaluated pairs x {FLOP_EVAL} + {n_contrib:,} blended x {FLOP_CONTRIB} flops "
-                         f"(the paper's 3-sigma lists; the rendered {args.tiles} lists evaluate {r_eval:,})")}
-    elif names[dom] == "sort_bin":
-        ach = bytes_sort / (stage_ms[1] / 1000.0) / 1e9
-        roof = {"kernel": "sort_bin_kernel (K3-K5)", "bound": "hbm", "achieved": ach, "peak": hbm_peak,
-                "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None, "peak_basis": "MEASURED_PEAKS.json hbm_gbs"}
-    else:
-        ach = bytes_proj / (stage_ms[0] / 1000.0) / 1e9
-        roof = {"kernel": "cull_count+project (K1)", "bound": "hbm", "achieved": ach, "peak": hbm_peak,
-                "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None, "peak_basis": "MEASURED_PEAKS.json hbm_gbs"}
-    roof["stage_ms_per_step"] = {n: float(v) for n, v in zip(names, stage_ms)}
-    roof["stage_share"] = {n: float(v / max(stage_ms.sum(), 1e-9)) for n, v in zip(names, stage_ms)}
-
-    # ---- whole-path roofline: each stage's algorithmic work on
-    # its bounding resource, summed, against the measured stage times
-    lane_ops = SM_COUNT * FP32_LANES * clock_mhz * 1e6             # FP32 lane-ops/s
-    ex2_rate = SM_COUNT * 16 * clock_mhz * 1e6                      # MUFU ex2/s
-    hbm = hbm_peak * 1e9
-    sh_eff = scene.sh_degree if want_rgb else 0
-    b_g = 60 + (4 * 3 * (sh_eff + 1) ** 2 if sh_eff > 0 else 0)     # scene bytes per Gaussian
-    ops_proj = E * scene.n * 25 + n_vis * (150 + (130 if sh_eff > 0 else 0))
-    by_proj = S * scene.n * b_g + n_vis * 60
-    passes = 3                                                     # 10-bit digits over the ~26-bit depth span
-    by_sort = n_vis * 8 * 2 * passes + n_vis * 4 + n_keys * 12
-    by_out = E * W * H * ((3 if want_rgb else 0) + (4 if want_depth else 0))
-    t_alg = {
-        "project": (max(ops_proj / lane_ops, by_proj / hbm), "fp32" if ops_proj / lane_ops > by_proj / hbm else "hbm"),
-        "sort_bin": (by_sort / hbm, "hbm"),
-        "raster": max((flops / (alu_peak * 1e12), "fp32"), (n_contrib / ex2_rate, "mufu"), (by_out / hbm, "hbm")),
-    }
-    stages = {}
-    for n_, v in zip(names, stage_ms):
-        ta, bnd = t_alg[n_]
-        stages[n_] = {"bound": bnd, "alg_ms": ta * 1e3, "measured_ms": float(v), "frac": ta * 1e3 / max(float(v), 1e-9)}
-    t_roof = sum(v["alg_ms"] for v in stages.values())
-    roof_path = {"stages": stages, "t_roof_ms": t_roof, "measured_ms": float(stage_ms.sum()),
-                 "frac": t_roof / max(float(stage_ms.sum()), 1e-9),
-                 "basis": ("SURVEY §8(d).2: project = max(25 ops per (env, Gaussian) candidate + 150 (+130 SH) per "
-                           "visible record on FP32 lanes, scene + 60 B/record on HBM); sort = 16 B x passes + 4 B per "
-                           "record + 12 B per key on HBM; raster = max(definition flops on FP32, one ex2 per blended "
-                           "pair on MUFU, frame bytes on HBM); counts from the GG_COUNTERS pass")}
+    # ---- rooflines (live CUDA-event stage times on the render stream)
+    roof, roof_path = roofline(args, c, E, W, H, S, scene, want_rgb, want_depth, stage_ms, clocks, kb,
+                               (n_eval, n_contrib, n_vis, n_keys), (r_eval, r_contrib, r_vis, r_keys))
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None

@@ -437,6 +437,84 @@ def config_cameras(cfg: str, scene: Scene, n_envs: int | None = None, index: int
 
 
 # ---------------------------------------------------------------------------
+# Benchmark workloads (bench.py and the full-size parity tests share them)
+# ---------------------------------------------------------------------------
+
+def _room_job(args3):
+    k, n, d = args3
+    return room_scene(100 + k, n, d)
+
+
+class Workload:
+    """The seeded inputs of one BASELINE config as bench.py renders them.
+
+    One scene (c1-c3: `config_scene`) or S rooms `room_scene(100 + k, ...)`
+    with a seeded uniform env->scene binding (c4/c5).  Pose set
+    s of env e is drawn in e's own scene: seed 10,000 (rank+1) + s for one
+    scene, 10,000 (rank+1) + 4,096 s + k for scene k of several.  `scenes()`
+    generates the rooms in parallel and streams them (c5's 2,500 rooms never
+    sit in host memory at once), filling `viewmats[s, envs of k]` as scene k
+    goes by; `scene(k)` regenerates one scene on its own (same seed, same
+    arrays).
+    """
+
+    def __init__(self, cfg: str, n_envs: int | None = None, n_sets: int = 1, rank: int = 0,
+                 n_scenes: int | None = None, n_gauss: int | None = None, sh_degree: int | None = None):
+        c = CONFIGS[cfg]
+        self.cfg = cfg
+        self.n_envs = c["n_envs"] if n_envs is None else n_envs
+        self.n_sets, self.rank = n_sets, rank
+        self.width, self.height = c["width"], c["height"]
+        self.n_gauss = c["n_gauss"] if n_gauss is None else n_gauss
+        self.sh_degree = c["sh_degree"] if sh_degree is None else sh_degree
+        self.n_scenes = n_scenes or (c["n_scenes"] if cfg in ("c4", "c5") else 1)
+        S, E = self.n_scenes, self.n_envs
+        self.binding = scene_binding(7 + rank, E, S) if S > 1 else np.zeros(E, np.int32)
+        self.viewmats = np.empty((n_sets, E, 4, 4), np.float32)
+        self.intrinsics = np.tile(pinhole(self.width, self.height).astype(np.float32), (E, 1))
+
+    def scene(self, k: int) -> Scene:
+        if self.n_scenes == 1:
+            return config_scene(self.cfg, n_gauss=self.n_gauss, sh_degree=self.sh_degree)
+        return _room_job((k, self.n_gauss, self.sh_degree))
+
+    def _fill(self, k: int, sc: Scene):
+        idx = np.flatnonzero(self.binding == k)
+        if not idx.size:
+            return
+        for s_ in range(self.n_sets):
+            seed = 10_000 * (self.rank + 1) + (s_ if self.n_scenes == 1 else 4096 * s_ + k)
+            self.viewmats[s_, idx] = cameras(seed, idx.size, self.width, self.height, sc).viewmats
+
+    def scenes(self, n_proc: int | None = None):
+        """Yield (k, scene) for k = 0..S-1 in order (parallel host generation)."""
+        S = self.n_scenes
+        if S == 1:
+            sc = self.scene(0)
+            self._fill(0, sc)
+            yield 0, sc
+            return
+        import concurrent.futures as cf
+        import os
+        if n_proc is None:
+            n_proc = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 4)
+            n_proc = max(1, min(16, n_proc))
+        job = (self.n_gauss, self.sh_degree)
+        with cf.ProcessPoolExecutor(n_proc) as ex:
+            futs = {k: ex.submit(_room_job, (k,) + job) for k in range(min(S, 2 * n_proc))}
+            for k in range(S):
+                sc = futs.pop(k).result()
+                nxt = k + 2 * n_proc
+                if nxt < S:
+                    futs[nxt] = ex.submit(_room_job, (nxt,) + job)
+                self._fill(k, sc)
+                yield k, sc
+
+    def cameras(self, s: int = 0) -> Cameras:
+        return Cameras(self.viewmats[s], self.intrinsics, self.width, self.height)
+
+
+# ---------------------------------------------------------------------------
 # 3DGS PLY writer (input construction for the PLY-reader tests): stores the
 # *raw* parameters the 3DGS format holds (log scales, opacity logits,
 # channel-major f_rest).

@@ -243,10 +243,17 @@ gg_status gg_get_counters(gg_context* ctx, int32_t n_envs, int64_t* host_dst);
 /* Number of kernels this context has launched since creation. */
 int64_t gg_launch_count(const gg_context* ctx);
 
-/* Per-stage device time (ms) of the last render, measured with CUDA events
- * when `enable` was set by gg_set_timing; order: project, sort, raster. */
+/* Per-stage device time (ms) of the last render, measured with CUDA events on
+ * the render stream when `enable` was set by gg_set_timing (events are
+ * resolved lazily: the first query after a render synchronises with it).
+ * gg_get_stage_ms: 3 stages = project (cull + project), sort (depth passes +
+ * placement), raster.  gg_get_stage_times: the first n (1..5) of the finer
+ * stages cull (K1a + K2), project (K1b), depth passes (K3/K4 depth),
+ * placement (K4/K5 tile pass + ranges), raster (K6).  In the host-synchronising
+ * sync mode the project stage also spans the host's per-chunk readback. */
 gg_status gg_set_timing(gg_context* ctx, int32_t enable);
 gg_status gg_get_stage_ms(gg_context* ctx, float* out3);
+gg_status gg_get_stage_times(gg_context* ctx, float* out, int32_t n);
 
 const char* gg_last_error(const gg_context* ctx);
 const char* gg_status_string(gg_status s);

@@ -33,6 +33,7 @@ F_UNTRUNCATED = 2
 F_PLAIN = 4
 F_TIGHT = 8         # work-reduction variant: opacity-aware tile rects (R35)
 F_ELLIPSE = 16      # work-reduction variant: ellipse ∩ tile masks on tight rects (R37)
+F_INTEGER_ONLY = 32 # stop after O3: integer artefacts only (image outputs empty)
 
 K_RGB, K_DEPTH, K_ALPHA, K_NEVAL, K_NCONTRIB, K_EXEMPT = 0, 1, 2, 3, 4, 5
 K_TILE_COUNTS, K_SORTED_TILE, K_SORTED_ZBITS, K_SORTED_GID, K_RANGES = 6, 7, 8, 9, 10
@@ -156,7 +157,7 @@ def render_env(scene: OracleScene, viewmat, intr, width: int, height: int, *, ne
             if n:
                 L.or_result_copy(h, kind, a.ctypes.data_as(C.c_void_p))
             return a
-        H, W = height, width
+        H, W = (height, width) if not (flags & F_INTEGER_ONLY) else (0, 0)
         return EnvResult(width, height,
                          get(K_RGB).reshape(H, W, 3), get(K_RGB8).reshape(H, W, 3),
                          get(K_DEPTH).reshape(H, W), get(K_ALPHA).reshape(H, W),

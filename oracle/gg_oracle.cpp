@@ -343,7 +343,7 @@ struct Result {
   std::vector<float> proj;     // [n*16]
 };
 
-enum { F_NO_EARLY_OUT = 1, F_UNTRUNCATED = 2, F_PLAIN = 4, F_TIGHT = 8, F_ELLIPSE = 16 };
+enum { F_NO_EARLY_OUT = 1, F_UNTRUNCATED = 2, F_PLAIN = 4, F_TIGHT = 8, F_ELLIPSE = 16, F_INTEGER_ONLY = 32 };
 
 // O4 + O5 for one pixel over an ordered sequence of records.
 struct PixelOut {
@@ -400,7 +400,7 @@ struct OrOpts {
   double background[3];
   int32_t sh_degree;   // -1: scene degree
   int32_t mode;        // 0 = A (f32 canonical projection), 1 = B (f64 projection)
-  int32_t flags;       // F_NO_EARLY_OUT | F_UNTRUNCATED | F_PLAIN | F_TIGHT | F_ELLIPSE
+  int32_t flags;       // F_NO_EARLY_OUT | F_UNTRUNCATED | F_PLAIN | F_TIGHT | F_ELLIPSE | F_INTEGER_ONLY
 };
 
 void* or_scene_create(int64_t n, int32_t d, const float* means, const float* scales,
@@ -529,6 +529,10 @@ void* or_render_env(const void* scene, const float* view, const float* intr, int
   for (size_t k = 0; k < items.size(); ++k) {
     R->s_tile[k] = items[k].t; R->s_zbits[k] = items[k].zbits; R->s_gid[k] = items[k].gid;
   }
+
+  // F_INTEGER_ONLY: stop after O3 (the integer artefacts); the image
+  // outputs are left empty (a test-time shortcut, no arithmetic changes)
+  if (opt->flags & F_INTEGER_ONLY) return R;
 
   // O4-O5
   const size_t npx = (size_t)W * H;

@@ -33,7 +33,7 @@ GG_ELLIPSE_TILES = 16       # + ellipse-intersects-tile masks (DESIGN.md reading
 EXPORTS = ["gg_default_opts", "gg_create", "gg_destroy", "gg_load_scene", "gg_unload_scene", "gg_reserve",
            "gg_render", "gg_render_host", "gg_render_blur", "gg_blur_poses", "gg_checksum", "gg_check_errors", "gg_debug_dump", "gg_get_counters",
            "gg_launch_count", "gg_set_timing", "gg_get_stage_ms", "gg_last_error", "gg_status_string",
-           "gg_read_ply", "gg_load_ply", "gg_ply_error", "gg_reserve_async", "gg_dino_input"]
+           "gg_read_ply", "gg_load_ply", "gg_ply_error", "gg_reserve_async", "gg_dino_input", "gg_get_stage_times"]
 
 
 class GGError(RuntimeError):
@@ -92,6 +92,7 @@ def load_library(path: str = LIB_PATH):
     L.gg_launch_count.restype = i64
     L.gg_set_timing.argtypes = [vp, i32]
     L.gg_get_stage_ms.argtypes = [vp, C.POINTER(C.c_float)]
+    L.gg_get_stage_times.argtypes = [vp, C.POINTER(C.c_float), i32]
     L.gg_last_error.argtypes = [vp]
     L.gg_last_error.restype = C.c_char_p
     L.gg_status_string.argtypes = [C.c_int]
@@ -279,6 +280,16 @@ def gg_set_timing(ctx, enable: bool):
 def gg_get_stage_ms(ctx) -> tuple[float, float, float]:
     a = (C.c_float * 3)()
     _check(ctx, load_library().gg_get_stage_ms(ctx, a))
+    return tuple(a)
+
+
+STAGES = ("cull", "project", "depth_sort", "placement", "raster")
+
+
+def gg_get_stage_times(ctx, n: int = 5) -> tuple:
+    """Finer per-stage ms of the last timed render (STAGES order)."""
+    a = (C.c_float * n)()
+    _check(ctx, load_library().gg_get_stage_times(ctx, a, n))
     return tuple(a)
 
 

@@ -36,7 +36,7 @@ int depth_passes(uint32_t span);
 int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, uint32_t* blk_env, int passes,
                     const RenderParams& rp,
                     const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s, bool nb_is_capacity,
-                    uint32_t* qctr);
+                    uint32_t* qctr, cudaEvent_t after_depth);
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s);
@@ -89,6 +89,8 @@ struct SceneSlot {
 };
 
 constexpr int DEFAULT_CHUNK = 1024;
+// timed stages: cull+scan, project, depth passes, placement (+ranges), raster
+constexpr int NSTAGE = 5;
 constexpr int SCENE_TABLE_MIN = 4096;   // scene-table slots allocated up front
 
 }  // namespace
@@ -129,8 +131,10 @@ struct gg_context {
   int64_t d_counters[4] = {0, 0, 0, 0};
   // timing
   bool timing = false;
-  float stage_ms[3] = {0, 0, 0};
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  float stage_ms[NSTAGE] = {0, 0, 0, 0, 0};
+  std::vector<cudaEvent_t> tev;   // per-chunk stage events [chunk][NSTAGE + 1], resolved lazily
+  int t_nchunks = 0;              // chunks of the last timed render not yet resolved
+  int t_used = 0;                 // events handed out in the current render
   cudaEvent_t ev_copy = nullptr;
   int last_E = 0;
   // sync-free mode (gg_reserve_async)
@@ -138,8 +142,6 @@ struct gg_context {
   int a_max_envs = 0, a_W = 0, a_H = 0, a_chunk = 0, a_nblk = 0, a_maxdeg = 0;
   uint64_t a_vcap = 0, a_kcap = 0, a_nbcap = 0;
   DevBuf okflag;
-  std::vector<cudaEvent_t> a_ev;   // per-chunk stage events (timing only)
-  int a_nchunks = 0;
 };
 
 namespace {
@@ -297,7 +299,6 @@ gg_status gg_create(int device, const gg_allocator* a, gg_context** out) {
   CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
   CK(sort_bin_init());
   CK(project_init());
-  for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
   CK(cudaEventCreateWithFlags(&ctx->ev_copy, cudaEventDisableTiming));
   CK(cudaMallocHost(&ctx->h_err, 4));
   if (!ensure_host(ctx, 1024)) return fail(ctx, GG_E_OOM, "pinned host alloc failed");
@@ -317,7 +318,7 @@ gg_status gg_destroy(gg_context* ctx) {
     dev_free(ctx, sc.pos_op, s); dev_free(ctx, sc.cov_a, s); dev_free(ctx, sc.cov_b, s);
     dev_free(ctx, sc.aux, s); dev_free(ctx, sc.qmax, s); dev_free(ctx, sc.sh, s);
   }
-  for (auto& e : ctx->a_ev) cudaEventDestroy(e);
+  for (auto& e : ctx->tev) cudaEventDestroy(e);
   for (Work* w : {&ctx->sw, &ctx->aw})
     for (int i = 0; i < Work::count; ++i) dev_free(ctx, w->all()[i], s);
   DevBuf* all[] = {&ctx->scene_table, &ctx->errflag, &ctx->valid_out,
@@ -329,7 +330,6 @@ gg_status gg_destroy(gg_context* ctx) {
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
   cudaFreeHost(ctx->h_kbase); cudaFreeHost(ctx->h_err);
   cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
-  for (auto& e : ctx->ev) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev_copy);
   cudaStreamDestroy(s);
   delete ctx;
@@ -488,21 +488,36 @@ gg_status gg_set_timing(gg_context* ctx, int32_t en) {
   return GG_OK;
 }
 
+static gg_status resolve_timing(gg_context* ctx) {
+  if (ctx->t_nchunks == 0) return GG_OK;
+  float ms[NSTAGE] = {0, 0, 0, 0, 0};
+  CK(cudaEventSynchronize(ctx->tev[ctx->t_nchunks * (NSTAGE + 1) - 1]));
+  for (int c = 0; c < ctx->t_nchunks; ++c)
+    for (int k = 0; k < NSTAGE; ++k) {
+      float x = 0;
+      CK(cudaEventElapsedTime(&x, ctx->tev[c * (NSTAGE + 1) + k], ctx->tev[c * (NSTAGE + 1) + k + 1]));
+      ms[k] += x;
+    }
+  for (int k = 0; k < NSTAGE; ++k) ctx->stage_ms[k] = ms[k];
+  ctx->t_nchunks = 0;
+  return GG_OK;
+}
+
 gg_status gg_get_stage_ms(gg_context* ctx, float* out3) {
   if (!ctx || !out3) return GG_E_INVALID;
-  if (ctx->a_nchunks > 0) {   // async-mode events: resolve now (synchronises)
-    float ms[3] = {0, 0, 0};
-    CK(cudaEventSynchronize(ctx->a_ev[ctx->a_nchunks * 4 - 1]));
-    for (int c = 0; c < ctx->a_nchunks; ++c)
-      for (int k = 0; k < 3; ++k) {
-        float x = 0;
-        cudaEventElapsedTime(&x, ctx->a_ev[c * 4 + k], ctx->a_ev[c * 4 + k + 1]);
-        ms[k] += x;
-      }
-    for (int k = 0; k < 3; ++k) ctx->stage_ms[k] = ms[k];
-    ctx->a_nchunks = 0;
-  }
-  for (int i = 0; i < 3; ++i) out3[i] = ctx->stage_ms[i];
+  gg_status st = resolve_timing(ctx);
+  if (st != GG_OK) return st;
+  out3[0] = ctx->stage_ms[0] + ctx->stage_ms[1];
+  out3[1] = ctx->stage_ms[2] + ctx->stage_ms[3];
+  out3[2] = ctx->stage_ms[4];
+  return GG_OK;
+}
+
+gg_status gg_get_stage_times(gg_context* ctx, float* out, int32_t n) {
+  if (!ctx || !out || n < 1 || n > NSTAGE) return GG_E_INVALID;
+  gg_status st = resolve_timing(ctx);
+  if (st != GG_OK) return st;
+  for (int i = 0; i < n; ++i) out[i] = ctx->stage_ms[i];
   return GG_OK;
 }
 
@@ -522,6 +537,23 @@ static uint32_t f32_bits(float x) {
 
 // depth-sort passes: keys are z bits - bits(near) in (0, bits(far) - bits(near)]
 static int depth_passes_for(float near_p, float far_p) { return depth_passes(f32_bits(far_p) - f32_bits(near_p)); }
+
+// The NSTAGE + 1 timing events of chunk c of the current render (created on
+// demand; events are never created or recorded unless timing is enabled).
+static cudaEvent_t* chunk_events(gg_context* ctx, int c) {
+  const size_t need = (size_t)(c + 1) * (NSTAGE + 1);
+  while (ctx->tev.size() < need) {
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreate(&ev) != cudaSuccess) return nullptr;
+    ctx->tev.push_back(ev);
+  }
+  return ctx->tev.data() + (size_t)c * (NSTAGE + 1);
+}
+
+#define TREC(k)                                                                  \
+  do {                                                                           \
+    if (tev) CK(cudaEventRecord(tev[k], s));                                     \
+  } while (0)
 
 static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
                              const float* intr, int32_t W, int32_t H, const gg_render_opts* opts_in,
@@ -598,8 +630,11 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   CK(cudaGetLastError());
   if (keep && !ensure(ctx, ctx->sw.gid, 16, s)) return fail(ctx, GG_E_OOM, "alloc");
 
-  float ms[3] = {0, 0, 0};
-  for (int e0 = 0, ec = 0; e0 < E; e0 += ec) {
+  ctx->t_nchunks = 0;
+  int cidx = 0;
+  for (int e0 = 0, ec = 0; e0 < E; e0 += ec, ++cidx) {
+    cudaEvent_t* tev = ctx->timing ? chunk_events(ctx, cidx) : nullptr;
+    if (ctx->timing && !tev) return fail(ctx, GG_E_CUDA, "gg_render: timing events");
     ec = std::min(chunk, E - e0);
     if (cb && chunk >= 64) {
       // host path: a short first chunk gets frames onto the copy engine early,
@@ -637,12 +672,13 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ws.nblk = nblk;
     ws.ec = ec;
     const EnvGroup* groups = P<EnvGroup>(ctx->sw.groups);
-    if (ctx->timing) CK(cudaEventRecord(ctx->ev[0], s));
+    TREC(0);
     // K1a + K2
     launch_cull_count(e0, ngroups, nblk, groups, P<EnvConst>(ctx->sw.envc), P<DevScene>(ctx->scene_table), rp, ws, s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
     ctx->launches += 2;
     CK(cudaGetLastError());
+    TREC(1);
     ctx->launches += launch_copy_words(ctx->h_vcnt, ws.vcnt, ec * 4, s);
     CK(cudaStreamSynchronize(s));
     uint64_t V = 0;
@@ -670,7 +706,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ctx->launches++;
     CK(cudaGetLastError());
     ctx->launches += launch_copy_words(ctx->h_kcnt, ws.kcnt, ec * 8, s);
-    if (ctx->timing) CK(cudaEventRecord(ctx->ev[1], s));
+    TREC(2);
     CK(cudaStreamSynchronize(s));
     uint64_t K = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_kbase[i] = K; K += ctx->h_kcnt[i]; }
@@ -694,9 +730,9 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ctx->launches += launch_copy_words(ctx->sw.blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, s);
     ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->sw.blkbase), P<uint32_t>(ctx->sw.blkenv), passes, rp, ws,
                                      P<uint32_t>(ctx->sw.ghist),
-                                     P<uint32_t>(ctx->sw.thist), s, false, nullptr);
+                                     P<uint32_t>(ctx->sw.thist), s, false, nullptr, tev ? tev[3] : nullptr);
     CK(cudaGetLastError());
-    if (ctx->timing) CK(cudaEventRecord(ctx->ev[2], s));
+    TREC(4);
     // K6
     const int dbg_eloc = (dbg_pos >= e0 && dbg_pos < e0 + ec) ? dbg_pos - e0 : -1;
     int32_t* dbg_neval = nullptr;
@@ -730,15 +766,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       ctx->launches++;
       CK(cudaGetLastError());
     }
-    if (ctx->timing) {
-      CK(cudaEventRecord(ctx->ev[3], s));
-      CK(cudaEventSynchronize(ctx->ev[3]));
-      float a, b, c;
-      cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
-      cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
-      cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
-      ms[0] += a; ms[1] += b; ms[2] += c;
-    }
+    TREC(5);
     if (dbg_eloc >= 0) {
       // K8: snapshot the debug env's integer artefacts to host
       const uint32_t Vd = ctx->h_vcnt[dbg_eloc], Kd = (uint32_t)ctx->h_kcnt[dbg_eloc];
@@ -785,7 +813,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       }
     }
   }
-  if (ctx->timing) for (int i = 0; i < 3; ++i) ctx->stage_ms[i] = ms[i];
+  if (ctx->timing) ctx->t_nchunks = cidx;
   ctx->last_E = E;
   ctx->launches += launch_copy_words(ctx->h_err, ctx->errflag.p, 4, s);
   CK(cudaStreamSynchronize(s));
@@ -836,14 +864,10 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
                     H, opts.sh_degree, P<EnvConst>(ctx->aw.envc), err, s);
   ctx->launches++;
   const int nchunks = (E + chunk - 1) / chunk;
-  if (ctx->timing) {
-    while ((int)ctx->a_ev.size() < nchunks * 4) {
-      cudaEvent_t ev;
-      CK(cudaEventCreate(&ev));
-      ctx->a_ev.push_back(ev);
-    }
-  }
+  ctx->t_nchunks = 0;
   for (int c = 0; c < nchunks; ++c) {
+    cudaEvent_t* tev = ctx->timing ? chunk_events(ctx, c) : nullptr;
+    if (ctx->timing && !tev) return fail(ctx, GG_E_CUDA, "gg_render: timing events");
     const int e0 = c * chunk, ec = std::min(chunk, E - e0);
     const int ngroups = (ec + ENV_GROUP - 1) / ENV_GROUP;
     ChunkWS ws{};
@@ -864,30 +888,31 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     ws.nwords = nwords;
     ws.nblk = nblk;
     ws.ec = ec;
-    if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 0], s));
+    TREC(0);
     CK(cudaMemsetAsync(ws.kcnt, 0, ec * 8, s));
     CK(cudaMemsetAsync(ok, 0x01, 4, s));
     launch_cull_count(e0, ngroups, nblk, nullptr, P<EnvConst>(ctx->aw.envc), P<DevScene>(ctx->scene_table), rp, ws, s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
     launch_tables_v(ec, ws.vcnt, P<uint64_t>(ctx->aw.rbase), ctx->a_vcap, ok, err, s);
+    TREC(1);
     launch_project(e0, ngroups, nblk, ctx->a_maxdeg, nullptr, P<EnvConst>(ctx->aw.envc), P<DevScene>(ctx->scene_table),
                    rp, ws, s);
     launch_tables_k(ec, ws.vcnt, ws.kcnt, P<uint64_t>(ctx->aw.kbase), P<uint32_t>(ctx->aw.blkbase), sort_block_size(),
                     ctx->a_kcap, ctx->a_nbcap, ok, err, s);
     ctx->launches += 5;
-    if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 1], s));
+    TREC(2);
     ctx->launches += launch_sort_bin(ec, (uint32_t)ctx->a_nbcap, P<uint32_t>(ctx->aw.blkbase), P<uint32_t>(ctx->aw.blkenv),
                                      passes, rp, ws,
                                      P<uint32_t>(ctx->aw.ghist), P<uint32_t>(ctx->aw.thist), s, true,
-                                     P<uint32_t>(ctx->aw.qctr));
-    if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 2], s));
+                                     P<uint32_t>(ctx->aw.qctr), tev ? tev[3] : nullptr);
+    TREC(4);
     launch_raster(e0, ec, P<EnvConst>(ctx->aw.envc), rp, ws, rgb, depth, alpha, counters,
                   counters ? P<unsigned long long>(ctx->aw.counters) : nullptr, nullptr, -1, s);
     ctx->launches++;
-    if (ctx->timing) CK(cudaEventRecord(ctx->a_ev[c * 4 + 3], s));
+    TREC(5);
     CK(cudaGetLastError());
   }
-  ctx->a_nchunks = ctx->timing ? nchunks : 0;
+  if (ctx->timing) ctx->t_nchunks = nchunks;
   ctx->last_E = E;
   return GG_OK;
 }

@@ -681,7 +681,8 @@ int depth_passes(uint32_t span) {
 // blocks; ghist >= nb*DS_RADIX u32; thist >= nb*ntiles u32.  Returns launches.
 template <bool LOOP>
 static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, const RenderParams& rp,
-                             const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s, uint32_t* qctr) {
+                             const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s, uint32_t* qctr,
+                             cudaEvent_t after_depth) {
   // sync mode (LOOP = false): one CTA per block; async mode: nb is only a
   // capacity, so a bounded grid (a few waves of resident CTAs) takes the
   // blocks that exist from per-launch work counters
@@ -703,6 +704,7 @@ static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, con
     depth_downsweep_kernel<LOOP><<<g1, DS_THREADS, depth_down_smem(), s>>>(bt, ws, io, DS_BITS * p, ghist);
     launches += 3;
   }
+  if (after_depth) cudaEventRecord(after_depth, s);   // stage timing: depth passes | placement
   const uint32_t* order = ws.order;   // records of the last depth pass
   if (LOOP) bt.q = qctr + qi++;
   const bool mask = ws.rmask != nullptr;
@@ -731,15 +733,17 @@ static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, con
 // nb*ntiles u32.  Returns the number of launches.
 int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, uint32_t* blk_env, int passes,
                     const RenderParams& rp, const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s,
-                    bool nb_is_capacity, uint32_t* qctr) {
+                    bool nb_is_capacity, uint32_t* qctr, cudaEvent_t after_depth) {
   if (nb == 0) {
+    if (after_depth) cudaEventRecord(after_depth, s);
     cudaMemsetAsync(ws.ranges, 0, (size_t)ec * rp.ntiles * sizeof(uint2), s);
     return 0;
   }
   blk_env_kernel<<<ec, 128, 0, s>>>(blk_base, ec, blk_env);
   BlockTable bt{blk_base, blk_env, ec, nullptr};
-  return 1 + (nb_is_capacity ? launch_sort_bin_t<true>(ec, nb, bt, passes, rp, ws, ghist, thist, s, qctr)
-                            : launch_sort_bin_t<false>(ec, nb, bt, passes, rp, ws, ghist, thist, s, nullptr));
+  return 1 + (nb_is_capacity ? launch_sort_bin_t<true>(ec, nb, bt, passes, rp, ws, ghist, thist, s, qctr, after_depth)
+                            : launch_sort_bin_t<false>(ec, nb, bt, passes, rp, ws, ghist, thist, s, nullptr,
+                                                       after_depth));
 }
 
 }  // namespace gg

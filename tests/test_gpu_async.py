@@ -3,6 +3,8 @@ import numpy as np
 import pytest
 
 import gg_inputs as gi
+import oracle
+from parity import Tally
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -50,6 +52,15 @@ def test_async_equals_sync_mixed_scenes(gg):
     b = _render(gg, r, ids, vm, K, W, H, flags=gg.GG_ASYNC)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+    # and the sync-free render against the oracle, every env
+    osc = [oracle.OracleScene.from_inputs(s) for s in scenes]
+    intr = np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1))
+    t = Tally()
+    for e in range(E):
+        o = oracle.render_env(osc[int(bind[e])], vms[e], intr[e], W, H)
+        t.add(b[0][e], b[1][e], b[2][e], o)
+    print(t)
+    t.check()
     r.close()
 
 
@@ -74,14 +85,59 @@ def test_async_graph_capture_replay(gg):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         gg.gg_render(r.ctx, E, ids, vm, K, W, H, opts, rgb, dep, al, stream=s)
+    osc = oracle.OracleScene.from_inputs(sc)
     for cams in (cams_b, cams_a):
         vm.copy_(dev(cams.viewmats))
         g.replay()
         torch.cuda.synchronize()
+        got = (rgb.cpu().numpy(), dep.cpu().numpy(), al.cpu().numpy())
+        t = Tally()                                  # the replayed graph against the oracle
+        for e in range(E):
+            t.add(got[0][e], got[1][e], got[2][e],
+                  oracle.render_env(osc, cams.viewmats[e], cams.intrinsics[e], W, H))
+        print(t)
+        t.check()
         ref = _render(gg, r, ids, dev(cams.viewmats), K, W, H)
-        assert np.array_equal(rgb.cpu().numpy(), ref[0])
-        assert np.array_equal(dep.cpu().numpy(), ref[1])
-        assert np.array_equal(al.cpu().numpy(), ref[2])
+        for x, y in zip(got, ref):
+            assert np.array_equal(x, y)
+    r.close()
+
+
+def test_graph_survives_sync_renders_and_scene_loads(gg):
+    """a graph captured over a GG_ASYNC render must stay valid when
+    sync renders (which grow their own workspace) and scene loads happen
+    between replays."""
+    r = gg.Renderer(0)
+    sc = gi.config_scene("c1")
+    sid = r.load_scene(dev(sc.means), dev(sc.scales), dev(sc.quats), dev(sc.opacities), dev(sc.sh), sc.sh_degree)
+    E, W, H = 8, 64, 48
+    cams = gi.cameras(4, E, W, H, sc)
+    ids = dev(np.full(E, sid, np.int32))
+    K, vm = dev(cams.intrinsics), dev(cams.viewmats)
+    rgb, dep, al = _outs(E, H, W)
+    gg.gg_reserve_async(r.ctx, E, W, H, 0, 0.9, 6.0)
+    opts = gg.default_opts(flags=gg.GG_ASYNC)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        gg.gg_render(r.ctx, E, ids, vm, K, W, H, opts, rgb, dep, al, stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        gg.gg_render(r.ctx, E, ids, vm, K, W, H, opts, rgb, dep, al, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    first = (rgb.cpu().numpy(), dep.cpu().numpy(), al.cpu().numpy())
+    # a much larger sync render (its workspace grows) and another scene load
+    big = gi.room_scene(9, 200_000, 3)
+    bid = r.load_scene(dev(big.means), dev(big.scales), dev(big.quats), dev(big.opacities), dev(big.sh), 3)
+    cb = gi.cameras(5, 64, 320, 240, big)
+    _render(gg, r, dev(np.full(64, bid, np.int32)), dev(cb.viewmats), dev(cb.intrinsics), 320, 240)
+    rgb.zero_(); dep.zero_(); al.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for x, y in zip(first, (rgb.cpu().numpy(), dep.cpu().numpy(), al.cpu().numpy())):
+        assert np.array_equal(x, y)
     r.close()
 
 

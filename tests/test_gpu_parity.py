@@ -90,6 +90,20 @@ def test_c1_full(gg, R):
     print(t)
 
 
+def test_near_far_cull_boundaries(gg, R):
+    """The GPU's cull predicate on the f32 boundary values (test_oracle_pins
+    near_far_fixture): tile counts bit-exact with the oracle, images in tolerance."""
+    from test_oracle_pins import FAR32, NEAR32, near_far_fixture
+    sc, expect, _ = near_far_fixture()
+    cams = gi.identity_cameras(1, 64, 48, 32.0)
+    sid = load(R, sc)
+    t = Tally()
+    parity_envs(gg, R, {sid: sc}, [sid], cams, [0], t, near_plane=float(NEAR32), far_plane=float(FAR32))
+    t.check()
+    tc = gg.gg_debug_dump(R.ctx, gg.GG_DUMP_TILE_COUNTS)
+    assert ((tc > 0) == expect).all()
+
+
 @pytest.mark.parametrize("near,far,passes", [(4.0, 4.4, 2), (0.01, 1e10, 3), (1e-30, 1e10, 4)])
 def test_depth_pass_counts(gg, R, near, far, passes):
     """The depth-sort key is z bits - bits(near) (every record has near < z <= far),

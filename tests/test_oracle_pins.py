@@ -137,6 +137,42 @@ def test_project_mean_matches_pinhole():
         assert not np.any(vis[p[:, 2] <= 0.0])
 
 
+NEAR32, FAR32 = np.float32(0.01), np.float32(100.0)
+
+
+def near_far_fixture():
+    """Gaussians on the optical axis of an identity camera at the cull
+    boundaries.  With R = I, t = 0 the canonical p_z = ((0 mu_x + 0 mu_y) +
+    1 mu_z) + 0 is mu_z exactly, so each z below is the f32 value the
+    predicate p_z <= near or p_z > far sees."""
+    zs = [np.nextafter(NEAR32, np.float32(0)), NEAR32, np.nextafter(NEAR32, np.float32(1)),
+          np.float32(5.0), FAR32, np.nextafter(FAR32, np.float32(1e9)), np.float32(-1.0)]
+    expect = [False, False, True, True, True, False, False]
+    gs = [gi.single_gaussian([0.0, 0.0, float(z)], max(1e-3, float(z) * 1e-2) if z > 0 else 0.01, 0.8,
+                             [0.5, 0.5, 0.5]) for z in zs]
+    return gi.concat(gs), np.array(expect), np.array(zs, np.float32)
+
+
+def test_near_far_cull_boundaries():
+    """Visible iff near < p_z <= far, decided on the f32 value: z = near and
+    nextafter(near, 0) are culled, nextafter(near, +inf) is kept; z = far is
+    kept, nextafter(far, +inf) culled; behind the camera culled."""
+    sc, expect, zs = near_far_fixture()
+    assert sc.means[:, 2].tobytes() == zs.tobytes()
+    cams = gi.identity_cameras(1, 64, 48, 32.0)
+    os_ = oracle.OracleScene.from_inputs(sc)
+    r = oracle.render_env(os_, cams.viewmats[0], cams.intrinsics[0], 64, 48, near=float(NEAR32), far=float(FAR32))
+    vis = r.proj[:, PROJ_VIS] == 1
+    assert vis.tolist() == expect.tolist()
+    assert np.all(r.tile_counts[expect] > 0) and np.all(r.tile_counts[~expect] == 0)
+    assert np.array_equal(r.proj[expect, PROJ_Z], zs[expect])     # depth bits = mu_z
+    # shifting the planes by one ulp flips exactly the boundary Gaussians
+    r2 = oracle.render_env(os_, cams.viewmats[0], cams.intrinsics[0], 64, 48,
+                           near=float(np.nextafter(NEAR32, np.float32(0))), far=float(np.nextafter(FAR32, np.float32(0))))
+    vis2 = r2.proj[:, PROJ_VIS] == 1
+    assert vis2.tolist() == [False, True, True, True, False, False, False]
+
+
 def test_cov2_monte_carlo():
     """cov2d within 2% Frobenius of 1e5 Monte-Carlo projected
     samples (s/z <= 0.02), dilation removed.  Samples use scipy's rotation."""
