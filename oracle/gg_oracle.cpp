@@ -352,11 +352,28 @@ struct PixelOut {
   bool exempt;
 };
 
+// Near-miss flags (reading R28).  The definition is evaluated here
+// in f64; an f32 renderer evaluates the same records with rounding, so a
+// pixel is flagged ("exempt" candidate) when one of its decisions lies within
+// an f32 error bound of its threshold:
+//   cutoff  |alpha 255 - 1| < max(1e-4, da),
+//   stop    |T' / 1e-4 - 1| < max(1e-4, dT'),
+// da = relative error bound of an f32 alpha = ln2 e_x + 2^-21 (ex2 rounding),
+// e_x = 2^-21 M the f32 exponent's absolute error, M = the magnitude of the
+// exponent's terms expanded about the pixel's tile origin (the form a tiled
+// renderer evaluates: (log2 e / 2)(|A| + 2|B| + |C|)(max(|Dx|, |Dy|) + 16)^2
+// + |log2 o|, D = mean - the tile's first pixel centre); dT' = the relative
+// error bound of an f32 T' = sum over the blended pairs so far (and this one)
+// of alpha/(1 - alpha) da + 2^-22 per step (dT/T = sum dalpha/(1 - alpha)).
+// The flags mark candidates only; tests/parity.py caps the failures.
 template <typename Seq>
 PixelOut composite(const Seq& seq, const std::vector<Proj>& P, int px, int py, const double bg[3],
                    int flags) {
   const double cxp = px + 0.5, cyp = py + 0.5;     // pixel centre (reading R1)
+  const double tox = TILE * (px / TILE) + 0.5, toy = TILE * (py / TILE) + 0.5;   // tile origin (flags only)
+  const double HALF_LOG2E = 0.72134752044448170, LN2 = 0.69314718055994531;
   double T = 1.0, C[3] = {0, 0, 0}, Dn = 0.0, A = 0.0;
+  double relT = 0.0;                               // f32 error bound of T, relative (flags only)
   int32_t ne = 0, nc = 0;
   bool ex = false;
   for (int gid : seq) {
@@ -366,16 +383,25 @@ PixelOut composite(const Seq& seq, const std::vector<Proj>& P, int px, int py, c
     double q = g.A * dx * dx + 2.0 * g.B * dx * dy + g.C * dy * dy;
     q = std::max(q, 0.0);                                 // reading R13
     const double alpha = std::min(0.99, g.o * std::exp(-0.5 * q));
-    if (std::fabs(alpha * 255.0 - 1.0) < 1e-4) ex = true;   // cutoff near-miss
+    double dal = 1e-4;
+    if (g.o > 0.0) {
+      const double m = std::max(std::fabs(g.u - tox), std::fabs(g.v - toy)) + TILE;
+      const double M = HALF_LOG2E * (std::fabs(g.A) + 2.0 * std::fabs(g.B) + std::fabs(g.C)) * m * m +
+                       std::fabs(std::log2(g.o));
+      dal = LN2 * (M * 0x1p-21) + 0x1p-21;
+    }
+    if (std::fabs(alpha * 255.0 - 1.0) < std::max(1e-4, dal)) ex = true;   // cutoff near-miss
     if (alpha < 1.0 / 255.0) continue;                       // skip (reading R11)
     const double Tn = T * (1.0 - alpha);
-    if (std::fabs(Tn / 1e-4 - 1.0) < 1e-4) ex = true;       // early-out near-miss
+    const double dTn = relT + alpha / (1.0 - alpha) * dal + 0x1p-22;
+    if (std::fabs(Tn / 1e-4 - 1.0) < std::max(1e-4, dTn)) ex = true;   // early-out near-miss
     if (Tn < 1e-4 && !(flags & F_NO_EARLY_OUT)) break;       // stop, i not blended (R12)
     const double w = alpha * T;
     C[0] += w * g.col[0]; C[1] += w * g.col[1]; C[2] += w * g.col[2];
     Dn += w * g.z;
     A += w;
     T = Tn;
+    relT = dTn;
     ++nc;
   }
   PixelOut o;
