@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -17,8 +18,12 @@ namespace gg {
 void launch_validate(int64_t n, int K, const float* means, const float* scales, const float* quats,
                      const float* opac, const float* sh, ValidateOut* out, cudaStream_t s);
 void launch_pack(int64_t n, int K, int sh_stride, const float* means, const float* scales,
-                 const float* quats, const float* opac, const float* sh, float4* pos_op, float4* cov_a,
-                 float4* cov_b, float2* aux, float* qmax, float* sh_out, cudaStream_t s);
+                 const float* quats, const float* opac, const float* sh, const uint32_t* perm, float4* pos_op,
+                 float4* cov_a, float4* cov_b, float2* aux, float* qmax, float* sh_out, uint32_t* gid_out,
+                 cudaStream_t s);
+int launch_spatial_order(int64_t n, const float* means, uint32_t* box, uint32_t* tmp, uint32_t* hist,
+                         uint32_t* perm, cudaStream_t s);
+void launch_block_bounds(int n, const float4* pos_op, const float2* aux, float4* bbox, cudaStream_t s);
 void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, const float* viewmats,
                        const float* intr, const DevScene* scenes, int nscenes, int W, int H, int sh_degree,
                        EnvConst* out, uint32_t* err, cudaStream_t s);
@@ -84,8 +89,9 @@ static_assert(sizeof(Work) == Work::count * sizeof(DevBuf), "Work::count");
 
 struct SceneSlot {
   DevScene d{};
-  DevBuf pos_op, cov_a, cov_b, aux, qmax, sh;
+  DevBuf pos_op, cov_a, cov_b, aux, qmax, sh, gid, bbox;
   bool live = false;
+  void free_all(gg_context* ctx, cudaStream_t s);
 };
 
 constexpr int DEFAULT_CHUNK = 1024;
@@ -120,6 +126,7 @@ struct gg_context {
   uint64_t* h_kbase = nullptr;
   uint32_t* h_err = nullptr;
   int32_t* h_ids = nullptr;
+  float* h_vm = nullptr;        // view matrices (env ordering key)
   int32_t* h_perm = nullptr;
   EnvGroup* h_groups = nullptr;
   uint32_t* h_blkbase = nullptr;
@@ -187,6 +194,10 @@ void dev_free(gg_context* ctx, DevBuf& b, cudaStream_t s) {
   b.bytes = 0;
 }
 
+void SceneSlot::free_all(gg_context* ctx, cudaStream_t s) {
+  for (DevBuf* b : {&pos_op, &cov_a, &cov_b, &aux, &qmax, &sh, &gid, &bbox}) dev_free(ctx, *b, s);
+}
+
 // grow-only buffer
 bool ensure(gg_context* ctx, DevBuf& b, size_t bytes, cudaStream_t s) {
   if (b.bytes >= bytes && b.p) return true;
@@ -206,19 +217,20 @@ bool ensure_host(gg_context* ctx, int n) {
   if (ctx->h_cap >= n) return true;
   cudaDeviceSynchronize();   // in-flight copy kernels may still read/write the old mirrors
   const int cap = std::max(n, 1024);
-  void* p[8] = {};
-  const size_t sz[8] = {(size_t)(cap + 1) * 4, (size_t)cap * 4, (size_t)cap * 4, (size_t)cap * sizeof(EnvGroup),
-                        (size_t)cap * 4, (size_t)cap * 8, (size_t)cap * 8, (size_t)cap * 8};
-  for (int i = 0; i < 8; ++i) {
+  void* p[9] = {};
+  const size_t sz[9] = {(size_t)(cap + 1) * 4, (size_t)cap * 4, (size_t)cap * 4, (size_t)cap * sizeof(EnvGroup),
+                        (size_t)cap * 4, (size_t)cap * 8, (size_t)cap * 8, (size_t)cap * 8, (size_t)cap * 64};
+  for (int i = 0; i < 9; ++i) {
     if (cudaMallocHost(&p[i], sz[i]) != cudaSuccess) {
       cudaGetLastError();
       for (int j = 0; j < i; ++j) cudaFreeHost(p[j]);
       return false;
     }
   }
-  void** cur[8] = {(void**)&ctx->h_blkbase, (void**)&ctx->h_ids, (void**)&ctx->h_perm, (void**)&ctx->h_groups,
-                   (void**)&ctx->h_vcnt, (void**)&ctx->h_kcnt, (void**)&ctx->h_rbase, (void**)&ctx->h_kbase};
-  for (int i = 0; i < 8; ++i) {
+  void** cur[9] = {(void**)&ctx->h_blkbase, (void**)&ctx->h_ids, (void**)&ctx->h_perm, (void**)&ctx->h_groups,
+                   (void**)&ctx->h_vcnt, (void**)&ctx->h_kcnt, (void**)&ctx->h_rbase, (void**)&ctx->h_kbase,
+                   (void**)&ctx->h_vm};
+  for (int i = 0; i < 9; ++i) {
     if (*cur[i]) cudaFreeHost(*cur[i]);
     *cur[i] = p[i];
   }
@@ -314,10 +326,7 @@ gg_status gg_destroy(gg_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStream_t s = ctx->own;
   cudaDeviceSynchronize();
-  for (auto& sc : ctx->scenes) {
-    dev_free(ctx, sc.pos_op, s); dev_free(ctx, sc.cov_a, s); dev_free(ctx, sc.cov_b, s);
-    dev_free(ctx, sc.aux, s); dev_free(ctx, sc.qmax, s); dev_free(ctx, sc.sh, s);
-  }
+  for (auto& sc : ctx->scenes) sc.free_all(ctx, s);
   for (auto& e : ctx->tev) cudaEventDestroy(e);
   for (Work* w : {&ctx->sw, &ctx->aw})
     for (int i = 0; i < Work::count; ++i) dev_free(ctx, w->all()[i], s);
@@ -330,6 +339,7 @@ gg_status gg_destroy(gg_context* ctx) {
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
   cudaFreeHost(ctx->h_kbase); cudaFreeHost(ctx->h_err);
   cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
+  cudaFreeHost(ctx->h_vm);
   cudaEventDestroy(ctx->ev_copy);
   cudaStreamDestroy(s);
   delete ctx;
@@ -406,27 +416,42 @@ gg_status gg_load_scene(gg_context* ctx, int64_t n, int32_t d, const float* mean
   }
   SceneSlot slot;
   const int sh_stride = d > 0 ? ((K * 3 + 3) / 4) * 4 : 0;
+  const int64_t nblk = (n + PROJ_BLOCK - 1) / PROJ_BLOCK;
   bool ok = ensure(ctx, slot.pos_op, n * 16, s) && ensure(ctx, slot.cov_a, n * 16, s) &&
             ensure(ctx, slot.cov_b, n * 16, s) && ensure(ctx, slot.aux, n * 8, s) && ensure(ctx, slot.qmax, n * 4, s) &&
+            ensure(ctx, slot.gid, n * 4, s) && ensure(ctx, slot.bbox, nblk * 32, s) &&
             (d == 0 || ensure(ctx, slot.sh, (size_t)n * sh_stride * 4, s));
+  // spatial (Morton) storage order: scratch for the load-time sort
+  const bool spatial = getenv("GG_NO_SPATIAL_ORDER") == nullptr;   // A/B switch (input order when set)
+  DevBuf perm, tmp, hist, box;
+  if (ok && spatial)
+    ok = ensure(ctx, perm, n * 4, s) && ensure(ctx, tmp, n * 12, s) &&
+         ensure(ctx, hist, (size_t)((n + 255) / 256) * 16 * 4, s) && ensure(ctx, box, 32, s);
   if (!ok) {
     for (auto& b : stage) dev_free(ctx, b, s);
-    dev_free(ctx, slot.pos_op, s); dev_free(ctx, slot.cov_a, s); dev_free(ctx, slot.cov_b, s);
-    dev_free(ctx, slot.aux, s); dev_free(ctx, slot.qmax, s); dev_free(ctx, slot.sh, s);
+    for (DevBuf* b : {&perm, &tmp, &hist, &box}) dev_free(ctx, *b, s);
+    slot.free_all(ctx, s);
     return fail(ctx, GG_E_OOM, "gg_load_scene: out of device memory for %lld Gaussians", (long long)n);
   }
-  launch_pack(n, K, sh_stride, dsrc[0], dsrc[1], dsrc[2], dsrc[3], dsrc[4], P<float4>(slot.pos_op),
-              P<float4>(slot.cov_a), P<float4>(slot.cov_b), P<float2>(slot.aux), P<float>(slot.qmax),
-              d > 0 ? P<float>(slot.sh) : nullptr, s);
-  ctx->launches++;
+  if (spatial)
+    ctx->launches += launch_spatial_order(n, dsrc[0], P<uint32_t>(box), P<uint32_t>(tmp), P<uint32_t>(hist),
+                                          P<uint32_t>(perm), s);
+  launch_pack(n, K, sh_stride, dsrc[0], dsrc[1], dsrc[2], dsrc[3], dsrc[4], spatial ? P<uint32_t>(perm) : nullptr,
+              P<float4>(slot.pos_op), P<float4>(slot.cov_a), P<float4>(slot.cov_b), P<float2>(slot.aux),
+              P<float>(slot.qmax), d > 0 ? P<float>(slot.sh) : nullptr, P<uint32_t>(slot.gid), s);
+  launch_block_bounds((int)n, P<float4>(slot.pos_op), P<float2>(slot.aux), P<float4>(slot.bbox), s);
+  ctx->launches += 2;
   CK(cudaGetLastError());
   for (auto& b : stage) dev_free(ctx, b, s);
+  for (DevBuf* b : {&perm, &tmp, &hist, &box}) dev_free(ctx, *b, s);
   slot.d.pos_op = P<float4>(slot.pos_op);
   slot.d.cov_a = P<float4>(slot.cov_a);
   slot.d.cov_b = P<float4>(slot.cov_b);
   slot.d.aux = P<float2>(slot.aux);
   slot.d.qmax = P<float>(slot.qmax);
   slot.d.sh4 = d > 0 ? P<float4>(slot.sh) : nullptr;
+  slot.d.gid = P<uint32_t>(slot.gid);
+  slot.d.bbox = P<float4>(slot.bbox);
   slot.d.n = (int32_t)n;
   slot.d.degree = d;
   slot.d.sh_stride = sh_stride;
@@ -455,8 +480,7 @@ gg_status gg_unload_scene(gg_context* ctx, int32_t id) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaDeviceSynchronize());
   SceneSlot& sc = ctx->scenes[id];
-  dev_free(ctx, sc.pos_op, ctx->own); dev_free(ctx, sc.cov_a, ctx->own); dev_free(ctx, sc.cov_b, ctx->own);
-  dev_free(ctx, sc.aux, ctx->own); dev_free(ctx, sc.qmax, ctx->own); dev_free(ctx, sc.sh, ctx->own);
+  sc.free_all(ctx, ctx->own);
   sc.live = false;
   sc.d = DevScene{};
   return upload_scene_table(ctx);
@@ -604,11 +628,22 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   }
   CK(cudaMemsetAsync(ctx->errflag.p, 0, 4, s));
 
-  // Scene-sorted env order (stable): envs bound to one scene become
-  // contiguous, so the projection kernels can share each Gaussian load
-  // across a group of envs.  Outputs are still written at the caller's
-  // env index (EnvConst.out_index).
+  // Processing order of the envs (outputs are still written at the caller's
+  // env index, EnvConst.out_index, and every env's result depends only on its
+  // own camera and scene, so the order changes no output bit): envs bound to
+  // one scene become contiguous, so the projection kernels share each
+  // Gaussian load across a group of <= 16 envs; inside a scene, envs are
+  // ordered by view direction (a cube-map face of the forward axis, 2 x 2
+  // cells per face) and then by the Morton code of the camera centre, so the
+  // envs of a group look at the same storage blocks: whole (group, block)
+  // tiles of the cull then fail the block test together and the projection's
+  // pair lists get denser (spatial chunk culling).  With
+  // host outputs (gg_render_host) the order is first by windows of
+  // HOST_COPY_SLICE caller envs, so each raster slice's frames are one
+  // contiguous range of the caller's buffer (one copy per slice).
   ctx->launches += launch_copy_words(ctx->h_ids, scene_ids, (size_t)E * 4, s);
+  const bool view_order = getenv("GG_NO_ENV_ORDER") == nullptr;   // A/B switch
+  if (view_order) ctx->launches += launch_copy_words(ctx->h_vm, viewmats, (size_t)E * 64, s);
   CK(cudaStreamSynchronize(s));
   const int nsc = (int)ctx->scenes.size();
   auto key = [&](int e) {
@@ -617,7 +652,48 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   };
   std::vector<int32_t> order(E);
   for (int e = 0; e < E; ++e) order[e] = e;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
+  std::vector<uint32_t> vkey(view_order ? E : 0);
+  if (view_order) {
+    float lo[3] = {1e30f, 1e30f, 1e30f}, hi[3] = {-1e30f, -1e30f, -1e30f};
+    std::vector<float> cc((size_t)E * 3);
+    for (int e = 0; e < E; ++e) {
+      const float* V = ctx->h_vm + (size_t)e * 16;
+      for (int k = 0; k < 3; ++k) {
+        const float c = -(V[0 * 4 + k] * V[3] + V[1 * 4 + k] * V[7] + V[2 * 4 + k] * V[11]);
+        cc[(size_t)e * 3 + k] = std::isfinite(c) ? c : 0.f;
+        lo[k] = std::min(lo[k], cc[(size_t)e * 3 + k]);
+        hi[k] = std::max(hi[k], cc[(size_t)e * 3 + k]);
+      }
+    }
+    auto spread = [](uint32_t x) {   // 4 bits -> every third bit
+      uint32_t r = 0;
+      for (int b = 0; b < 4; ++b) r |= ((x >> b) & 1u) << (3 * b);
+      return r;
+    };
+    for (int e = 0; e < E; ++e) {
+      const float* F = ctx->h_vm + (size_t)e * 16 + 8;   // forward axis (row 2 of R) in world coordinates
+      int ax = 0;
+      for (int k = 1; k < 3; ++k)
+        if (std::fabs(F[k]) > std::fabs(F[ax])) ax = k;
+      const float m = std::fabs(F[ax]) > 0.f ? std::fabs(F[ax]) : 1.f;
+      const float a = F[(ax + 1) % 3] / m, b = F[(ax + 2) % 3] / m;   // in [-1, 1] on the face
+      const uint32_t face = (uint32_t)(2 * ax + (F[ax] < 0.f));
+      const uint32_t cell = (a >= 0.f ? 1u : 0u) | (b >= 0.f ? 2u : 0u);
+      uint32_t pos = 0;
+      for (int k = 0; k < 3; ++k) {
+        const float ext = hi[k] - lo[k];
+        const uint32_t qk = ext > 0.f ? (uint32_t)std::min(15.f, std::max(0.f, (cc[(size_t)e * 3 + k] - lo[k]) / ext * 16.f)) : 0u;
+        pos |= spread(qk) << k;
+      }
+      vkey[e] = ((face * 4 + cell) << 12) | pos;
+    }
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    if (cb && a / HOST_COPY_SLICE != b / HOST_COPY_SLICE) return a / HOST_COPY_SLICE < b / HOST_COPY_SLICE;
+    const int ka = key(a), kb = key(b);
+    if (ka != kb) return ka < kb;
+    return view_order && vkey[a] < vkey[b];
+  });
   int dbg_pos = -1;
   for (int p = 0; p < E; ++p) {
     ctx->h_perm[p] = order[p];
@@ -628,7 +704,6 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
                     opts.sh_degree, P<EnvConst>(ctx->sw.envc), P<uint32_t>(ctx->errflag), s);
   ctx->launches++;
   CK(cudaGetLastError());
-  if (keep && !ensure(ctx, ctx->sw.gid, 16, s)) return fail(ctx, GG_E_OOM, "alloc");
 
   ctx->t_nchunks = 0;
   int cidx = 0;
@@ -685,7 +760,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     for (int i = 0; i < ec; ++i) { ctx->h_rbase[i] = V; V += ctx->h_vcnt[i]; }
     if (!ensure(ctx, ctx->sw.rec0, V * 16, s) || !ensure(ctx, ctx->sw.rec1, V * 16, s) ||
         !ensure(ctx, ctx->sw.rec2, V * 16, s) || !ensure(ctx, ctx->sw.rect, V * 8, s) ||
-        !ensure(ctx, ctx->sw.zkey, V * 4, s) || (keep && !ensure(ctx, ctx->sw.gid, V * 4, s)) ||
+        !ensure(ctx, ctx->sw.zkey, V * 4, s) || !ensure(ctx, ctx->sw.gid, V * 4, s) ||
         (rp.ellipse && !ensure(ctx, ctx->sw.rmask, V * 4 + 4, s)) ||
         (keep && !ensure(ctx, ctx->sw.dconic, V * 16, s)) ||
         !ensure(ctx, ctx->sw.dk0, V * 8, s) || !ensure(ctx, ctx->sw.dk1, V * 8, s) ||
@@ -697,7 +772,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ws.rec0 = P<float4>(ctx->sw.rec0); ws.rec1 = P<float4>(ctx->sw.rec1); ws.rec2 = P<float4>(ctx->sw.rec2);
     ws.rect = P<uint2>(ctx->sw.rect); ws.zkey = P<uint32_t>(ctx->sw.zkey);
     ws.rmask = rp.ellipse ? P<uint32_t>(ctx->sw.rmask) : nullptr;
-    ws.gid = keep ? P<uint32_t>(ctx->sw.gid) : nullptr;
+    ws.gid = P<uint32_t>(ctx->sw.gid);
     ws.dconic = keep ? P<float4>(ctx->sw.dconic) : nullptr;
     ws.dp0 = P<uint64_t>(ctx->sw.dk0); ws.dp1 = P<uint64_t>(ctx->sw.dk1); ws.order = P<uint32_t>(ctx->sw.dv0);
     // K1b
@@ -878,7 +953,7 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     ws.rec_base = P<uint64_t>(ctx->aw.rbase);
     ws.k_base = P<uint64_t>(ctx->aw.kbase);
     ws.rec0 = P<float4>(ctx->aw.rec0); ws.rec1 = P<float4>(ctx->aw.rec1); ws.rec2 = P<float4>(ctx->aw.rec2);
-    ws.rect = P<uint2>(ctx->aw.rect); ws.zkey = P<uint32_t>(ctx->aw.zkey);
+    ws.rect = P<uint2>(ctx->aw.rect); ws.zkey = P<uint32_t>(ctx->aw.zkey); ws.gid = P<uint32_t>(ctx->aw.gid);
     ws.rmask = rp.ellipse ? P<uint32_t>(ctx->aw.rmask) : nullptr;
     ws.zbase = f32_bits(opts.near_plane);
     ws.dp0 = P<uint64_t>(ctx->aw.dk0); ws.dp1 = P<uint64_t>(ctx->aw.dk1); ws.order = P<uint32_t>(ctx->aw.dv0);
@@ -945,6 +1020,7 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
              ensure(ctx, ctx->aw.counters, (size_t)max_envs * 32, s) && ensure(ctx, ctx->aw.rec0, vcap * 16, s) &&
              ensure(ctx, ctx->aw.rec1, vcap * 16, s) && ensure(ctx, ctx->aw.rec2, vcap * 16, s) &&
              ensure(ctx, ctx->aw.rect, vcap * 8, s) && ensure(ctx, ctx->aw.zkey, vcap * 4, s) &&
+             ensure(ctx, ctx->aw.gid, vcap * 4, s) &&
              ensure(ctx, ctx->aw.rmask, vcap * 4 + 4, s) &&
              ensure(ctx, ctx->aw.dk0, vcap * 8, s) && ensure(ctx, ctx->aw.dk1, vcap * 8, s) &&
              ensure(ctx, ctx->aw.dv0, vcap * 4, s) &&

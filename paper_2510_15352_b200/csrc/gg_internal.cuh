@@ -26,6 +26,8 @@ struct DevScene {
   const float2* aux;     // (dc_b, max_j s_j^2)
   const float* qmax;     // f32(2 ln(255 o)): alpha >= 1/255 <=> q <= qmax (reading R35)
   const float4* sh4;     // [sh_stride/4][n] float4 planes of the (k, ch) coefficients, zero padded; null if d = 0
+  const uint32_t* gid;   // [n] input index of each stored Gaussian (storage is in Morton order of the means)
+  const float4* bbox;    // [2 * nblk] per PROJ_BLOCK storage block: (lo.xyz, max scale), (hi.xyz, 0)
   int32_t n;
   int32_t degree;
   int32_t sh_stride;     // floats per Gaussian (multiple of 4) = 4 x planes
@@ -98,7 +100,7 @@ struct ChunkWS {
   uint32_t* rmask;      // [V] R37 kept-tile masks of <= 32-tile rects (null: variant off)
   uint32_t* zkey;       // f32 bits of z
   uint32_t zbase;       // f32 bits of the near plane: depth-sort key = z bits - zbase, in (0, bits(far) - zbase]
-  uint32_t* gid;        // Gaussian index (debug dumps only; may be null)
+  uint32_t* gid;        // input (gid) index of each record: the tie-break of equal depth keys, debug dumps
   // depth-sort scratch [V]: packed (key - zmin) << 32 | record ping-pong, and
   // the last pass's output (records in depth order)
   uint64_t* dp0; uint64_t* dp1;

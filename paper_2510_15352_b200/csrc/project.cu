@@ -132,16 +132,81 @@ __device__ __forceinline__ bool maybe_visible(const EnvConst& c, float4 g, float
   return (u + rb > 0.f) && (u - rb < (float)(rp.TX * TILE)) && (v + rb > 0.f) && (v - rb < (float)(rp.TY * TILE));
 }
 
+// Block test (per-scene spatial chunk culling): can any
+// Gaussian of a storage block -- means in [lo, hi], scales <= smax -- have a
+// non-empty canonical tile rect for this camera?  A NECESSARY condition, so
+// a culled block never holds a visible Gaussian:
+//   near < p_z <= far for some mean of the box, and the 4 screen-edge
+//   conditions u + r > 0, u - r < 16 TX (v alike) with r = ceil(3 sqrt(l1))
+//   < 3 sqrt(l1) + 1, l1 <= a + c + 0.32 <= smax^2 |T|_F^2 + 0.92 and
+//   |T|_F^2 <= rgram |J|_F^2 <= rgram G / p_z^2, G = fx^2 (1 + limx^2) +
+//   fy^2 (1 + limy^2) (clamped Jacobian).  Multiplied by p_z > 0 each edge
+//   condition is linear in the mean: e.g. fx p_x + (cx + 3.88) p_z +
+//   3 smax sqrt(rgram G) > 0, whose maximum over the box is exact.
+// Evaluated in f32 with a relative tolerance that covers its rounding.
+__device__ __forceinline__ bool block_may_see(const EnvConst& c, float4 b0, float4 b1, const RenderParams& rp) {
+  const float lo[3] = {b0.x, b0.y, b0.z}, hi[3] = {b1.x, b1.y, b1.z};
+  float mx[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) mx[k] = fmaxf(fabsf(lo[k]), fabsf(hi[k]));
+  // max over the box of n . mu + d, and a bound on the magnitude of its terms
+  auto maxlin = [&](float n0, float n1, float n2, float d, float& mag) {
+    mag = fabsf(n0) * mx[0] + fabsf(n1) * mx[1] + fabsf(n2) * mx[2] + fabsf(d);
+    return fmaxf(n0 * lo[0], n0 * hi[0]) + fmaxf(n1 * lo[1], n1 * hi[1]) + fmaxf(n2 * lo[2], n2 * hi[2]) + d;
+  };
+  const float rel = 1e-4f;
+  float mag;
+  const float zmax = maxlin(c.R[6], c.R[7], c.R[8], c.t[2], mag);
+  if (zmax + rel * mag + 1e-6f <= rp.near_p) return false;
+  const float zmin = -maxlin(-c.R[6], -c.R[7], -c.R[8], -c.t[2], mag);
+  if (zmin - rel * mag - 1e-6f > rp.far_p) return false;
+  const float limx = fmaxf(c.lim_xp, c.lim_xn), limy = fmaxf(c.lim_yp, c.lim_yn);
+  const float G = c.fx * c.fx * (1.f + limx * limx) + c.fy * c.fy * (1.f + limy * limy);
+  const float m = 3.f * b0.w * sqrtf(c.rgram * G) * 1.01f;   // 3 smax |J|_F p_z, with slack
+  const float CR = 3.88f;                                     // 3 sqrt(0.92) + 1, rounded up
+  const float Wp = (float)(rp.TX * TILE), Hp = (float)(rp.TY * TILE);
+  // u + r > 0 ; u - r < Wp ; v + r > 0 ; v - r < Hp  (each times p_z)
+  const float ax[4] = {c.fx, -c.fx, 0.f, 0.f}, ay[4] = {0.f, 0.f, c.fy, -c.fy};
+  const float az[4] = {c.cx + CR, Wp - c.cx + CR, c.cy + CR, Hp - c.cy + CR};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float n0 = ax[e] * c.R[0] + ay[e] * c.R[3] + az[e] * c.R[6];
+    const float n1 = ax[e] * c.R[1] + ay[e] * c.R[4] + az[e] * c.R[7];
+    const float n2 = ax[e] * c.R[2] + ay[e] * c.R[5] + az[e] * c.R[8];
+    const float d = ax[e] * c.t[0] + ay[e] * c.t[1] + az[e] * c.t[2];
+    const float v = maxlin(n0, n1, n2, d, mag);
+    if (v + m + rel * (mag + m) + 1e-3f <= 0.f) return false;
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(PROJ_BLOCK)
 cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
                   const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
   __shared__ EnvConst cams[ENV_GROUP];
   __shared__ uint32_t wc[ENV_GROUP][PROJ_BLOCK / 32];
+  __shared__ uint32_t bvis;   // bit k: env k may see some Gaussian of this storage block
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0) return;
   load_group_cams(cams, envs, e0, grp);
+  if (threadIdx.x == 0) bvis = 0u;
   __syncthreads();
+  if (threadIdx.x < grp.cnt) {
+    const EnvConst c = load_cam(&cams[threadIdx.x]);
+    if (c.n > (int)(blockIdx.y * PROJ_BLOCK)) {
+      const DevScene& sc = scenes[c.scene];
+      if (block_may_see(c, __ldg(&sc.bbox[2 * blockIdx.y]), __ldg(&sc.bbox[2 * blockIdx.y + 1]), rp))
+        atomicOr(&bvis, 1u << threadIdx.x);
+    }
+  }
+  __syncthreads();
+  const uint32_t bv = bvis;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (bv == 0u) {   // the whole block is outside every camera of the group
+    if (lane < grp.cnt) ws.flags[(size_t)(grp.elo + lane) * ws.nwords + blockIdx.y * (PROJ_BLOCK / 32) + warp] = 0u;
+    if (threadIdx.x < grp.cnt) ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blockIdx.y] = 0u;
+    return;
+  }
   const int i = blockIdx.y * PROJ_BLOCK + threadIdx.x;
   int cur = -2;                       // scene whose Gaussian i is in registers
   float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -150,7 +215,8 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
   // lane k keeps env k's visibility word (no per-env branch in the loop;
   // ENV_GROUP <= 32)
   uint32_t my_word = 0u;
-  for (int k = 0; k < grp.cnt; ++k) {
+  for (uint32_t bm = bv; bm; bm &= bm - 1u) {   // only the envs whose block test passed (CTA-uniform)
+    const int k = __ffs(bm) - 1;
     const EnvConst c = load_cam(&cams[k]);
     if (c.scene != cur) {             // uniform across the CTA
       cur = c.scene;
@@ -340,12 +406,20 @@ struct ProjSmem {
   CamWord camT[CAM_F2][ENV_GROUP];
   uint32_t fw[ENV_GROUP * PROJ_WPB];   // visibility words (env, word)
   uint32_t cnt[ENV_GROUP * PROJ_WPB];  // popc per (env, word), then exclusive prefix within the env
-  uint32_t wsum[PROJ_BLOCK / 32];
   uint32_t kacc[ENV_GROUP];
-  uint32_t total;
-  uint16_t list[ENV_GROUP * PROJ_BLOCK];   // (k << PROJ_LB) | local
+  uint32_t nunits;
+  uint8_t units[ENV_GROUP * PROJ_WPB]; // non-empty (word, env) units, word-major: (w << 4) | k
 };
 
+// Work decomposition (DESIGN.md §4 K1b).  A unit = one visibility word (32
+// consecutive storage Gaussians) x one env of the group; a warp projects the
+// unit's visible Gaussians, lane l taking the l-th set bit.  The unit's
+// records are consecutive slots of its env (rank = the set bits before it),
+// so a warp's stores are contiguous runs, its scene loads are consecutive
+// Gaussians, its camera is warp-uniform, and the warps of the CTA walk the
+// block word by word (all envs of word w before word w + 1), so the 32
+// Gaussians being projected stay in L1.  With the Morton storage order a
+// non-empty word is ~90% full (visibility is spatially coherent).
 template <bool ELL>   // GG_ELLIPSE_TILES (reading R37): per-record tile masks
 __global__ void __launch_bounds__(PROJ_BLOCK, 1024 / PROJ_BLOCK)
 project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
@@ -353,17 +427,13 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   __shared__ ProjSmem sm;
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0 || !chunk_ok(ws.ok)) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gblk = blockIdx.y;
   const int i0 = gblk * PROJ_BLOCK;
   {
     const CamWord* src = reinterpret_cast<const CamWord*>(envs + e0 + grp.elo);
     for (int i = threadIdx.x; i < grp.cnt * CAM_F2; i += blockDim.x) sm.camT[i % CAM_F2][i / CAM_F2] = src[i];
   }
-  // visibility words of the group -> (Gaussian, env) pair list in (gid, env)
-  // order: lanes that share a Gaussian read the same scene lines (L1
-  // broadcast) and a warp touches only a few adjacent Gaussians.  A record's index is its rank within its env (gid order),
-  // which does not depend on which thread computes it.
   for (int q = tid; q < ENV_GROUP * PROJ_WPB; q += PROJ_BLOCK) {
     const int k = q / PROJ_WPB, w = q % PROJ_WPB;
     uint32_t word = 0;
@@ -373,7 +443,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   }
   if (tid < ENV_GROUP) sm.kacc[tid] = 0;
   __syncthreads();
-  if (tid < ENV_GROUP) {   // per env: exclusive prefix of its 8 word counts
+  if (tid < ENV_GROUP) {   // per env: exclusive prefix of its word counts
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < PROJ_WPB; ++w) {
@@ -381,54 +451,29 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
       sm.cnt[tid * PROJ_WPB + w] = run;
       run += c;
     }
-  }
-  // this thread's Gaussian: mask of the group's envs that see it
-  uint32_t emask = 0;
-  {
-    const int w = tid >> 5, b = tid & 31;
-#pragma unroll
-    for (int k = 0; k < ENV_GROUP; ++k) emask |= ((sm.fw[k * PROJ_WPB + w] >> b) & 1u) << k;
-  }
-  const uint32_t ecnt = __popc(emask);
-  {
-    const int lane = tid & 31, warp = tid >> 5;
-    uint32_t incl = ecnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
+  } else if (warp == 1) {  // non-empty units, word-major (w << 4 | k)
+    uint32_t n = 0;
+    for (int u0 = 0; u0 < ENV_GROUP * PROJ_WPB; u0 += 32) {
+      const int u = u0 + lane, w = u / ENV_GROUP, k = u % ENV_GROUP;
+      const bool live = u < ENV_GROUP * PROJ_WPB && sm.fw[k * PROJ_WPB + w] != 0u;
+      const uint32_t m = __ballot_sync(0xffffffffu, live);
+      if (live) sm.units[n + __popc(m & ((1u << lane) - 1u))] = (uint8_t)((w << 4) | k);
+      n += __popc(m);
     }
-    if (lane == 31) sm.wsum[warp] = incl;
-    __syncthreads();
-    if (tid == 0) {
-      uint32_t run = 0;
-#pragma unroll
-      for (int q = 0; q < PROJ_BLOCK / 32; ++q) {
-        const uint32_t c = sm.wsum[q];
-        sm.wsum[q] = run;
-        run += c;
-      }
-      sm.total = run;
-    }
-    __syncthreads();
-    uint32_t o = sm.wsum[warp] + incl - ecnt;
-    uint32_t m = emask;
-    while (m) {
-      const int k = __ffs(m) - 1;
-      m &= m - 1;
-      sm.list[o++] = (uint16_t)((k << PROJ_LB) | tid);
-    }
+    if (lane == 0) sm.nunits = n;
   }
-  const uint32_t total = sm.total;
-  if (total == 0) return;
-  __syncthreads();   // the pair list is complete
-  for (uint32_t s = tid; s < total; s += PROJ_BLOCK) {
-    const uint32_t ent = sm.list[s];
-    const int k = ent >> PROJ_LB, l = ent & (PROJ_BLOCK - 1);
+  __syncthreads();
+  const uint32_t nunits = sm.nunits;
+  for (uint32_t j = warp; j < nunits; j += PROJ_BLOCK / 32) {
+    const uint32_t unit = sm.units[j];
+    const int w = (int)(unit >> 4), k = (int)(unit & 15u);
+    const uint32_t word = sm.fw[k * PROJ_WPB + w];
+    uint32_t ntiles = 0;
+    if (lane < __popc(word)) {
+      const int l = w * 32 + (int)__fns(word, 0u, lane + 1);   // the lane-th visible Gaussian of the word
     const EnvConst c = load_cam_t(sm.camT, k);
     const int eloc = grp.elo + k;
-    const uint32_t rank = sm.cnt[k * PROJ_WPB + (l >> 5)] + __popc(sm.fw[k * PROJ_WPB + (l >> 5)] & ((1u << (l & 31)) - 1u));
-    const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + rank;
+    const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + sm.cnt[k * PROJ_WPB + w] + lane;
     const DevScene& scn = scenes[c.scene];
     const int gi = i0 + l;
     // the scene is read through L1: lanes of a warp share few, adjacent
@@ -487,7 +532,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
         if (rp.tight) qm_r = tight_rect(u, v, cA, cB, cC, __ldg(&scn.qmax[gi]), x0, x1, y0, y1);
       }
     }
-    uint32_t ntiles = (x1 - x0) * (y1 - y0);
+    ntiles = (x1 - x0) * (y1 - y0);
     if (ELL) {
       uint32_t m = 0xffffffffu;
       if (ntiles > 0u && ntiles <= 32u && qm_r < __int_as_float(0x7f800000)) {
@@ -536,11 +581,13 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     ws.rec2[r] = make_float4(col[0], col[1], col[2], ey);
     ws.rect[r] = make_uint2(x0 | (x1 << 16), y0 | (y1 << 16));
     ws.zkey[r] = __float_as_uint(p.z);
-    if (ws.gid) {
-      ws.gid[r] = (uint32_t)(i0 + l);
-      ws.dconic[r] = make_float4(cA, cB, cC, exp2f(L));
+    ws.gid[r] = __ldg(&scn.gid[gi]);                  // input index: the depth sort's tie-break
+    if (ws.dconic) ws.dconic[r] = make_float4(cA, cB, cC, exp2f(L));
     }
-    if (ntiles) atomicAdd(&sm.kacc[k], ntiles);
+    // the unit's tile keys -> its env's key count (one shared atomic per unit)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ntiles += __shfl_xor_sync(0xffffffffu, ntiles, o);
+    if (lane == 0 && ntiles) atomicAdd(&sm.kacc[k], ntiles);
   }
   __syncthreads();
   if (tid < grp.cnt && sm.kacc[tid]) atomicAdd(&ws.kcnt[grp.elo + tid], (unsigned long long)sm.kacc[tid]);

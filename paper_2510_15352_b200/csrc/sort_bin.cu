@@ -52,7 +52,7 @@ constexpr int DS_WARPS = DS_THREADS / 32;
 constexpr int DS_IPT = SORT_BLK / DS_THREADS;
 constexpr int DS_BITS = 10;                     // digit width of the depth passes
 constexpr int DS_RADIX = 1 << DS_BITS;
-constexpr int SORT_QCTR = 16;                   // async-mode work counters per chunk (2 per pass + 2)
+constexpr int SORT_QCTR = 16;                   // async-mode work counters per chunk (2 per pass + 3)
 
 // blocks of the chunk: env of block b is the e with blk_base[e] <= b < blk_base[e+1],
 // tabulated once per chunk (blk_env_kernel) so a block finds it with one load
@@ -136,6 +136,7 @@ struct DepthIO {
   const uint64_t* pin;   // later passes: packed (z bits - zbase) << 32 | record
   uint64_t* pout;        // packed out (null on the last pass)
   uint32_t* vout;        // last pass: records in depth order
+  uint32_t* kout;        // last pass: their keys (the tie fix-up reads them)
 };
 
 __device__ __forceinline__ uint32_t depth_digit(uint32_t key, int shift) {
@@ -329,9 +330,12 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
     }
   } else {
     uint32_t* vout = io.vout + rb;
+    uint32_t* kout = io.kout + rb;
     for (uint32_t q = tid; q < n; q += DS_THREADS) {
       const uint64_t xx = sm.u.o.sp[q];
-      vout[sm.dstart[depth_digit((uint32_t)(xx >> 32), shift)] + q] = (uint32_t)xx;
+      const uint32_t at = sm.dstart[depth_digit((uint32_t)(xx >> 32), shift)] + q;
+      vout[at] = (uint32_t)xx;
+      kout[at] = (uint32_t)(xx >> 32);
     }
   }
 }
@@ -354,6 +358,85 @@ depth_downsweep_kernel(BlockTable bt, ChunkWS ws, DepthIO io, int shift, const u
     const uint32_t b = next_block(bt.q);
     if (b >= nb) break;
     depth_downsweep_block(b, bt, ws, io, shift, ghist, sm);
+  }
+}
+
+// ---- tie fix-up ------------------------------------------------------------
+// The records of an env are in storage order (Morton order of the means, not
+// input order), so the stable depth sort leaves exactly-equal depth keys in
+// storage order.  The canonical order breaks them by gid (SPEC.md:139
+// "ties broken by input index"; DESIGN.md §2 O3): every run of equal keys
+// (a few hundred short runs per env: coincident f32 depths) is re-sorted by
+// gid in place, by the thread that owns the run's first position.
+__device__ __noinline__ void sort_run_by_gid(uint32_t* __restrict__ o, uint32_t len, const uint32_t* __restrict__ gid) {
+  if (len == 2) {                                   // the common run: one compare
+    const uint32_t r0 = o[0], r1 = o[1];
+    if (gid[r0] > gid[r1]) { o[0] = r1; o[1] = r0; }
+    return;
+  }
+  // shell sort in place (a long run of exact ties, e.g. duplicated
+  // Gaussians, stays O(len^1.3)); gaps 3h+1 below len
+  uint32_t gap = 1;
+  while (gap < len / 3) gap = 3 * gap + 1;
+  for (; gap > 0; gap /= 3) {
+    for (uint32_t i = gap; i < len; ++i) {
+      const uint32_t r = o[i], g = gid[r];
+      uint32_t k = i;
+      while (k >= gap && gid[o[k - gap]] > g) {
+        o[k] = o[k - gap];
+        k -= gap;
+      }
+      o[k] = r;
+    }
+  }
+}
+
+// One CTA per sort block (its env's bounds are known): 8 keys per thread and
+// step in two 128-bit loads; the rare tie (an equal successor) is resolved by
+// the thread owning the run's first position.
+constexpr int TIES_THREADS = 256;
+__device__ __forceinline__ void ties_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws, const uint32_t* keys) {
+  const int e = block_env(bt, b);
+  const uint32_t V = ws.vcnt[e];
+  const uint32_t j0 = (b - bt.blk_base[e]) * SORT_BLK;
+  const uint32_t n = min((uint32_t)SORT_BLK, V - j0);
+  const uint64_t rb = ws.rec_base[e];
+  const uint32_t* __restrict__ K = keys + rb;
+  for (uint32_t q = threadIdx.x * 8; q < n; q += TIES_THREADS * 8) {
+    const uint32_t j = j0 + q;
+    uint32_t k[9];
+    if (((rb + j) & 3u) == 0u && q + 8 <= n) {      // 16-B aligned: two 128-bit loads
+      const uint4 a = *reinterpret_cast<const uint4*>(K + j), c = *reinterpret_cast<const uint4*>(K + j + 4);
+      k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w; k[4] = c.x; k[5] = c.y; k[6] = c.z; k[7] = c.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) k[i] = q + i < n ? K[j + i] : 0u;
+    }
+    k[8] = j + 8 < V ? K[j + 8] : 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t p = j + i;
+      if (q + i >= n || p + 1 >= V || k[i + 1] != k[i]) continue;   // no equal successor (the common case)
+      if (p > 0 && (i > 0 ? k[i - 1] : K[p - 1]) == k[i]) continue;  // not the run's first position
+      uint32_t end = p + 2;
+      while (end < V && K[end] == k[i]) ++end;
+      sort_run_by_gid(ws.order + rb + p, end - p, ws.gid + rb);
+    }
+  }
+}
+
+template <bool LOOP>
+__global__ void __launch_bounds__(TIES_THREADS) depth_ties_kernel(BlockTable bt, ChunkWS ws, const uint32_t* keys) {
+  if (!chunk_ok(ws.ok)) return;
+  const uint32_t nb = bt.blk_base[bt.ec];
+  if (!LOOP) {
+    if (blockIdx.x < nb) ties_block(blockIdx.x, bt, ws, keys);
+    return;
+  }
+  for (;;) {
+    const uint32_t b = next_block(bt.q);
+    if (b >= nb) break;
+    ties_block(b, bt, ws, keys);
   }
 }
 
@@ -697,6 +780,7 @@ static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, con
     io.pin = p == 0 ? nullptr : ((p & 1) ? ws.dp0 : ws.dp1);
     io.pout = p == passes - 1 ? nullptr : ((p & 1) ? ws.dp1 : ws.dp0);
     io.vout = ws.order;
+    io.kout = reinterpret_cast<uint32_t*>((p & 1) ? ws.dp1 : ws.dp0);   // free on the last pass (it reads the other)
     if (LOOP) bt.q = qctr + qi++;
     depth_upsweep_kernel<LOOP><<<g1, DS_THREADS, 0, s>>>(bt, ws, io, DS_BITS * p, ghist);
     depth_scan_kernel<<<ec, DS_RADIX, 0, s>>>(bt, ghist, ws.ok);
@@ -704,6 +788,11 @@ static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, con
     depth_downsweep_kernel<LOOP><<<g1, DS_THREADS, depth_down_smem(), s>>>(bt, ws, io, DS_BITS * p, ghist);
     launches += 3;
   }
+  // gid order inside runs of equal depth keys (records are in storage order)
+  if (LOOP) bt.q = qctr + qi++;
+  depth_ties_kernel<LOOP><<<g1, TIES_THREADS, 0, s>>>(
+      bt, ws, reinterpret_cast<const uint32_t*>(((passes - 1) & 1) ? ws.dp1 : ws.dp0));
+  launches += 1;
   if (after_depth) cudaEventRecord(after_depth, s);   // stage timing: depth passes | placement
   const uint32_t* order = ws.order;   // records of the last depth pass
   if (LOOP) bt.q = qctr + qi++;
