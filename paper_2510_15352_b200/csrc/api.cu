@@ -47,8 +47,6 @@ void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp,
                    int dbg_eloc, cudaStream_t s);
 void launch_blur_poses(int E, int K, int Kc, const float* viewmats, const float* lin, const float* ang,
                        float shutter, float* out, cudaStream_t s);
-void launch_blur_average(int ec, int e0, int K, int Kc, int dk, size_t P, const float* srgb, const float* sdepth,
-                         const float* salpha, int rgb_format, void* rgb, float* depth, float* alpha, cudaStream_t s);
 void launch_blur_expand(int ec, int K, const int32_t* ids, const float* intr, int32_t* ids_k, float* intr_k,
                         cudaStream_t s);
 void launch_tables_v(int ec, const uint32_t* vcnt, uint64_t* rbase, uint64_t vcap, uint32_t* ok, uint32_t* err,
@@ -118,7 +116,7 @@ struct gg_context {
   DevBuf errflag, valid_out;
   DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval;
   DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
-  DevBuf blur_vm, blur_ids, blur_intr, blur_rgb, blur_depth, blur_alpha;   // gg_render_blur
+  DevBuf blur_vm, blur_ids, blur_intr;   // gg_render_blur sample cameras
   // pinned host mirrors
   uint32_t* h_vcnt = nullptr;
   uint64_t* h_kcnt = nullptr;
@@ -141,7 +139,7 @@ struct gg_context {
   float stage_ms[NSTAGE] = {0, 0, 0, 0, 0};
   std::vector<cudaEvent_t> tev;   // per-chunk stage events [chunk][NSTAGE + 1], resolved lazily
   int t_nchunks = 0;              // chunks of the last timed render not yet resolved
-  int t_used = 0;                 // events handed out in the current render
+  bool t_append = false;          // gg_render_blur: its render_impl calls add to one timing record
   cudaEvent_t ev_copy = nullptr;
   int last_E = 0;
   // sync-free mode (gg_reserve_async)
@@ -333,7 +331,7 @@ gg_status gg_destroy(gg_context* ctx) {
   DevBuf* all[] = {&ctx->scene_table, &ctx->errflag, &ctx->valid_out,
                    &ctx->dbg_tc, &ctx->dbg_proj, &ctx->dbg_stile, &ctx->dbg_sz, &ctx->dbg_sgid,
                    &ctx->dbg_neval, &ctx->h_in, &ctx->blur_vm, &ctx->blur_ids,
-                   &ctx->blur_intr, &ctx->blur_rgb, &ctx->blur_depth, &ctx->blur_alpha};
+                   &ctx->blur_intr};
   for (DevBuf* b : all) dev_free(ctx, *b, s);
   cudaStreamSynchronize(s);
   cudaFreeHost(ctx->h_vcnt); cudaFreeHost(ctx->h_kcnt); cudaFreeHost(ctx->h_rbase);
@@ -579,10 +577,16 @@ static cudaEvent_t* chunk_events(gg_context* ctx, int c) {
     if (tev) CK(cudaEventRecord(tev[k], s));                                     \
   } while (0)
 
+// Motion blur fused into the raster (gg_render_blur): the E cameras are the
+// Kc consecutive sample cameras of E / Kc envs; outputs are per env.
+struct BlurSpec {
+  int K, Kc, dk;
+};
+
 static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
                              const float* intr, int32_t W, int32_t H, const gg_render_opts* opts_in,
                              void* rgb, float* depth, float* alpha, cudaStream_t s, chunk_cb cb,
-                             void* cb_user) {
+                             void* cb_user, const BlurSpec* blur = nullptr) {
   gg_render_opts opts;
   if (opts_in) opts = *opts_in; else gg_default_opts(&opts);
   if (E <= 0 || W <= 0 || H <= 0) return fail(ctx, GG_E_INVALID, "gg_render: n_envs/width/height must be > 0");
@@ -606,13 +610,17 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   rp.tight = (opts.flags & (GG_TIGHT_TILES | GG_ELLIPSE_TILES)) != 0;
   rp.ellipse = (opts.flags & GG_ELLIPSE_TILES) != 0;
   rp.color = rgb != nullptr;
-  const bool counters = (opts.flags & GG_COUNTERS) != 0;
-  const bool keep = (opts.flags & GG_KEEP_INTERMEDIATES) != 0 && opts.debug_env >= 0 && opts.debug_env < E;
+  rp.blur_k = blur ? blur->K : 0;
+  rp.blur_kc = blur ? blur->Kc : 0;
+  rp.blur_dk = blur ? blur->dk : 0;
+  const bool counters = (opts.flags & GG_COUNTERS) != 0 && !blur;
+  const bool keep = (opts.flags & GG_KEEP_INTERMEDIATES) != 0 && opts.debug_env >= 0 && opts.debug_env < E && !blur;
 
   const int nmax = std::max(max_scene_n(ctx), 1);
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   const int nwords = nblk * (PROJ_BLOCK / 32);
-  const int chunk = std::min(E, ctx->chunk);
+  int chunk = std::min(E, ctx->chunk);
+  if (blur) chunk = std::max(blur->Kc, chunk / blur->Kc * blur->Kc);   // an env's samples never straddle chunks
 
   if (!ensure(ctx, ctx->sw.envc, sizeof(EnvConst) * E, s) || !ensure(ctx, ctx->sw.perm, (size_t)E * 4, s) ||
       !ensure(ctx, ctx->sw.groups, sizeof(EnvGroup) * (size_t)chunk, s) ||
@@ -642,7 +650,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   // HOST_COPY_SLICE caller envs, so each raster slice's frames are one
   // contiguous range of the caller's buffer (one copy per slice).
   ctx->launches += launch_copy_words(ctx->h_ids, scene_ids, (size_t)E * 4, s);
-  const bool view_order = getenv("GG_NO_ENV_ORDER") == nullptr;   // A/B switch
+  // (not for blur: an env's Kc sample cameras must stay consecutive)
+  const bool view_order = getenv("GG_NO_ENV_ORDER") == nullptr && !blur;   // A/B switch
   if (view_order) ctx->launches += launch_copy_words(ctx->h_vm, viewmats, (size_t)E * 64, s);
   CK(cudaStreamSynchronize(s));
   const int nsc = (int)ctx->scenes.size();
@@ -705,8 +714,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   ctx->launches++;
   CK(cudaGetLastError());
 
-  ctx->t_nchunks = 0;
-  int cidx = 0;
+  if (!ctx->t_append) ctx->t_nchunks = 0;
+  int cidx = ctx->t_nchunks;
   for (int e0 = 0, ec = 0; e0 < E; e0 += ec, ++cidx) {
     cudaEvent_t* tev = ctx->timing ? chunk_events(ctx, cidx) : nullptr;
     if (ctx->timing && !tev) return fail(ctx, GG_E_CUDA, "gg_render: timing events");
@@ -922,6 +931,7 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
   rp.bg[0] = opts.background[0]; rp.bg[1] = opts.background[1]; rp.bg[2] = opts.background[2];
   rp.rgb_format = opts.rgb_format;
   rp.tight = (opts.flags & (GG_TIGHT_TILES | GG_ELLIPSE_TILES)) != 0;
+  rp.blur_k = rp.blur_kc = rp.blur_dk = 0;
   rp.ellipse = (opts.flags & GG_ELLIPSE_TILES) != 0;
   rp.color = rgb != nullptr;
   const bool counters = (opts.flags & GG_COUNTERS) != 0;
@@ -1158,13 +1168,15 @@ gg_status gg_render_blur(gg_context* ctx, int32_t E, const int32_t* scene_ids, c
   const int ecb = std::max(1, std::min(E, ctx->chunk / Kc));
   const size_t nk = (size_t)ecb * Kc;
   if (!ensure(ctx, ctx->blur_vm, nk * 64, s) || !ensure(ctx, ctx->blur_ids, nk * 4, s) ||
-      !ensure(ctx, ctx->blur_intr, nk * 16, s) || (rgb && !ensure(ctx, ctx->blur_rgb, nk * npx * 12, s)) ||
-      (depth && !ensure(ctx, ctx->blur_depth, nk * npx * 4, s)) || (alpha && !ensure(ctx, ctx->blur_alpha, nk * npx * 4, s)))
-    return fail(ctx, GG_E_OOM, "gg_render_blur: sample buffers");
+      !ensure(ctx, ctx->blur_intr, nk * 16, s))
+    return fail(ctx, GG_E_OOM, "gg_render_blur: sample cameras");
   gg_render_opts sub = opts;
-  sub.rgb_format = 1;   // linear f32 samples, averaged before quantisation
   sub.flags = opts.flags & (GG_TIGHT_TILES | GG_ELLIPSE_TILES);   // tile-list variants apply per sample
   sub.debug_env = -1;
+  const BlurSpec bs{K, Kc, dk};
+  ctx->t_nchunks = 0;
+  ctx->t_append = true;   // the stage times cover every sample chunk of this call
+  const size_t rgb_px = opts.rgb_format == 1 ? 12 : 3;
   for (int e0 = 0; e0 < E; e0 += ecb) {
     const int ec = std::min(ecb, E - e0);
     launch_blur_poses(ec, K, Kc, viewmats + (size_t)e0 * 16, lin + (size_t)e0 * 3, ang + (size_t)e0 * 3, shutter,
@@ -1173,17 +1185,18 @@ gg_status gg_render_blur(gg_context* ctx, int32_t E, const int32_t* scene_ids, c
                        P<float>(ctx->blur_intr), s);
     ctx->launches += 2;
     CK(cudaGetLastError());
+    // the raster averages each env's samples in registers and writes its frame once (fused, R34)
     gg_status st = render_impl(ctx, ec * Kc, P<int32_t>(ctx->blur_ids), P<float>(ctx->blur_vm),
-                               P<float>(ctx->blur_intr), W, H, &sub, rgb ? ctx->blur_rgb.p : nullptr,
-                               depth ? P<float>(ctx->blur_depth) : nullptr, alpha ? P<float>(ctx->blur_alpha) : nullptr,
-                               s, nullptr, nullptr);
-    if (st != GG_OK) return st;
-    launch_blur_average(ec, e0, K, Kc, dk, npx, rgb ? P<float>(ctx->blur_rgb) : nullptr,
-                        depth ? P<float>(ctx->blur_depth) : nullptr, alpha ? P<float>(ctx->blur_alpha) : nullptr,
-                        opts.rgb_format, rgb, depth, alpha, s);
-    ctx->launches++;
-    CK(cudaGetLastError());
+                               P<float>(ctx->blur_intr), W, H, &sub,
+                               rgb ? (void*)((uint8_t*)rgb + (size_t)e0 * npx * rgb_px) : nullptr,
+                               depth ? depth + (size_t)e0 * npx : nullptr, alpha ? alpha + (size_t)e0 * npx : nullptr,
+                               s, nullptr, nullptr, &bs);
+    if (st != GG_OK) {
+      ctx->t_append = false;
+      return st;
+    }
   }
+  ctx->t_append = false;
   return GG_OK;
 }
 

@@ -1,4 +1,5 @@
-// blur.cu — motion-blur sample poses and the in-order sample average
+// blur.cu — motion-blur sample poses and cameras (the average is fused into
+// the raster: raster.cu raster_blur_kernel)
 // (§3.3; readings R32-R34 in DESIGN.md).
 #include "gg_internal.cuh"
 
@@ -56,40 +57,6 @@ __global__ void blur_poses_kernel(int E, int K, int Kc, const float* __restrict_
   O[12] = 0.f; O[13] = 0.f; O[14] = 0.f; O[15] = 1.f;
 }
 
-// Average the K colour samples of each env (R34; frames e*Kc + i, i < K):
-// m = x0 + (sum_{i>=1} (x_i - x0)) / K, then u8 round-half-even or f32.
-// Depth comes from the nominal-pose sample dk (t = 0).
-__global__ void blur_average_kernel(int ec, int e0, int K, int Kc, int dk, size_t P, const float* __restrict__ srgb,
-                                    const float* __restrict__ sdepth, const float* __restrict__ salpha,
-                                    int rgb_format, void* __restrict__ rgb, float* __restrict__ depth,
-                                    float* __restrict__ alpha) {
-  const size_t n = (size_t)ec * P;
-  for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
-    const size_t e = q / P, p = q - e * P;
-    const size_t base = e * Kc * P + p;    // sample i of env e at frame e*Kc + i
-    const size_t out = (size_t)(e0 + e) * P + p;
-    if (rgb) {
-      for (int ch = 0; ch < 3; ++ch) {
-        const float x0 = srgb[base * 3 + ch];
-        float s = 0.f;
-        for (int i = 1; i < K; ++i) s += srgb[(base + (size_t)i * P) * 3 + ch] - x0;
-        const float m = x0 + s / (float)K;
-        if (rgb_format == 0)
-          reinterpret_cast<uint8_t*>(rgb)[out * 3 + ch] = (uint8_t)__float2uint_rn(fminf(fmaxf(m, 0.f), 1.f) * 255.f);
-        else
-          reinterpret_cast<float*>(rgb)[out * 3 + ch] = m;
-      }
-    }
-    if (alpha) {
-      const float a0 = salpha[base];
-      float s = 0.f;
-      for (int i = 1; i < K; ++i) s += salpha[base + (size_t)i * P] - a0;
-      alpha[out] = a0 + s / (float)K;
-    }
-    if (depth) depth[out] = sdepth[base + (size_t)dk * P];
-  }
-}
-
 // replicate per-env ids / intrinsics K times (sample-major inside each env)
 __global__ void blur_expand_kernel(int ec, int K, const int32_t* __restrict__ ids, const float* __restrict__ intr,
                                    int32_t* __restrict__ ids_k, float* __restrict__ intr_k) {
@@ -103,12 +70,6 @@ __global__ void blur_expand_kernel(int ec, int K, const int32_t* __restrict__ id
 void launch_blur_poses(int E, int K, int Kc, const float* viewmats, const float* lin, const float* ang,
                        float shutter, float* out, cudaStream_t s) {
   blur_poses_kernel<<<(E * Kc + 127) / 128, 128, 0, s>>>(E, K, Kc, viewmats, lin, ang, shutter, out);
-}
-
-void launch_blur_average(int ec, int e0, int K, int Kc, int dk, size_t P, const float* srgb, const float* sdepth,
-                         const float* salpha, int rgb_format, void* rgb, float* depth, float* alpha, cudaStream_t s) {
-  blur_average_kernel<<<148 * 8, 256, 0, s>>>(ec, e0, K, Kc, dk, P, srgb, sdepth, salpha, rgb_format, rgb, depth,
-                                               alpha);
 }
 
 void launch_blur_expand(int ec, int K, const int32_t* ids, const float* intr, int32_t* ids_k, float* intr_k,

@@ -80,6 +80,7 @@ struct RenderParams {
   int tight;             // GG_TIGHT_TILES: opacity-aware tile rects (reading R35)
   int color;             // 0 = depth-only render (rgb == null): no SH/colour work
   int ellipse;           // GG_ELLIPSE_TILES: per-record tile masks (reading R37)
+  int blur_k, blur_kc, blur_dk;   // fused motion blur: K colour samples, Kc cameras per env, depth sample (0 = off)
 };
 
 // Workspace pointers for one env chunk (indices are chunk-local envs).

@@ -232,39 +232,30 @@ constexpr int RW_THREADS = 128;
 
 // The stop test looks at T' alone: a non-passing pixel has w = 0 and T' = T >=
 // 1e-4, so only a passing pixel can stop; its weight is zeroed by a select.
-template <bool RGB>   // false: depth-only render (no colour accumulation)
-#ifndef GG_RW_MINB
-#define GG_RW_MINB 12   // 40 registers, 48 warps/SM: measured best (10: 82.2, 11-12: 81.5, 14: 90.2 ms per c3 step)
-#endif
-__global__ void __launch_bounds__(RW_THREADS, GG_RW_MINB)
-raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
-                      float* __restrict__ depth, float* __restrict__ alpha_out) {
-  __shared__ float4 srec[RW_THREADS / 32][32 * 3];
-  const int eloc = blockIdx.y;
-  const int tile = blockIdx.x;
-  const int e = envs[e0 + eloc].out_index;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tx = tile % rp.TX, ty = tile / rp.TX;
-  const int bx = warp & 1, by = warp >> 1;
-  const int px = tx * TILE + bx * 8 + (lane & 7);
-  const int py0 = ty * TILE + by * 8 + (lane >> 3), py1 = py0 + 4;
-  constexpr float BW = 7.f, BH = 7.f;   // 8 x 8 blocks (16 x 4 bands measured 7% slower)
-  const bool in0 = px < rp.W && py0 < rp.H, in1 = px < rp.W && py1 < rp.H;
-  // the lane's pixel offsets in the tile: (lx, ly) and (lx, ly + 4)
-  const float lx = (float)(px - tx * TILE);
-  const f2 LY = pk((float)(py0 - ty * TILE), (float)(py1 - ty * TILE));
-  const float tox = (float)(tx * TILE) + 0.5f, toy = (float)(ty * TILE) + 0.5f;
-  const float bx0 = (float)(tx * TILE + bx * 8) + 0.5f, by0 = (float)(ty * TILE + by * 8) + 0.5f;
+// One warp's walk of one camera's tile list for its 8 x 8 block (the lane's
+// pixels (lx, ly) and (lx, ly + 4)); `col` (runtime, warp-uniform) turns the
+// colour accumulation off for a depth-only sample of a motion-blur render.
+struct WarpGeom {
+  float lx, tox, toy, bx0, by0;
+  f2 LY;
+  bool in0, in1;
+};
 
+template <bool RGB>
+__device__ __forceinline__ void warp_walk(const ChunkWS& ws, const RenderParams& rp, int eloc, int tile,
+                                          const WarpGeom& g, bool col, float4* __restrict__ srec, f2& T, f2& Cr,
+                                          f2& Cg, f2& Cb, f2& Dn) {
+  const int lane = threadIdx.x & 31;
+  constexpr float BW = 7.f, BH = 7.f;   // 8 x 8 blocks (16 x 4 bands measured 7% slower)
   const uint2 rg = chunk_ok(ws.ok) ? ws.ranges[(size_t)eloc * rp.ntiles + tile] : make_uint2(0u, 0u);
   const float4* __restrict__ R0 = ws.rec0 + ws.rec_base[eloc];
   const float4* __restrict__ R1 = ws.rec1 + ws.rec_base[eloc];
   const float4* __restrict__ R2 = ws.rec2 + ws.rec_base[eloc];
   const uint32_t* __restrict__ list = ws.sorted + ws.k_base[eloc];
 
-  f2 T = pk(1.f, 1.f), Cr = pk(0.f, 0.f), Cg = Cr, Cb = Cr, Dn = Cr;
+  T = pk(1.f, 1.f); Cr = pk(0.f, 0.f); Cg = Cr; Cb = Cr; Dn = Cr;
   const float INF = __int_as_float(0x7f800000);
-  float cut0 = in0 ? LOG2_CUTOFF : INF, cut1 = in1 ? LOG2_CUTOFF : INF;
+  float cut0 = g.in0 ? LOG2_CUTOFF : INF, cut1 = g.in1 ? LOG2_CUTOFF : INF;
   const uint32_t lt = (1u << lane) - 1u;
 
   // this batch's list entries are loaded one batch ahead
@@ -275,7 +266,7 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
     float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
     if (valid) { a0 = __ldg(&R0[nidx]); a1 = __ldg(&R1[nidx]); a2 = __ldg(&R2[nidx]); }
     nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
-    const float lx0 = bx0, lx1 = bx0 + BW, ly0 = by0, ly1 = by0 + BH;
+    const float lx0 = g.bx0, lx1 = g.bx0 + BW, ly0 = g.by0, ly1 = g.by0 + BH;
     bool mine = false;
     if (valid && a1.w >= 0.f && a0.z >= LOG2_CUTOFF) {
       const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
@@ -284,19 +275,19 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
     const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (mine) {
       const int pos = __popc(m & lt);
-      srec[warp][3 * pos] = tile_coefs(a0, a1, tox, toy);
-      srec[warp][3 * pos + 1] = make_float4(a1.x, a1.y, a1.z, a0.w);
-      srec[warp][3 * pos + 2] = a2;
+      srec[3 * pos] = tile_coefs(a0, a1, g.tox, g.toy);
+      srec[3 * pos + 1] = make_float4(a1.x, a1.y, a1.z, a0.w);
+      srec[3 * pos + 2] = a2;
     }
     __syncwarp();
     const uint32_t cnt = __popc(m);
     for (uint32_t i = 0; i < cnt; ++i) {
-      const float4 r0 = srec[warp][3 * i], r1 = srec[warp][3 * i + 1];
+      const float4 r0 = srec[3 * i], r1 = srec[3 * i + 1];
       // x = c0 + lx (c1 + A' lx) + ly (c2 + B' lx + C' ly)  (tile_coefs)
-      const float P = fmaf(lx, fmaf(r1.x, lx, r0.y), r0.x);
-      const float Q = fmaf(r1.y, lx, r0.z);
+      const float P = fmaf(g.lx, fmaf(r1.x, g.lx, r0.y), r0.x);
+      const float Q = fmaf(r1.y, g.lx, r0.z);
       float x0, x1;
-      upk(fma2(LY, fma2(pk(r1.z, r1.z), LY, pk(Q, Q)), pk(P, P)), x0, x1);
+      upk(fma2(g.LY, fma2(pk(r1.z, r1.z), g.LY, pk(Q, Q)), pk(P, P)), x0, x1);
       // no pixel of the warp passes: nothing to blend, nothing stops (exact)
       if (!__any_sync(0xffffffffu, x0 >= cut0 || x1 >= cut1)) continue;
       const float al0 = x0 >= cut0 ? ex2_approx(fminf(x0, r0.w)) : 0.f;
@@ -310,8 +301,8 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
       W = pk(s0 ? 0.f : w0, s1 ? 0.f : w1);
       cut0 = s0 ? INF : cut0;
       cut1 = s1 ? INF : cut1;
-      if (RGB) {
-        const float4 r2 = srec[warp][3 * i + 2];
+      if (RGB && col) {
+        const float4 r2 = srec[3 * i + 2];
         Cr = fma2(W, pk(r2.x, r2.x), Cr);
         Cg = fma2(W, pk(r2.y, r2.y), Cg);
         Cb = fma2(W, pk(r2.z, r2.z), Cb);
@@ -321,13 +312,111 @@ raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
     }
     __syncwarp();
   }
+}
 
+__device__ __forceinline__ WarpGeom warp_geom(const RenderParams& rp, int tile, int& px, int& py0, int& py1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx = tile % rp.TX, ty = tile / rp.TX;
+  const int bx = warp & 1, by = warp >> 1;
+  px = tx * TILE + bx * 8 + (lane & 7);
+  py0 = ty * TILE + by * 8 + (lane >> 3);
+  py1 = py0 + 4;
+  WarpGeom g;
+  g.in0 = px < rp.W && py0 < rp.H;
+  g.in1 = px < rp.W && py1 < rp.H;
+  g.lx = (float)(px - tx * TILE);
+  g.LY = pk((float)(py0 - ty * TILE), (float)(py1 - ty * TILE));
+  g.tox = (float)(tx * TILE) + 0.5f;
+  g.toy = (float)(ty * TILE) + 0.5f;
+  g.bx0 = (float)(tx * TILE + bx * 8) + 0.5f;
+  g.by0 = (float)(ty * TILE + by * 8) + 0.5f;
+  return g;
+}
+
+template <bool RGB>   // false: depth-only render (no colour accumulation)
+#ifndef GG_RW_MINB
+#define GG_RW_MINB 12   // 40 registers, 48 warps/SM: measured best (10: 82.2, 11-12: 81.5, 14: 90.2 ms per c3 step)
+#endif
+__global__ void __launch_bounds__(RW_THREADS, GG_RW_MINB)
+raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
+                      float* __restrict__ depth, float* __restrict__ alpha_out) {
+  __shared__ float4 srec[RW_THREADS / 32][32 * 3];
+  const int eloc = blockIdx.y;
+  const int tile = blockIdx.x;
+  const int e = envs[e0 + eloc].out_index;
+  int px, py0, py1;
+  const WarpGeom g = warp_geom(rp, tile, px, py0, py1);
+  f2 T, Cr, Cg, Cb, Dn;
+  warp_walk<RGB>(ws, rp, eloc, tile, g, true, srec[threadIdx.x >> 5], T, Cr, Cg, Cb, Dn);
   float t[2], cr[2], cg[2], cb[2], dn[2];
   upk(T, t[0], t[1]); upk(Cr, cr[0], cr[1]); upk(Cg, cg[0], cg[1]); upk(Cb, cb[0], cb[1]);
   upk(Dn, dn[0], dn[1]);
   const size_t p0 = ((size_t)e * rp.H + py0) * rp.W + px;
-  if (in0) write_pixel(rp, RGB ? rgb : nullptr, depth, alpha_out, p0, t[0], cr[0], cg[0], cb[0], dn[0]);
-  if (in1) write_pixel(rp, RGB ? rgb : nullptr, depth, alpha_out, p0 + (size_t)(py1 - py0) * rp.W, t[1], cr[1], cg[1], cb[1], dn[1]);
+  if (g.in0) write_pixel(rp, RGB ? rgb : nullptr, depth, alpha_out, p0, t[0], cr[0], cg[0], cb[0], dn[0]);
+  if (g.in1) write_pixel(rp, RGB ? rgb : nullptr, depth, alpha_out, p0 + (size_t)(py1 - py0) * rp.W, t[1], cr[1], cg[1], cb[1], dn[1]);
+}
+
+// Motion blur fused into the raster (reading
+// R34): a CTA renders the Kc sample cameras of one env (consecutive
+// chunk-local envs), keeps each pixel's f32 colour and alpha of sample 0 and
+// the running sum of the later samples' differences, and writes the env's
+// frame once: m = x0 + (sum_{i>=1} (x_i - x0)) / K (the same operations, in
+// the same order, as averaging K rendered f32 frames), depth from sample dk
+// (the nominal pose t = 0).  Sample K of an even K is that depth-only pose.
+template <bool RGB>
+__global__ void __launch_bounds__(RW_THREADS, 8)
+raster_blur_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
+                   float* __restrict__ depth, float* __restrict__ alpha_out) {
+  __shared__ float4 srec[RW_THREADS / 32][32 * 3];
+  const int K = rp.blur_k, Kc = rp.blur_kc, dk = rp.blur_dk;
+  const int c0 = blockIdx.y * Kc;                      // chunk-local camera of sample 0
+  const int tile = blockIdx.x;
+  const int e = envs[e0 + c0].out_index / Kc;          // output env (relative to this render)
+  int px, py0, py1;
+  const WarpGeom g = warp_geom(rp, tile, px, py0, py1);
+  float x0[2][4], sm[2][4], dep[2] = {0.f, 0.f};
+  for (int k = 0; k < Kc; ++k) {
+    f2 T, Cr, Cg, Cb, Dn;
+    warp_walk<RGB>(ws, rp, c0 + k, tile, g, k < K, srec[threadIdx.x >> 5], T, Cr, Cg, Cb, Dn);
+    float t[2], cr[2], cg[2], cb[2], dn[2];
+    upk(T, t[0], t[1]); upk(Cr, cr[0], cr[1]); upk(Cg, cg[0], cg[1]); upk(Cb, cb[0], cb[1]);
+    upk(Dn, dn[0], dn[1]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      // this sample's f32 pixel (write_pixel's arithmetic): rgb = C + T bg, alpha = 1 - T
+      const float x[4] = {fmaf(t[q], rp.bg[0], cr[q]), fmaf(t[q], rp.bg[1], cg[q]), fmaf(t[q], rp.bg[2], cb[q]),
+                          1.f - t[q]};
+      if (k == dk) dep[q] = x[3] > 0.f ? dn[q] / x[3] : 0.f;
+      if (k == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { x0[q][c] = x[c]; sm[q][c] = 0.f; }
+      } else if (k < K) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sm[q][c] += x[c] - x0[q][c];
+      }
+    }
+  }
+  const size_t p0 = ((size_t)e * rp.H + py0) * rp.W + px;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    if (!(q == 0 ? g.in0 : g.in1)) continue;
+    const size_t p = p0 + (size_t)(q * (py1 - py0)) * rp.W;
+    float m[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) m[c] = x0[q][c] + sm[q][c] / (float)K;
+    if (RGB && rgb) {
+      if (rp.rgb_format == 0) {
+        uint8_t* o = reinterpret_cast<uint8_t*>(rgb) + p * 3;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) o[c] = (uint8_t)__float2uint_rn(fminf(fmaxf(m[c], 0.f), 1.f) * 255.f);
+      } else {
+        float* o = reinterpret_cast<float*>(rgb) + p * 3;
+        o[0] = m[0]; o[1] = m[1]; o[2] = m[2];
+      }
+    }
+    if (alpha_out) alpha_out[p] = m[3];
+    if (depth) depth[p] = dep[q];
+  }
 }
 
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
@@ -335,6 +424,12 @@ void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp,
                    int dbg_eloc, cudaStream_t s) {
   CounterOut co{env_counts, dbg_neval, dbg_eloc};
   dim3 grid(rp.ntiles, ec);
+  if (rp.blur_k > 0) {   // fused motion-blur average: one CTA per (tile, env) over the env's Kc cameras
+    grid.y = ec / rp.blur_kc;
+    if (rgb) raster_blur_kernel<true><<<grid, RW_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
+    else raster_blur_kernel<false><<<grid, RW_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
+    return;
+  }
   if (counters)
     raster_kernel<true><<<grid, TILE_PX, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha, co);
   else if (rgb)
