@@ -280,6 +280,39 @@ def roofline(args, c, E, W, H, S, scene, want_rgb, want_depth, stage_ms, clocks,
     return roof, roof_path
 
 
+def scene_stream(wl, rank, world, cdev, dev):
+    """Yield (k, (means, scales, quats, opacities, sh on `dev`, host Scene or None)) for every scene of the
+    workload.  Single process: generated here.  Several ranks: rank 0 generates each scene and broadcasts its
+    arrays and its floor description (camera placement); the others receive them and place their own envs'
+    cameras."""
+    import torch
+    import torch.distributed as dist
+
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    if world == 1:
+        for k, sc in wl.scenes():
+            yield k, (t(sc.means), t(sc.scales), t(sc.quats), t(sc.opacities), t(sc.sh), sc)
+        return
+    n, kk = wl.n_gauss, (wl.sh_degree + 1) ** 2
+    shapes = [(n, 3), (n, 3), (n, 4), (n,), (n, kk, 3)]
+    it = wl.scenes() if rank == 0 else None
+    for k in range(wl.n_scenes):
+        if rank == 0:
+            _, sc = next(it)
+            arrs = [sc.means, sc.scales, sc.quats, sc.opacities, sc.sh]
+            bufs = [torch.from_numpy(np.ascontiguousarray(a)).to(cdev) for a in arrs]
+            floor = torch.from_numpy(gi.pack_floor(sc)).to(cdev)
+        else:
+            sc = None
+            bufs = [torch.empty(sh_, dtype=torch.float32, device=cdev) for sh_ in shapes]
+            floor = torch.empty(2 + 4 * gi.MAX_FREE_BOXES, dtype=torch.float64, device=cdev)
+        for b in bufs + [floor]:
+            dist.broadcast(b, 0)
+        if rank != 0:
+            wl.place(k, *gi.unpack_floor(floor.cpu().numpy()))
+        yield k, tuple(b.to(dev) for b in bufs) + (sc,)
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle on the box's host cores, same metric/config."""
     from paper_2510_15352_b200.dist import dist_env
@@ -322,7 +355,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2510_15352_b200 as gg
-    from paper_2510_15352_b200.dist import dist_env, fold_digests, gather_stats, max_over_ranks
+    from paper_2510_15352_b200.dist import dist_env, fold_digests, gather_env_digests, gather_stats, max_over_ranks
 
     rank, world, local = dist_env()
     gpu = local % torch.cuda.device_count()
@@ -347,15 +380,20 @@ def main():
     # a fresh, seeded pose set for every step, all resident in HBM; each env's camera
     # lives in its own scene, drawn while that scene is at hand (gg_inputs.Workload, shared with the
     # full-size parity tests)
-    wl = gi.Workload(args.config, n_envs=E, n_sets=n_sets, rank=rank, n_scenes=S, n_gauss=c["n_gauss"],
-                     sh_degree=c["sh_degree"])
+    # Weak scaling over one GLOBAL env set: rank r renders envs [r E, (r + 1) E) of E x world; every input
+    # is a function of the global env index (gg_inputs.Workload), so the folded digest of all envs equals a
+    # one-GPU render of the same set (SURVEY §8(e) checks).  Rank 0 generates each scene once and broadcasts
+    # it (C3: NCCL over NVLink, or gloo), instead of every rank generating every scene.
+    wl = gi.Workload(args.config, n_envs=E * world, n_sets=n_sets, env_range=(rank * E, (rank + 1) * E),
+                     n_scenes=S, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])
     binding = wl.binding
     sids, scene = [], None
-    for k, sc_ in wl.scenes():
-        sids.append(R.load_scene(t(sc_.means), t(sc_.scales), t(sc_.quats), t(sc_.opacities), t(sc_.sh),
-                                 sc_.sh_degree))
-        if k == int(binding[0]):
-            scene = sc_                          # kept for the CPU baseline's sample
+    t_load0 = time.perf_counter()
+    for k, sc_ in scene_stream(wl, rank, world, cdev, dev):
+        sids.append(R.load_scene(*sc_[:5], wl.sh_degree))
+        if rank == 0 and k == int(binding[0]):
+            scene = sc_[5]                       # kept for the CPU baseline's sample
+    load_s = time.perf_counter() - t_load0
     vm = wl.viewmats
     ids_np = np.asarray(sids, np.int32)[binding]
     gg.gg_reserve(R.ctx, E, W, H, args.chunk)
@@ -459,12 +497,13 @@ def main():
         torch.cuda.synchronize()                # (its last render is the last timed pose set)
     gg.gg_set_timing(R.ctx, False)
 
-    # ---- digest of the last frame set, C1 all_gather
+    # ---- digest of the last frame set: per-env digests of every rank, folded in global env order (C1)
     dig = torch.zeros(E, dtype=torch.int64, device=dev)
     gg.gg_checksum(R.ctx, E, W, H, rgb, 0, depth, dig, stream)
     torch.cuda.synchronize()
     digest = fold_digests([int(x) & 0xFFFFFFFFFFFFFFFF for x in dig.cpu().tolist()])
     frames_total, tmax_ns, digests = gather_stats(E * args.steps, digest, int(elapsed_ms * 1e6), cdev)
+    all_digests = gather_env_digests(dig.to(cdev))
     tmax_ms = tmax_ns / 1e6
     value = frames_total / (tmax_ms / 1000.0)
     stage_ms = stage / args.steps          # per step, this rank
@@ -535,7 +574,9 @@ def main():
                             "rendered_lists": {"n_eval": r_eval, "n_contrib": r_contrib, "keys": r_keys,
                                                "n_eval_per_px": r_eval / (E * W * H),
                                                "tiles": args.tiles}},
-               "digest": f"{fold_digests(digests):016x}",
+               "digest": f"{fold_digests(all_digests):016x}",
+               "digest_basis": f"per-env digests of all {E * world} envs folded in global env order",
+               "load_s": round(load_s, 2),
                "paper_context": "~20k env-frames/s derived for 1x RTX 4090 incl. physics (BASELINE.md §1)"}
         print(json.dumps(rec), flush=True)
     R.close()

@@ -449,49 +449,71 @@ class Workload:
     """The seeded inputs of one BASELINE config as bench.py renders them.
 
     One scene (c1-c3: `config_scene`) or S rooms `room_scene(100 + k, ...)`
-    with a seeded uniform env->scene binding (c4/c5).  Pose set
-    s of env e is drawn in e's own scene: seed 10,000 (rank+1) + s for one
-    scene, 10,000 (rank+1) + 4,096 s + k for scene k of several.  `scenes()`
-    generates the rooms in parallel and streams them (c5's 2,500 rooms never
-    sit in host memory at once), filling `viewmats[s, envs of k]` as scene k
-    goes by; `scene(k)` regenerates one scene on its own (same seed, same
-    arrays).
-    """
+    with a seeded uniform env->scene binding over the GLOBAL env set
+    (c4/c5).  Every input is a function of the global env
+    index, never of the rank or world size, so a rank-sliced multi-GPU run
+    renders exactly the envs of a single-GPU run of the same global set
+    (SURVEY §8(e) determinism checks): the poses of the envs of block
+    b = e // POSE_BLOCK bound to scene k in pose set s are drawn from
+    rng(KIND_CAMERAS, pose_index(s, b, k)), in env order, in scene k.
 
-    def __init__(self, cfg: str, n_envs: int | None = None, n_sets: int = 1, rank: int = 0,
+    `env_range` = [a, b) materialises only those envs (a rank's slice).
+    `scenes()` generates the rooms in parallel and streams them (c5's 2,500
+    rooms never sit in host memory at once), placing the cameras of scene k's
+    envs as it goes by; `place(k, free_boxes, half_extent)` does the same from
+    a scene's floor description alone (ranks that receive scenes by broadcast);
+    `scene(k)` regenerates one scene on its own (same seed, same arrays).
+    """
+    POSE_BLOCK = 32
+
+    def __init__(self, cfg: str, n_envs: int | None = None, n_sets: int = 1, env_range=None,
                  n_scenes: int | None = None, n_gauss: int | None = None, sh_degree: int | None = None):
         c = CONFIGS[cfg]
         self.cfg = cfg
-        self.n_envs = c["n_envs"] if n_envs is None else n_envs
-        self.n_sets, self.rank = n_sets, rank
+        self.n_total = c["n_envs"] if n_envs is None else n_envs
+        self.a, self.b = env_range if env_range is not None else (0, self.n_total)
+        self.n_envs = self.b - self.a
+        self.n_sets = n_sets
         self.width, self.height = c["width"], c["height"]
         self.n_gauss = c["n_gauss"] if n_gauss is None else n_gauss
         self.sh_degree = c["sh_degree"] if sh_degree is None else sh_degree
         self.n_scenes = n_scenes or (c["n_scenes"] if cfg in ("c4", "c5") else 1)
-        S, E = self.n_scenes, self.n_envs
-        self.binding = scene_binding(7 + rank, E, S) if S > 1 else np.zeros(E, np.int32)
-        self.viewmats = np.empty((n_sets, E, 4, 4), np.float32)
-        self.intrinsics = np.tile(pinhole(self.width, self.height).astype(np.float32), (E, 1))
+        S = self.n_scenes
+        self.glob_binding = scene_binding(7, self.n_total, S) if S > 1 else np.zeros(self.n_total, np.int32)
+        self.binding = np.ascontiguousarray(self.glob_binding[self.a:self.b])
+        self.viewmats = np.empty((n_sets, self.n_envs, 4, 4), np.float32)
+        self.intrinsics = np.tile(pinhole(self.width, self.height).astype(np.float32), (self.n_envs, 1))
+
+    @staticmethod
+    def pose_index(s: int, block: int, k: int) -> int:
+        return (s << 40) | (block << 16) | k
 
     def scene(self, k: int) -> Scene:
         if self.n_scenes == 1:
             return config_scene(self.cfg, n_gauss=self.n_gauss, sh_degree=self.sh_degree)
         return _room_job((k, self.n_gauss, self.sh_degree))
 
-    def _fill(self, k: int, sc: Scene):
-        idx = np.flatnonzero(self.binding == k)
+    def place(self, k: int, free_boxes, half_extent: float):
+        """Cameras of this slice's envs bound to scene k (all pose sets)."""
+        idx = np.flatnonzero(self.binding == k) + self.a        # global envs of this slice bound to k
         if not idx.size:
             return
-        for s_ in range(self.n_sets):
-            seed = 10_000 * (self.rank + 1) + (s_ if self.n_scenes == 1 else 4096 * s_ + k)
-            self.viewmats[s_, idx] = cameras(seed, idx.size, self.width, self.height, sc).viewmats
+        PB = self.POSE_BLOCK
+        for blk in np.unique(idx // PB):
+            lo, hi = int(blk) * PB, min(self.n_total, (int(blk) + 1) * PB)
+            blk_envs = lo + np.flatnonzero(self.glob_binding[lo:hi] == k)   # all of the block's envs on k
+            mine = (blk_envs >= self.a) & (blk_envs < self.b)
+            for s_ in range(self.n_sets):
+                cams = cameras(self.pose_index(s_, int(blk), k), blk_envs.size, self.width, self.height,
+                               half_extent=half_extent, obstacles=list(free_boxes))
+                self.viewmats[s_, blk_envs[mine] - self.a] = cams.viewmats[mine]
 
     def scenes(self, n_proc: int | None = None):
         """Yield (k, scene) for k = 0..S-1 in order (parallel host generation)."""
         S = self.n_scenes
         if S == 1:
             sc = self.scene(0)
-            self._fill(0, sc)
+            self.place(0, sc.free_boxes, sc.half_extent)
             yield 0, sc
             return
         import concurrent.futures as cf
@@ -507,11 +529,32 @@ class Workload:
                 nxt = k + 2 * n_proc
                 if nxt < S:
                     futs[nxt] = ex.submit(_room_job, (nxt,) + job)
-                self._fill(k, sc)
+                self.place(k, sc.free_boxes, sc.half_extent)
                 yield k, sc
 
     def cameras(self, s: int = 0) -> Cameras:
         return Cameras(self.viewmats[s], self.intrinsics, self.width, self.height)
+
+
+MAX_FREE_BOXES = 64
+
+
+def pack_floor(scene: Scene) -> np.ndarray:
+    """A scene's camera-placement description (half extent, obstacle boxes) as
+    a fixed-size float64 vector, for broadcast to ranks that only receive the
+    scene's Gaussians."""
+    v = np.zeros(2 + 4 * MAX_FREE_BOXES, np.float64)
+    boxes = list(scene.free_boxes)[:MAX_FREE_BOXES]
+    v[0], v[1] = scene.half_extent, len(boxes)
+    for i, b in enumerate(boxes):
+        v[2 + 4 * i: 6 + 4 * i] = b
+    return v
+
+
+def unpack_floor(v) -> tuple:
+    v = np.asarray(v, np.float64)
+    n = int(v[1])
+    return [tuple(float(x) for x in v[2 + 4 * i: 6 + 4 * i]) for i in range(n)], float(v[0])
 
 
 # ---------------------------------------------------------------------------

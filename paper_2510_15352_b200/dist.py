@@ -61,6 +61,19 @@ def gather_stats(frames: int, digest: int, elapsed_ns: int, device=None):
     return total, tmax, digs
 
 
+def gather_env_digests(dig) -> list:
+    """All ranks' per-env digests (int64 tensors of equal length, 64-bit
+    patterns) in rank order = global env order; a single process returns its own."""
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return [int(x) & 0xFFFFFFFFFFFFFFFF for x in dig.cpu().tolist()]
+    import torch
+    out = torch.zeros(dist.get_world_size() * dig.numel(), dtype=dig.dtype, device=dig.device)
+    dist.all_gather_into_tensor(out, dig.contiguous())
+    return [int(x) & 0xFFFFFFFFFFFFFFFF for x in out.cpu().tolist()]
+
+
 def max_over_ranks(x: float, device=None) -> float:
     import torch
     import torch.distributed as dist

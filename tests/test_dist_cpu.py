@@ -81,3 +81,64 @@ def test_single_process_passthrough():
     assert not dist.is_initialized()
     assert gather_stats(5, 42, 100) == (5, 100, [42])
     assert max_over_ranks(2.5) == 2.5
+
+
+def _digest(a) -> int:
+    import hashlib
+    return int.from_bytes(hashlib.blake2b(a.tobytes(), digest_size=7).digest(), "little")
+
+
+def _stream_worker(rank, world, port, q):
+    """bench.scene_stream over gloo: rank 0 generates and broadcasts the scenes
+    (C3), rank 1 receives them and places its own envs' cameras."""
+    import sys
+    import numpy as np
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    import gg_inputs as gi
+    from paper_2510_15352_b200.dist import gather_env_digests
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        E = 24
+        wl = gi.Workload("c4", n_envs=E * world, n_sets=2, env_range=(rank * E, (rank + 1) * E), n_scenes=3,
+                         n_gauss=1500, sh_degree=1)
+        cpu = torch.device("cpu")
+        sums = [float(sum(float(x.double().sum()) for x in arrs[:5])) for _, arrs in
+                bench.scene_stream(wl, rank, world, cpu, cpu)]
+        # per-env "digests" that are a function of the env's inputs only
+        dig = torch.tensor([_digest(wl.viewmats[:, e]) for e in range(E)], dtype=torch.int64)
+        q.put((rank, sums, wl.viewmats.copy(), wl.binding.copy(), gather_env_digests(dig)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_scene_broadcast_and_global_env_slices_gloo():
+    """Rank-sliced inputs of a 2-rank run equal the single-process workload's
+    (every input is a function of the global env index), the broadcast scenes
+    equal the generated ones, and the gathered per-env digests come back in
+    global env order (SURVEY §8(e) determinism checks, C3 scene broadcast)."""
+    import numpy as np
+    import gg_inputs as gi
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_stream_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = gi.Workload("c4", n_envs=48, n_sets=2, n_scenes=3, n_gauss=1500, sh_degree=1)
+    ref_sums = [float(sum(float(np.asarray(a, np.float64).sum()) for a in
+                          (sc.means, sc.scales, sc.quats, sc.opacities, sc.sh))) for _, sc in full.scenes(n_proc=1)]
+    for rank, sums, vm, binding, digs in out:
+        assert sums == ref_sums
+        assert np.array_equal(vm, full.viewmats[:, rank * 24:(rank + 1) * 24])
+        assert np.array_equal(binding, full.binding[rank * 24:(rank + 1) * 24])
+    assert out[0][4] == out[1][4]                  # both ranks see all digests, rank (= global env) order
+    ref_dig = [_digest(full.viewmats[:, e]) for e in range(48)]
+    assert out[0][4] == ref_dig
