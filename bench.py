@@ -535,7 +535,8 @@ def main():
         del h_rgb, h_depth
 
     # ---- rooflines (live CUDA-event stage times on the render stream)
-    roof, roof_path = roofline(args, c, E, W, H, S, scene, want_rgb, want_depth, stage_ms, clocks, kb,
+    meta = argparse.Namespace(n=wl.n_gauss, sh_degree=wl.sh_degree)   # every rank (only rank 0 holds a host scene)
+    roof, roof_path = roofline(args, c, E, W, H, S, meta, want_rgb, want_depth, stage_ms, clocks, kb,
                                (n_eval, n_contrib, n_vis, n_keys), (r_eval, r_contrib, r_vis, r_keys))
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
@@ -554,8 +555,8 @@ def main():
                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                "config": {"workload": name + ("" if want_rgb and want_depth == c["depth"] else
                                               " [depth-only outputs]" if not want_rgb else " [RGB-only outputs]"),
-                          "envs_per_gpu": E, "total_envs": E * world, "n_gauss": scene.n, "n_scenes": S,
-                          "sh_degree": scene.sh_degree, "width": W, "height": H, "depth": want_depth, "rgb": want_rgb,
+                          "envs_per_gpu": E, "total_envs": E * world, "n_gauss": wl.n_gauss, "n_scenes": S,
+                          "sh_degree": wl.sh_degree, "width": W, "height": H, "depth": want_depth, "rgb": want_rgb,
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
                           "chunk_envs": args.chunk or 1024, "render_mode": {"sync": "sync", "async": "async (GG_ASYNC)",
