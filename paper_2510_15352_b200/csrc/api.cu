@@ -802,6 +802,9 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       return fail(ctx, GG_E_OOM, "gg_render: key workspace (%llu keys) allocation failed", (unsigned long long)K);
     ctx->launches += launch_copy_words(ctx->sw.kbase.p, ctx->h_kbase, ec * 8, s);
     ws.sorted = P<uint32_t>(ctx->sw.sorted);
+#ifdef GG_CHECK_PROTOCOLS
+    CK(cudaMemsetAsync(ws.sorted, 0xff, K * 4, s));   // placement asserts each slot is written once
+#endif
     // K3-K5: sort blocks of sort_block_size() records, never straddling an env
     uint32_t nb = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_blkbase[i] = nb; nb += sort_blocks(ctx->h_vcnt[i]); }

@@ -259,6 +259,12 @@ __device__ __forceinline__ void block_rank(const uint64_t (&x)[DS_IPT], int shif
     if (ok) atomicOr(&pm[rep], 1u << lane);
     __syncwarp();
     const uint32_t peers = ok ? pm[rep] : 0u;
+#ifdef GG_CHECK_PROTOCOLS   // race/protocol evidence build: the stamp protocol's peer mask = exact equal-digit set
+    {
+      const uint32_t ref = __match_any_sync(0xffffffffu, ok ? dd : 0xffffffffu);
+      if (ok && peers != ref) __trap();
+    }
+#endif
     const uint32_t before = ok ? (wc[dd >> 1] >> (16 * (dd & 1))) & 0xffffu : 0u;
     __syncwarp();
     if (ok && lane == (int)rep) pm[rep] = 0u;
@@ -322,6 +328,17 @@ __device__ __forceinline__ void depth_downsweep_block(uint32_t b, const BlockTab
     if (i < n) sm.u.o.sp[lp[j]] = x[j];
   }
   __syncthreads();
+#ifdef GG_CHECK_PROTOCOLS
+  {  // the staged block is sorted by (key bits below this pass's top, record): stable, no element lost or doubled
+    const uint32_t bits = (uint32_t)shift + DS_BITS;
+    const uint64_t km = bits >= 32 ? 0xffffffffull : ((1ull << bits) - 1ull);
+    for (uint32_t q = tid; q + 1 < n; q += DS_THREADS) {
+      const uint64_t a = sm.u.o.sp[q], c = sm.u.o.sp[q + 1];
+      const uint64_t ka = (a >> 32) & km, kc = (c >> 32) & km;
+      if (!(ka < kc || (ka == kc && (uint32_t)a < (uint32_t)c))) __trap();
+    }
+  }
+#endif
   if (io.pout) {
     uint64_t* pout = io.pout + rb;
     for (uint32_t q = tid; q < n; q += DS_THREADS) {
@@ -662,6 +679,12 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
         peers = ok ? pm[rep] : 0u;
         __syncwarp();
         if (ok && lane == (int)rep) pm[rep] = 0u;
+#ifdef GG_CHECK_PROTOCOLS
+        {
+          const uint32_t ref = __match_any_sync(0xffffffffu, ok ? t : 0xffffffffu);
+          if (ok && peers != ref) __trap();
+        }
+#endif
       } else {
         peers = __ballot_sync(0xffffffffu, ok);
 #pragma unroll
@@ -675,7 +698,11 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
       __syncwarp();
       if (ok && lane == __ffs(peers) - 1) atomicAdd(&h[t >> 1], __popc(peers) << (16 * (t & 1)));
       __syncwarp();
+#ifdef GG_CHECK_PROTOCOLS   // every list slot is written exactly once (the buffer is pre-filled with ~0)
+      if (ok && atomicExch(&out[gb[t] + before + __popc(peers & lt)], o_idx) != 0xffffffffu) __trap();
+#else
       if (ok) out[gb[t] + before + __popc(peers & lt)] = o_idx;
+#endif
     }
   }
 }
