@@ -989,6 +989,9 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
                     ctx->a_kcap, ctx->a_nbcap, ok, err, s);
     ctx->launches += 5;
     TREC(2);
+#ifdef GG_CHECK_PROTOCOLS
+    CK(cudaMemsetAsync(ws.sorted, 0xff, ctx->a_kcap * 4, s));   // placement asserts each slot is written once
+#endif
     ctx->launches += launch_sort_bin(ec, (uint32_t)ctx->a_nbcap, P<uint32_t>(ctx->aw.blkbase), P<uint32_t>(ctx->aw.blkenv),
                                      passes, rp, ws,
                                      P<uint32_t>(ctx->aw.ghist), P<uint32_t>(ctx->aw.thist), s, true,
