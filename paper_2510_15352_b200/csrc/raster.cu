@@ -229,6 +229,9 @@ raster_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkW
 // costs only the exponent and one vote (an exact ellipse-vs-block test in
 // the loader was measured slower: 87.9 vs 85.5 ms per c3 step).
 constexpr int RW_THREADS = 128;
+#ifndef GG_RW_PF
+#define GG_RW_PF 0   // 1: prefetch the next kept record's terms (A/B switch)
+#endif
 
 // The stop test looks at T' alone: a non-passing pixel has w = 0 and T' = T >=
 // 1e-4, so only a passing pixel can stop; its weight is zeroed by a select.
@@ -281,8 +284,18 @@ __device__ __forceinline__ void warp_walk(const ChunkWS& ws, const RenderParams&
     }
     __syncwarp();
     const uint32_t cnt = __popc(m);
+#if GG_RW_PF
+    // the next kept record's exponent terms are read from shared memory one
+    // record ahead, off the dependency chain of this record's vote
+    float4 n0 = srec[0], n1 = srec[1];
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const float4 r0 = n0, r1 = n1;
+      n0 = srec[3 * (i + 1)];
+      n1 = srec[3 * (i + 1) + 1];
+#else
     for (uint32_t i = 0; i < cnt; ++i) {
       const float4 r0 = srec[3 * i], r1 = srec[3 * i + 1];
+#endif
       // x = c0 + lx (c1 + A' lx) + ly (c2 + B' lx + C' ly)  (tile_coefs)
       const float P = fmaf(g.lx, fmaf(r1.x, g.lx, r0.y), r0.x);
       const float Q = fmaf(r1.y, g.lx, r0.z);
@@ -340,7 +353,7 @@ template <bool RGB>   // false: depth-only render (no colour accumulation)
 __global__ void __launch_bounds__(RW_THREADS, GG_RW_MINB)
 raster_warp_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
                       float* __restrict__ depth, float* __restrict__ alpha_out) {
-  __shared__ float4 srec[RW_THREADS / 32][32 * 3];
+  __shared__ float4 srec[RW_THREADS / 32][32 * 3 + 3];   // + 1 record of slack for the prefetch
   const int eloc = blockIdx.y;
   const int tile = blockIdx.x;
   const int e = envs[e0 + eloc].out_index;
@@ -367,7 +380,7 @@ template <bool RGB>
 __global__ void __launch_bounds__(RW_THREADS, 8)
 raster_blur_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
                    float* __restrict__ depth, float* __restrict__ alpha_out) {
-  __shared__ float4 srec[RW_THREADS / 32][32 * 3];
+  __shared__ float4 srec[RW_THREADS / 32][32 * 3 + 3];
   const int K = rp.blur_k, Kc = rp.blur_kc, dk = rp.blur_dk;
   const int c0 = blockIdx.y * Kc;                      // chunk-local camera of sample 0
   const int tile = blockIdx.x;
