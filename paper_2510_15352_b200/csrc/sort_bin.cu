@@ -605,23 +605,16 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
     }
   }
   __syncthreads();
-  // phase 2: per-warp cursors relative to the block's run of each tile: an
-  // exclusive scan over the S segments per packed word, two words per warp
-  // step (half-warp h scans word q + h across its lanes = segments); the u16
-  // halves add without carry (a tile's count in one block is < 2^16)
-  {
-    const int half = lane >> 4, seg = lane & 15;
-    for (int q0 = 2 * warp; q0 < nw2; q0 += 2 * PD_WARPS) {
-      const int q = q0 + half;
-      const bool ok = q < nw2 && seg < S;
-      const uint32_t x = ok ? wh[(size_t)seg * nw2 + q] : 0u;
-      uint32_t incl = x;
-#pragma unroll
-      for (int o = 1; o < 16; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o, 16);
-        if (seg >= o) incl += y;
-      }
-      if (ok) wh[(size_t)seg * nw2 + q] = incl - x;
+  // phase 2: per-warp cursors relative to the block's run of each tile (one
+  // thread per packed word; a warp-parallel scan over the segments measured
+  // slower: 30.96 vs 29.8 ms of placement per c3 step)
+  for (int q = tid; q < nw2; q += PD_THREADS) {
+    uint32_t run0 = 0, run1 = 0;
+    for (int w = 0; w < S; ++w) {
+      const uint32_t c = wh[(size_t)w * nw2 + q];
+      wh[(size_t)w * nw2 + q] = run0 | (run1 << 16);
+      run0 += c & 0xffffu;
+      run1 += c >> 16;
     }
   }
   __syncthreads();
