@@ -409,6 +409,7 @@ struct ProjSmem {
   uint32_t kacc[ENV_GROUP];
   uint32_t nunits;
   uint8_t units[ENV_GROUP * PROJ_WPB]; // non-empty (word, env) units, word-major: (w << 4) | k
+  uint8_t bitpos[PROJ_BLOCK / 32][32]; // per warp: position of the word's l-th set bit
 };
 
 // Work decomposition (DESIGN.md §4 K1b).  A unit = one visibility word (32
@@ -421,7 +422,10 @@ struct ProjSmem {
 // Gaussians being projected stay in L1.  With the Morton storage order a
 // non-empty word is ~90% full (visibility is spatially coherent).
 template <bool ELL>   // GG_ELLIPSE_TILES (reading R37): per-record tile masks
-__global__ void __launch_bounds__(PROJ_BLOCK, 1024 / PROJ_BLOCK)
+#ifndef GG_PROJ_MINB
+#define GG_PROJ_MINB (1024 / PROJ_BLOCK)   // 4 CTAs x 256 threads at <= 64 registers
+#endif
+__global__ void __launch_bounds__(PROJ_BLOCK, GG_PROJ_MINB)
 project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
                const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
   __shared__ ProjSmem sm;
@@ -469,8 +473,14 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     const int w = (int)(unit >> 4), k = (int)(unit & 15u);
     const uint32_t word = sm.fw[k * PROJ_WPB + w];
     uint32_t ntiles = 0;
+    // lane b with bit b set writes b at its rank among the set bits: lane l
+    // then reads the position of the word's l-th visible Gaussian
+    if ((word >> lane) & 1u) sm.bitpos[warp][__popc(word & ((1u << lane) - 1u))] = (uint8_t)lane;
+    __syncwarp();
+    const int bl = sm.bitpos[warp][lane];
+    __syncwarp();
     if (lane < __popc(word)) {
-      const int l = w * 32 + (int)__fns(word, 0u, lane + 1);   // the lane-th visible Gaussian of the word
+      const int l = w * 32 + bl;                                 // the lane-th visible Gaussian of the word
     const EnvConst c = load_cam_t(sm.camT, k);
     const int eloc = grp.elo + k;
     const size_t r = ws.rec_base[eloc] + ws.blkcnt[(size_t)eloc * ws.nblk + gblk] + sm.cnt[k * PROJ_WPB + w] + lane;

@@ -82,7 +82,7 @@ def full(kernel):
 agg, tot, nl = launches()
 kern = {}
 for k in ["raster_warp_kernel", "project_kernel", "cull_count_kernel", "depth_downsweep", "place_downsweep",
-          "depth_upsweep", "place_upsweep", "depth_scan", "place_scan"]:
+          "depth_upsweep", "place_upsweep", "depth_ties", "depth_scan", "place_scan"]:
     r = full(k)
     if r:
         kern[k] = r

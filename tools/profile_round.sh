@@ -14,7 +14,7 @@ $CMD > $O/bench_plain.json 2> $O/bench_plain.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > /dev/null 2>&1
 SMALL="python bench.py --envs 512 --steps 1 --warmup 3 --no-e2e --no-cpu"
 $SMALL > $O/small_plain.json 2>&1
-for k in raster_warp_kernel project_kernel cull_count_kernel depth_downsweep place_downsweep depth_upsweep place_upsweep depth_scan place_scan; do
+for k in raster_warp_kernel project_kernel cull_count_kernel depth_downsweep place_downsweep depth_upsweep place_upsweep depth_ties depth_scan place_scan; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o $O/full_$k $SMALL > $O/ncu_$k.log 2>&1 || echo "ncu $k failed"
 done
 ls -la $O
