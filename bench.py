@@ -511,28 +511,47 @@ def main():
     # ---- e2e through the public API with host buffers (pinned)
     e2e = None
     if not args.no_e2e:
-        h_ids = ids_np
-        h_vm = vm[: max(2, min(n_sets, 4))]
-        h_in = np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1))
-        h_rgb = torch.empty((E, H, W, 3), dtype=torch.uint8).pin_memory() if want_rgb else None
-        h_depth = torch.empty((E, H, W), dtype=torch.float32).pin_memory() if want_depth else None
+        # inputs from pinned host memory, frames to pinned host memory, every step
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        h_ids = pin(ids_np)
+        h_vm = [pin(vm[k]) for k in range(min(n_sets, 4))]
+        h_in = pin(np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1)))
+        outs = []
+        for _ in range(2):   # two host frame sets: the pipelined loop alternates them
+            outs.append((torch.empty((E, H, W, 3), dtype=torch.uint8, pin_memory=True) if want_rgb else None,
+                         torch.empty((E, H, W), dtype=torch.float32, pin_memory=True) if want_depth else None))
         hopts = gg.default_opts(flags=tiles_flag)
-        gg.gg_render_host(R.ctx, E, h_ids, h_vm[0], h_in, W, H, hopts, h_rgb, h_depth, None, stream)
+        gg.gg_render_host(R.ctx, E, h_ids, h_vm[0], h_in, W, H, hopts, outs[0][0], outs[0][1], None, stream)
         ke = max(2, min(args.steps, 5))
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for k in range(ke):
-            gg.gg_render_host(R.ctx, E, h_ids, h_vm[k % len(h_vm)], h_in, W, H, hopts, h_rgb, h_depth, None, stream)
-        torch.cuda.synchronize()
-        dt = max_over_ranks(time.perf_counter() - t0, cdev)
+
+        def timed(pipelined):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for k in range(ke):
+                o = outs[k % 2]
+                if pipelined:   # the RL loop's double-buffered observations: step k+1 renders while k copies out
+                    gg.gg_render_host_async(R.ctx, E, h_ids, h_vm[k % len(h_vm)], h_in, W, H, hopts, o[0], o[1],
+                                            None, stream)
+                else:           # one blocking call per step: frames are in host memory when it returns
+                    gg.gg_render_host(R.ctx, E, h_ids, h_vm[k % len(h_vm)], h_in, W, H, hopts, o[0], o[1], None,
+                                      stream)
+            gg.gg_host_sync(R.ctx)
+            torch.cuda.synchronize()
+            return max_over_ranks(time.perf_counter() - t0, cdev)
+
+        dt = timed(True)
+        dt_sync = timed(False)
         h2d = E * (4 + 64 + 16)
         d2h = E * W * H * ((3 if want_rgb else 0) + (4 if want_depth else 0))
         e2e = {"value": E * world * ke / dt, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": d2h * world, "steps": ke,
-               "note": "gg_render_host: pinned host inputs -> device, frames -> pinned host, every step"}
-        del h_rgb, h_depth
+               "value_blocking": E * world * ke / dt_sync,
+               "note": ("gg_render_host_async + gg_host_sync: pinned host inputs -> device and frames -> pinned host "
+                        "every step, two host frame sets alternating (step k+1 renders while step k's frames copy "
+                        "out); value_blocking = one blocking gg_render_host per step")}
+        del outs
 
     # ---- rooflines (live CUDA-event stage times on the render stream)
     meta = argparse.Namespace(n=wl.n_gauss, sh_degree=wl.sh_degree)   # every rank (only rank 0 holds a host scene)

@@ -161,6 +161,21 @@ gg_status gg_render_host(gg_context* ctx, int32_t n_envs, const int32_t* scene_i
                          const gg_render_opts* opts, void* rgb, float* depth, float* alpha,
                          void* stream);
 
+/* Pipelined form of gg_render_host (the RL loop's double-buffered
+ * observations): returns once the inputs, the render and the frame copies are
+ * enqueued.  Two internal device staging slots alternate between calls, so
+ * call t + 1 renders while call t's frames still stream to the host; the host
+ * buffers of a call must stay valid, and must not be read, until
+ * gg_host_sync returns (which waits for every outstanding frame copy).  The
+ * call still blocks on the render stream between the pipeline stages of each
+ * env chunk (workspace sizing), as gg_render does.  GG_ASYNC is not accepted
+ * here (GG_E_UNSUPPORTED). */
+gg_status gg_render_host_async(gg_context* ctx, int32_t n_envs, const int32_t* scene_ids,
+                               const float* viewmats, const float* intrinsics, int32_t width, int32_t height,
+                               const gg_render_opts* opts, void* rgb, float* depth, float* alpha,
+                               void* stream);
+gg_status gg_host_sync(gg_context* ctx);
+
 /* Motion blur (§3.3 "rendering a small set of frames offset
  * along the camera's velocity direction and alpha-blending them into a
  * single image"; SPEC.md:221-229 render_with_motion_blur).  Readings

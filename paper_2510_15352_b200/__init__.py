@@ -33,7 +33,8 @@ GG_ELLIPSE_TILES = 16       # + ellipse-intersects-tile masks (DESIGN.md reading
 EXPORTS = ["gg_default_opts", "gg_create", "gg_destroy", "gg_load_scene", "gg_unload_scene", "gg_reserve",
            "gg_render", "gg_render_host", "gg_render_blur", "gg_blur_poses", "gg_checksum", "gg_check_errors", "gg_debug_dump", "gg_get_counters",
            "gg_launch_count", "gg_set_timing", "gg_get_stage_ms", "gg_last_error", "gg_status_string",
-           "gg_read_ply", "gg_load_ply", "gg_ply_error", "gg_reserve_async", "gg_dino_input", "gg_get_stage_times"]
+           "gg_read_ply", "gg_load_ply", "gg_ply_error", "gg_reserve_async", "gg_dino_input", "gg_get_stage_times",
+           "gg_render_host_async", "gg_host_sync"]
 
 
 class GGError(RuntimeError):
@@ -80,6 +81,8 @@ def load_library(path: str = LIB_PATH):
     L.gg_reserve_async.argtypes = [vp, i32, i32, i32, i32, C.c_float, C.c_float]
     L.gg_render.argtypes = [vp, i32, vp, vp, vp, i32, i32, C.POINTER(gg_render_opts), vp, vp, vp, vp]
     L.gg_render_host.argtypes = [vp, i32, vp, vp, vp, i32, i32, C.POINTER(gg_render_opts), vp, vp, vp, vp]
+    L.gg_render_host_async.argtypes = [vp, i32, vp, vp, vp, i32, i32, C.POINTER(gg_render_opts), vp, vp, vp, vp]
+    L.gg_host_sync.argtypes = [vp]
     L.gg_render_blur.argtypes = [vp, i32, vp, vp, vp, vp, vp, C.c_float, i32, i32, i32, C.POINTER(gg_render_opts),
                                  vp, vp, vp, vp]
     L.gg_blur_poses.argtypes = [vp, i32, vp, vp, vp, C.c_float, i32, vp, vp]
@@ -221,6 +224,19 @@ def gg_render_host(ctx, n_envs, scene_ids, viewmats, intrinsics, width, height, 
     _check(ctx, load_library().gg_render_host(ctx, int(n_envs), _ptr(scene_ids), _ptr(viewmats), _ptr(intrinsics),
                                               int(width), int(height), C.byref(o), _ptr(rgb), _ptr(depth),
                                               _ptr(alpha), _stream_handle(stream)))
+
+
+def gg_render_host_async(ctx, n_envs, scene_ids, viewmats, intrinsics, width, height, opts=None, rgb=None,
+                         depth=None, alpha=None, stream=None):
+    """gg_render_host without the final wait: host buffers are valid after gg_host_sync."""
+    o = opts if opts is not None else default_opts()
+    _check(ctx, load_library().gg_render_host_async(ctx, int(n_envs), _ptr(scene_ids), _ptr(viewmats),
+                                                    _ptr(intrinsics), int(width), int(height), C.byref(o), _ptr(rgb),
+                                                    _ptr(depth), _ptr(alpha), _stream_handle(stream)))
+
+
+def gg_host_sync(ctx):
+    _check(ctx, load_library().gg_host_sync(ctx))
 
 
 def gg_render_blur(ctx, n_envs, scene_ids, viewmats, intrinsics, lin_vel, ang_vel, shutter, K, width, height,

@@ -115,7 +115,10 @@ struct gg_context {
   const DevBuf* last_counters = nullptr;   // counters buffer of the last render
   DevBuf errflag, valid_out;
   DevBuf dbg_tc, dbg_proj, dbg_stile, dbg_sz, dbg_sgid, dbg_neval;
-  DevBuf h_in;   // device copies for gg_render_host (ids | viewmats | intr | outputs)
+  DevBuf h_in[2];   // device staging of gg_render_host(_async) (ids | viewmats | intr | outputs), ping-pong
+  cudaEvent_t h_done[2] = {nullptr, nullptr};   // end of the frame copies of the call that last used slot i
+  bool h_pending[2] = {false, false};
+  int h_slot = 0;
   DevBuf blur_vm, blur_ids, blur_intr;   // gg_render_blur sample cameras
   // pinned host mirrors
   uint32_t* h_vcnt = nullptr;
@@ -330,7 +333,7 @@ gg_status gg_destroy(gg_context* ctx) {
     for (int i = 0; i < Work::count; ++i) dev_free(ctx, w->all()[i], s);
   DevBuf* all[] = {&ctx->scene_table, &ctx->errflag, &ctx->valid_out,
                    &ctx->dbg_tc, &ctx->dbg_proj, &ctx->dbg_stile, &ctx->dbg_sz, &ctx->dbg_sgid,
-                   &ctx->dbg_neval, &ctx->h_in, &ctx->blur_vm, &ctx->blur_ids,
+                   &ctx->dbg_neval, &ctx->h_in[0], &ctx->h_in[1], &ctx->blur_vm, &ctx->blur_ids,
                    &ctx->blur_intr};
   for (DevBuf* b : all) dev_free(ctx, *b, s);
   cudaStreamSynchronize(s);
@@ -339,6 +342,8 @@ gg_status gg_destroy(gg_context* ctx) {
   cudaFreeHost(ctx->h_ids); cudaFreeHost(ctx->h_perm); cudaFreeHost(ctx->h_groups); cudaFreeHost(ctx->h_blkbase);
   cudaFreeHost(ctx->h_vm);
   cudaEventDestroy(ctx->ev_copy);
+  for (auto& e : ctx->h_done)
+    if (e) cudaEventDestroy(e);
   cudaStreamDestroy(s);
   delete ctx;
   return GG_OK;
@@ -1102,14 +1107,24 @@ static gg_status copy_out_chunk(gg_context* ctx, int p0, int n, void* user) {
   return GG_OK;
 }
 
-gg_status gg_render_host(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
-                         const float* intr, int32_t W, int32_t H, const gg_render_opts* opts, void* rgb,
-                         float* depth, float* alpha, void* stream) {
+// Host-buffer render.  Two device staging slots alternate between calls, so
+// call t + 1 renders while call t's frames are still copying to the host: the
+// render stream only waits (on the device) for the copies of call t - 1, which
+// used the same slot.  The async form returns once everything is enqueued;
+// gg_host_sync waits for every outstanding frame copy.
+gg_status gg_render_host_async(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
+                               const float* intr, int32_t W, int32_t H, const gg_render_opts* opts, void* rgb,
+                               float* depth, float* alpha, void* stream) {
   if (!ctx) return GG_E_INVALID;
   if (E <= 0 || W <= 0 || H <= 0) return fail(ctx, GG_E_INVALID, "gg_render_host: bad sizes");
   if (!scene_ids || !viewmats || !intr) return fail(ctx, GG_E_INVALID, "gg_render_host: null input pointer");
+  if (opts && (opts->flags & GG_ASYNC)) return fail(ctx, GG_E_UNSUPPORTED, "gg_render_host: GG_ASYNC needs device buffers");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)stream;
+  const int slot = ctx->h_slot;
+  ctx->h_slot ^= 1;
+  if (!ctx->h_done[slot]) CK(cudaEventCreateWithFlags(&ctx->h_done[slot], cudaEventDisableTiming));
+  if (ctx->h_pending[slot]) CK(cudaStreamWaitEvent(s, ctx->h_done[slot], 0));   // slot's previous frames are out
   const int fmt = opts ? opts->rgb_format : 0;
   const size_t px = (size_t)W * H;
   const size_t rgb_px = fmt == 1 ? 12 : 3;
@@ -1119,8 +1134,8 @@ gg_status gg_render_host(gg_context* ctx, int32_t E, const int32_t* scene_ids, c
   const size_t out_a = alpha ? (size_t)E * px * 4 : 0;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
   const size_t total = al(in_bytes) + al(out_rgb) + al(out_d) + al(out_a);
-  if (!ensure(ctx, ctx->h_in, total, s)) return fail(ctx, GG_E_OOM, "gg_render_host: device staging");
-  uint8_t* base = P<uint8_t>(ctx->h_in);
+  if (!ensure(ctx, ctx->h_in[slot], total, s)) return fail(ctx, GG_E_OOM, "gg_render_host: device staging");
+  uint8_t* base = P<uint8_t>(ctx->h_in[slot]);
   int32_t* d_ids = (int32_t*)base;
   float* d_vm = (float*)(base + (size_t)E * 4);
   float* d_in = (float*)(base + (size_t)E * 68);
@@ -1134,9 +1149,26 @@ gg_status gg_render_host(gg_context* ctx, int32_t E, const int32_t* scene_ids, c
   gg_status st = render_impl(ctx, E, d_ids, d_vm, d_in, W, H, opts, rgb ? (void*)d_rgb : nullptr,
                              depth ? d_depth : nullptr, alpha ? d_alpha : nullptr, s, copy_out_chunk, &hc);
   if (st != GG_OK) return st;
-  CK(cudaStreamSynchronize(ctx->own));
-  CK(cudaStreamSynchronize(s));
+  CK(cudaEventRecord(ctx->h_done[slot], ctx->own));   // every frame copy of this call
+  ctx->h_pending[slot] = true;
   return GG_OK;
+}
+
+gg_status gg_host_sync(gg_context* ctx) {
+  if (!ctx) return GG_E_INVALID;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->own));
+  ctx->h_pending[0] = ctx->h_pending[1] = false;
+  return GG_OK;
+}
+
+gg_status gg_render_host(gg_context* ctx, int32_t E, const int32_t* scene_ids, const float* viewmats,
+                         const float* intr, int32_t W, int32_t H, const gg_render_opts* opts, void* rgb,
+                         float* depth, float* alpha, void* stream) {
+  gg_status st = gg_render_host_async(ctx, E, scene_ids, viewmats, intr, W, H, opts, rgb, depth, alpha, stream);
+  if (st != GG_OK) return st;
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return gg_host_sync(ctx);
 }
 
 gg_status gg_blur_poses(gg_context* ctx, int32_t E, const float* viewmats, const float* lin, const float* ang,

@@ -263,6 +263,29 @@ def test_render_host_multi_scene_slices(gg, R):
     assert np.array_equal(alpha.numpy(), ref[2])
 
 
+def test_render_host_async_pipelined(gg, R):
+    """gg_render_host_async: 4 back-to-back calls with different poses into 4
+    host frame sets (the two device staging slots are reused while earlier
+    frames may still be copying out), then gg_host_sync: every set equals the
+    device render of its poses."""
+    scs = [gi.random_cloud(720 + k, 200, sh_degree=k) for k in range(2)]
+    sids = [load(R, sc) for sc in scs]
+    E, W, H = 300, 48, 32
+    ids = np.array(sids, np.int32)[gi.rng(gi.KIND_CAMERAS, 721).integers(0, 2, E)]
+    gg.gg_reserve(R.ctx, E, W, H, 128)
+    poses = [gi.cloud_cameras(730 + k, E, W, H) for k in range(4)]
+    refs = [render(gg, R, ids, c) for c in poses]
+    outs = [(torch.zeros((E, H, W, 3), dtype=torch.uint8).pin_memory(),
+             torch.zeros((E, H, W), dtype=torch.float32).pin_memory(),
+             torch.zeros((E, H, W), dtype=torch.float32).pin_memory()) for _ in poses]
+    for c, o in zip(poses, outs):
+        gg.gg_render_host_async(R.ctx, E, ids, c.viewmats, c.intrinsics, W, H, None, *o)
+    gg.gg_host_sync(R.ctx)
+    for ref, o in zip(refs, outs):
+        for a, b in zip(ref, o):
+            assert np.array_equal(a, b.numpy())
+
+
 def test_errors(gg, R):
     sc = gi.random_cloud(800, 10)
     with pytest.raises(gg.GGError) as ei:
