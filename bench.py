@@ -186,13 +186,13 @@ STAGES = ("cull", "project", "depth_sort", "placement", "raster")
 
 
 def alu_peak_measured(clock_mhz):
-    """FP32 lane-ops/s measured by tools/ubench/alu_peak (profiles/round2/alu_peak.json), scaled to the run's
-    SM clock; None if absent."""
+    """FP32 lane-ops/s and MUFU.EX2/s measured by tools/ubench/alu_peak (profiles/round2/alu_peak.json) on this
+    pool's B200 at its maximum SM clock (1965 MHz, the clock every bench run here has held); None if absent."""
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "round2", "alu_peak.json")))
-        best = max(d["ffma"]["lane_ops_per_s"] / d["ffma"]["sm_mhz_est"], d["ffma2"]["lane_ops_per_s"] / d["ffma2"]["sm_mhz_est"])
-        return {"lane_ops_per_s": best * clock_mhz, "ex2_per_s": d["ex2"]["lane_ops_per_s"] / d["ex2"]["sm_mhz_est"] * clock_mhz,
-                "source": "profiles/round2/alu_peak.json (FFMA / FFMA2 / MUFU.EX2 microbenchmark)"}
+        best = max(d["ffma"]["lane_ops_per_s"], d["ffma2"]["lane_ops_per_s"])
+        return {"lane_ops_per_s": best, "ex2_per_s": d["ex2"]["lane_ops_per_s"],
+                "source": "profiles/round2/alu_peak.json (FFMA / FFMA2 / MUFU.EX2 microbenchmark, 148 x 8 CTAs)"}
     except Exception:
         return None
 
