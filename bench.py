@@ -254,7 +254,7 @@ def roofline(args, c, E, W, H, S, scene, want_rgb, want_depth, stage_ms, clocks,
             "work": k["work"], "traffic": None}
     if dom == "raster":
         tr, src, cap_envs = ncu_traffic("raster_warp_kernel")
-        launch_envs = min(E, args.chunk or 1024)
+        launch_envs = min(E, args.chunk_used)
         if tr and cap_envs:
             tr = tr * launch_envs / cap_envs          # per launch of this run (DRAM bytes scale with envs)
         roof["traffic"] = tr
@@ -555,6 +555,7 @@ def main():
 
     # ---- rooflines (live CUDA-event stage times on the render stream)
     meta = argparse.Namespace(n=wl.n_gauss, sh_degree=wl.sh_degree)   # every rank (only rank 0 holds a host scene)
+    args.chunk_used = gg.gg_chunk_envs(R.ctx) or args.chunk or 1024    # envs per pipeline pass of the timed render
     roof, roof_path = roofline(args, c, E, W, H, S, meta, want_rgb, want_depth, stage_ms, clocks, kb,
                                (n_eval, n_contrib, n_vis, n_keys), (r_eval, r_contrib, r_vis, r_keys))
 
@@ -578,7 +579,7 @@ def main():
                           "sh_degree": wl.sh_degree, "width": W, "height": H, "depth": want_depth, "rgb": want_rgb,
                           "parallelism": f"env-sharded x{world}, scenes replicated",
                           "l2": "working set >> 126 MB L2 each step (8.8 GB outputs, GBs of workspace)",
-                          "chunk_envs": args.chunk or 1024, "render_mode": {"sync": "sync", "async": "async (GG_ASYNC)",
+                          "chunk_envs": args.chunk_used, "render_mode": {"sync": "sync", "async": "async (GG_ASYNC)",
                                           "graph": "GG_ASYNC render replayed from a CUDA graph"}[args.mode]
                           if not args.blur else "sync",
                           "tile_lists": {"paper": "paper 3-sigma circle rects",

@@ -109,7 +109,9 @@ gg_status gg_unload_scene(gg_context* ctx, int32_t scene_id);
 
 /* Pre-size the workspace for renders of up to max_envs envs at width x
  * height and set the env chunk size (envs processed per pipeline pass;
- * 0 = default).  Optional: gg_render grows the workspace on demand. */
+ * 0 = automatic: the largest of 4096, 2048, 1024 whose workspace estimate
+ * fits 60% of the device memory available when rendering).  Optional:
+ * gg_render grows the workspace on demand. */
 gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t width, int32_t height,
                      int32_t chunk_envs);
 
@@ -257,6 +259,9 @@ gg_status gg_get_counters(gg_context* ctx, int32_t n_envs, int64_t* host_dst);
 
 /* Number of kernels this context has launched since creation. */
 int64_t gg_launch_count(const gg_context* ctx);
+
+/* Envs per pipeline pass (chunk) of the last render (0 before any). */
+int32_t gg_chunk_envs(const gg_context* ctx);
 
 /* Per-stage device time (ms) of the last render, measured with CUDA events on
  * the render stream when `enable` was set by gg_set_timing (events are

@@ -34,7 +34,8 @@ EXPORTS = ["gg_default_opts", "gg_create", "gg_destroy", "gg_load_scene", "gg_un
            "gg_render", "gg_render_host", "gg_render_blur", "gg_blur_poses", "gg_checksum", "gg_check_errors", "gg_debug_dump", "gg_get_counters",
            "gg_launch_count", "gg_set_timing", "gg_get_stage_ms", "gg_last_error", "gg_status_string",
            "gg_read_ply", "gg_load_ply", "gg_ply_error", "gg_reserve_async", "gg_dino_input", "gg_get_stage_times",
-           "gg_render_host_async", "gg_host_sync"]
+           "gg_render_host_async", "gg_host_sync",
+           "gg_chunk_envs"]
 
 
 class GGError(RuntimeError):
@@ -93,6 +94,8 @@ def load_library(path: str = LIB_PATH):
     L.gg_get_counters.argtypes = [vp, i32, vp]
     L.gg_launch_count.argtypes = [vp]
     L.gg_launch_count.restype = i64
+    L.gg_chunk_envs.argtypes = [vp]
+    L.gg_chunk_envs.restype = i32
     L.gg_set_timing.argtypes = [vp, i32]
     L.gg_get_stage_ms.argtypes = [vp, C.POINTER(C.c_float)]
     L.gg_get_stage_times.argtypes = [vp, C.POINTER(C.c_float), i32]
@@ -105,7 +108,8 @@ def load_library(path: str = LIB_PATH):
     L.gg_ply_error.argtypes = []
     L.gg_ply_error.restype = C.c_char_p
     for name in EXPORTS:
-        if name not in ("gg_default_opts", "gg_launch_count", "gg_last_error", "gg_status_string", "gg_ply_error"):
+        if name not in ("gg_default_opts", "gg_launch_count", "gg_last_error", "gg_status_string", "gg_ply_error",
+                        "gg_chunk_envs"):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -283,6 +287,10 @@ def gg_get_counters(ctx, n_envs: int) -> np.ndarray:
     a = np.zeros((n_envs, 4), np.int64)
     _check(ctx, load_library().gg_get_counters(ctx, n_envs, a.ctypes.data))
     return a
+
+
+def gg_chunk_envs(ctx) -> int:
+    return int(load_library().gg_chunk_envs(ctx))
 
 
 def gg_launch_count(ctx) -> int:
