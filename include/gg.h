@@ -110,8 +110,10 @@ gg_status gg_unload_scene(gg_context* ctx, int32_t scene_id);
 /* Pre-size the workspace for renders of up to max_envs envs at width x
  * height and set the env chunk size (envs processed per pipeline pass;
  * 0 = automatic: the largest of 4096, 2048, 1024 whose workspace estimate
- * fits 60% of the device memory available when rendering).  Optional:
- * gg_render grows the workspace on demand. */
+ * fits 80% of the device memory available when rendering; renders with host
+ * outputs use at most 1024).  Optional: gg_render grows the workspace on
+ * demand, and a chunk whose records or keys cannot be allocated is redone in
+ * halves before GG_E_OOM is returned. */
 gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t width, int32_t height,
                      int32_t chunk_envs);
 

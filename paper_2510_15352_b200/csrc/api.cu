@@ -355,8 +355,10 @@ gg_status gg_destroy(gg_context* ctx) {
 // Envs per pipeline pass when the caller did not fix it (gg_reserve chunk 0):
 // the largest of 4096, 2048, 1024 whose workspace estimate -- records,
 // depth-sort ping-pong and keys for `vis_frac` of the largest scene per env,
-// ~100 B per visible record -- fits 60% of the device memory available to
-// the context (free memory plus the workspace it already holds).  Fewer,
+// ~100 B per visible record -- fits 80% of the device memory available to
+// the context (free memory plus the workspace it already holds).  If a
+// chunk's records or keys still do not fit, render_impl redoes that chunk in
+// halves.  Fewer,
 // larger passes have fewer kernel tails and host round trips (c3: 24.08k,
 // 24.40k, 24.53k env-frames/s at 1024, 2048, 4096).
 static int auto_chunk(gg_context* ctx, int E, double vis_frac) {
@@ -369,7 +371,7 @@ static int auto_chunk(gg_context* ctx, int E, double vis_frac) {
   size_t held = 0;
   for (Work* w : {&ctx->sw, &ctx->aw})
     for (int i = 0; i < Work::count; ++i) held += w->all()[i].bytes;
-  const double avail = 0.6 * (double)(fr + held);
+  const double avail = 0.8 * (double)(fr + held);
   const double per_env = (double)std::max(max_scene_n(ctx), 1) * vis_frac * 100.0;
   for (int c : {4096, 2048})
     if ((double)std::min(E, c) * per_env <= avail) return std::min(E, c);
@@ -522,7 +524,7 @@ gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t W, int32_t H, in
   if (chunk > 0) ctx->chunk = chunk;
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->own;
-  const int ec = auto_chunk(ctx, max_envs, 0.35);
+  const int ec = auto_chunk(ctx, max_envs, 0.3);
   const int nmax = std::max(max_scene_n(ctx), 1);
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   const int ntiles = ((W + TILE - 1) / TILE) * ((H + TILE - 1) / TILE);
@@ -651,7 +653,8 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   const int nmax = std::max(max_scene_n(ctx), 1);
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   const int nwords = nblk * (PROJ_BLOCK / 32);
-  int chunk = auto_chunk(ctx, E, 0.35);
+  int chunk = auto_chunk(ctx, E, 0.3);
+  if (cb) chunk = std::min(chunk, 1024);   // host outputs: finer chunks interleave the frame copies with compute
   ctx->last_chunk = chunk;
   if (blur) chunk = std::max(blur->Kc, chunk / blur->Kc * blur->Kc);   // an env's samples never straddle chunks
 
@@ -806,9 +809,17 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
         (rp.ellipse && !ensure(ctx, ctx->sw.rmask, V * 4 + 4, s)) ||
         (keep && !ensure(ctx, ctx->sw.dconic, V * 16, s)) ||
         !ensure(ctx, ctx->sw.dk0, V * 8, s) || !ensure(ctx, ctx->sw.dk1, V * 8, s) ||
-        !ensure(ctx, ctx->sw.dv0, V * 4, s))
+        !ensure(ctx, ctx->sw.dv0, V * 4, s)) {
+      const int unit = blur ? blur->Kc : 64;
+      if (ec >= 2 * unit) {   // too many records for the memory left: redo this chunk in halves
+        chunk = std::max(unit, (ec / 2) / unit * unit);
+        ec = 0;
+        --cidx;
+        continue;
+      }
       return fail(ctx, GG_E_OOM, "gg_render: record workspace (%llu records) allocation failed",
                   (unsigned long long)V);
+    }
     ctx->launches += launch_copy_words(ctx->sw.rbase.p, ctx->h_rbase, ec * 8, s);
     CK(cudaMemsetAsync(ws.kcnt, 0, ec * 8, s));
     ws.rec0 = P<float4>(ctx->sw.rec0); ws.rec1 = P<float4>(ctx->sw.rec1); ws.rec2 = P<float4>(ctx->sw.rec2);
@@ -831,8 +842,16 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
       if (ctx->h_kcnt[i] > 0xffffffffull)
         return fail(ctx, GG_E_CAPACITY, "gg_render: env %d has %llu tile keys (>= 2^32)", ctx->h_perm[e0 + i],
                     (unsigned long long)ctx->h_kcnt[i]);
-    if (!ensure(ctx, ctx->sw.sorted, K * 4, s))
+    if (!ensure(ctx, ctx->sw.sorted, K * 4, s)) {
+      const int unit = blur ? blur->Kc : 64;
+      if (ec >= 2 * unit) {   // too many keys for the memory left: redo this chunk in halves
+        chunk = std::max(unit, (ec / 2) / unit * unit);
+        ec = 0;
+        --cidx;
+        continue;
+      }
       return fail(ctx, GG_E_OOM, "gg_render: key workspace (%llu keys) allocation failed", (unsigned long long)K);
+    }
     ctx->launches += launch_copy_words(ctx->sw.kbase.p, ctx->h_kbase, ec * 8, s);
     ws.sorted = P<uint32_t>(ctx->sw.sorted);
 #ifdef GG_CHECK_PROTOCOLS

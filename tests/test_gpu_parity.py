@@ -286,6 +286,47 @@ def test_render_host_async_pipelined(gg, R):
             assert np.array_equal(a, b.numpy())
 
 
+def test_chunk_halving_when_workspace_allocation_fails(gg):
+    """A chunk whose record workspace cannot be allocated is redone in halves:
+    with an allocator that refuses blocks above 1 MB, a 512-env chunk (~1.6 MB
+    of rec0) falls back to smaller chunks and the frames are unchanged."""
+    import ctypes as C
+    sc = gi.random_cloud(740, 300)
+    E, W, H = 512, 64, 64
+    cams = gi.cloud_cameras(740, E, W, H)
+    r_ref = gg.Renderer(0)
+    try:
+        sid = load(r_ref, sc)
+        gg.gg_reserve(r_ref.ctx, E, W, H, 512)
+        ref = render(gg, r_ref, [sid] * E, cams)
+    finally:
+        r_ref.close()
+    base, keep = gg.torch_allocator(0)
+    LIMIT = 1 << 20
+
+    def _alloc(size, stream, user):
+        return 0 if size > LIMIT else base.alloc(size, stream, user)
+
+    fa = gg.ALLOC_FN(_alloc)
+    lim = gg.gg_allocator(fa, base.free, None)
+    ctx = gg.gg_create(0, lim)
+    try:
+        sid = gg.gg_load_scene(ctx, sc.n, sc.sh_degree, dev(sc.means), dev(sc.scales), dev(sc.quats),
+                               dev(sc.opacities), dev(sc.sh))
+        gg.gg_reserve(ctx, E, W, H, 512)
+        out = [torch.zeros((E, H, W, 3), dtype=torch.uint8, device="cuda"),
+               torch.zeros((E, H, W), device="cuda"), torch.zeros((E, H, W), device="cuda")]
+        gg.gg_render(ctx, E, dev(np.full(E, sid, np.int32)), dev(cams.viewmats), dev(cams.intrinsics), W, H, None,
+                     *out)
+        gg.gg_check_errors(ctx)
+        torch.cuda.synchronize()
+        for a, b in zip(ref, out):
+            assert np.array_equal(a, b.cpu().numpy())
+    finally:
+        gg.gg_destroy(ctx)
+    del keep, fa
+
+
 def test_errors(gg, R):
     sc = gi.random_cloud(800, 10)
     with pytest.raises(gg.GGError) as ei:
