@@ -864,8 +864,16 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     const int passes = depth_passes_for(opts.near_plane, opts.far_plane);
     if (!ensure(ctx, ctx->sw.blkbase, (size_t)(ec + 1) * 4, s) || !ensure(ctx, ctx->sw.blkenv, (size_t)nb * 4 + 4, s) ||
         !ensure(ctx, ctx->sw.ghist, (size_t)nb * sort_ghist_words() * 4, s) ||
-        !ensure(ctx, ctx->sw.thist, (size_t)nb * ntiles * 4, s))
+        !ensure(ctx, ctx->sw.thist, (size_t)nb * ntiles * 4, s)) {
+      const int unit = blur ? blur->Kc : 64;
+      if (ec >= 2 * unit) {   // redo this chunk in halves
+        chunk = std::max(unit, (ec / 2) / unit * unit);
+        ec = 0;
+        --cidx;
+        continue;
+      }
       return fail(ctx, GG_E_OOM, "gg_render: sort workspace allocation failed");
+    }
     ctx->launches += launch_copy_words(ctx->sw.blkbase.p, ctx->h_blkbase, (size_t)(ec + 1) * 4, s);
     ctx->launches += launch_sort_bin(ec, nb, P<uint32_t>(ctx->sw.blkbase), P<uint32_t>(ctx->sw.blkenv), passes, rp, ws,
                                      P<uint32_t>(ctx->sw.ghist),
