@@ -111,6 +111,8 @@ struct gg_context {
   int scene_table_cap = 0;
   int chunk = DEFAULT_CHUNK;
   int last_chunk = 0;   // envs per pass of the last render
+  int ac_E = -1, ac_n = -1, ac_chunk = 0;   // auto_chunk cache
+  double ac_frac = 0.0;
   // workspace: sync path (sw) and sync-free path (aw), see Work
   Work sw, aw;
   const DevBuf* last_counters = nullptr;   // counters buffer of the last render
@@ -363,6 +365,10 @@ gg_status gg_destroy(gg_context* ctx) {
 // 24.40k, 24.53k env-frames/s at 1024, 2048, 4096).
 static int auto_chunk(gg_context* ctx, int E, double vis_frac) {
   if (ctx->chunk > 0) return std::min(E, ctx->chunk);
+  // cached per (E, largest scene, estimate): cudaMemGetInfo costs milliseconds
+  // on a context holding tens of GB, too much to pay on every render
+  const int nmax = max_scene_n(ctx);
+  if (ctx->ac_E == E && ctx->ac_n == nmax && ctx->ac_frac == vis_frac) return ctx->ac_chunk;
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
     cudaGetLastError();
@@ -373,9 +379,17 @@ static int auto_chunk(gg_context* ctx, int E, double vis_frac) {
     for (int i = 0; i < Work::count; ++i) held += w->all()[i].bytes;
   const double avail = 0.8 * (double)(fr + held);
   const double per_env = (double)std::max(max_scene_n(ctx), 1) * vis_frac * 100.0;
-  for (int c : {4096, 2048})
-    if ((double)std::min(E, c) * per_env <= avail) return std::min(E, c);
-  return std::min(E, 1024);
+  int c = std::min(E, 1024);
+  for (int cand : {4096, 2048})
+    if ((double)std::min(E, cand) * per_env <= avail) {
+      c = std::min(E, cand);
+      break;
+    }
+  ctx->ac_E = E;
+  ctx->ac_n = nmax;
+  ctx->ac_frac = vis_frac;
+  ctx->ac_chunk = c;
+  return c;
 }
 
 static gg_status upload_scene_table(gg_context* ctx) {
