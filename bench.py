@@ -398,13 +398,16 @@ def main():
     ids_np = np.asarray(sids, np.int32)[binding]
     gg.gg_reserve(R.ctx, E, W, H, args.chunk)
     use_async = args.mode in ("async", "graph") and not args.blur
-    if use_async:
-        gg.gg_reserve_async(R.ctx, E, W, H, args.chunk, 0.7, 4.0)
     tiles_flag = {"paper": 0, "tight": gg.GG_TIGHT_TILES, "ellipse": gg.GG_ELLIPSE_TILES}[args.tiles]
     mflag = (gg.GG_ASYNC if use_async else 0) | tiles_flag
     intr = t(np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1)))
     vm_d = t(vm)
     ids = t(ids_np)
+    if use_async:
+        # sync-free capacities calibrated by a synchronous render of the first pose set: 1.5x the densest
+        # chunk it saw (gg_reserve_async with a negative max_visible_frac)
+        gg.gg_render(R.ctx, E, ids, vm_d[0], intr, W, H, gg.default_opts(flags=tiles_flag), None, None, None)
+        gg.gg_reserve_async(R.ctx, E, W, H, args.chunk, -1.5, 0.0)
     rgb = torch.empty((E, H, W, 3), dtype=torch.uint8, device=dev) if want_rgb else None
     depth = torch.empty((E, H, W), dtype=torch.float32, device=dev) if want_depth else None
     stream = torch.cuda.current_stream()

@@ -56,7 +56,9 @@ class RateDecoupledRenderer:
         self.rgb = torch.empty((E, H, W, 3), dtype=torch.uint8, device=dev)
         self.depth = torch.empty((E, H, W), dtype=torch.float32, device=dev)
         self.dino = torch.empty((E, 3, dino_size, dino_size), dtype=torch.bfloat16, device=dev)
-        gg.gg_reserve_async(ctx, E, W, H, 0, 0.7, 4.0)
+        # capacities from a synchronous render of the first poses (1.5x the densest chunk seen)
+        gg.gg_render(ctx, E, scene_ids, viewmats, intrinsics, W, H, gg.default_opts(flags=gg.GG_TIGHT_TILES))
+        gg.gg_reserve_async(ctx, E, W, H, 0, -1.5, 0.0)
         opts = gg.default_opts(flags=gg.GG_ASYNC | gg.GG_TIGHT_TILES)
         self.stream = torch.cuda.Stream()
         self.stream.wait_stream(torch.cuda.current_stream())

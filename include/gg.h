@@ -122,7 +122,11 @@ gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t width, int32_t h
  * of up to max_envs envs at exactly width x height then run without any host
  * synchronisation or allocation, so they can be captured in a CUDA graph.
  * Capacities per env chunk: records = chunk * max_scene_n * max_visible_frac,
- * keys = records * keys_per_visible.  Envs are processed in caller order in
+ * keys = records * keys_per_visible.  A NEGATIVE max_visible_frac = -h sizes
+ * both from what earlier synchronous renders at this width x height saw
+ * instead: h times the densest observed chunk's records (keys) per env times
+ * the chunk, and at least h times the largest single env; keys_per_visible
+ * is then ignored (GG_E_INVALID if no such render happened).  Envs are processed in caller order in
  * groups of 16 (sort envs by scene id for best projection efficiency).  On
  * overflow that chunk's frames are background and gg_check_errors returns
  * GG_E_CAPACITY.  Counters (GG_COUNTERS) are supported; intermediates are not. */

@@ -112,6 +112,12 @@ struct gg_context {
   int chunk = DEFAULT_CHUNK;
   int last_chunk = 0;   // envs per pass of the last render
   int ac_E = -1, ac_n = -1, ac_chunk = 0;   // auto_chunk cache
+  // observed by synchronous renders (calibrates gg_reserve_async): the
+  // densest chunk's records and keys per env, the largest single env, and
+  // the image size they were seen at
+  double cal_vmean = 0.0, cal_kmean = 0.0;
+  uint64_t cal_vmax = 0, cal_kmax = 0;
+  int cal_W = 0, cal_H = 0;
   double ac_frac = 0.0;
   // workspace: sync path (sw) and sync-free path (aw), see Work
   Work sw, aw;
@@ -852,6 +858,19 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     CK(cudaStreamSynchronize(s));
     uint64_t K = 0;
     for (int i = 0; i < ec; ++i) { ctx->h_kbase[i] = K; K += ctx->h_kcnt[i]; }
+    if (!blur) {   // calibration record for gg_reserve_async (negative max_visible_frac)
+      if (ctx->cal_W != W || ctx->cal_H != H) {
+        ctx->cal_vmean = ctx->cal_kmean = 0.0;
+        ctx->cal_vmax = ctx->cal_kmax = 0;
+        ctx->cal_W = W; ctx->cal_H = H;
+      }
+      ctx->cal_vmean = std::max(ctx->cal_vmean, (double)V / ec);
+      ctx->cal_kmean = std::max(ctx->cal_kmean, (double)K / ec);
+      for (int i = 0; i < ec; ++i) {
+        ctx->cal_vmax = std::max<uint64_t>(ctx->cal_vmax, ctx->h_vcnt[i]);
+        ctx->cal_kmax = std::max<uint64_t>(ctx->cal_kmax, ctx->h_kcnt[i]);
+      }
+    }
     for (int i = 0; i < ec; ++i)
       if (ctx->h_kcnt[i] > 0xffffffffull)
         return fail(ctx, GG_E_CAPACITY, "gg_render: env %d has %llu tile keys (>= 2^32)", ctx->h_perm[e0 + i],
@@ -1086,23 +1105,34 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
 gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t H, int32_t chunk,
                            float max_visible_frac, float keys_per_visible) {
   if (!ctx) return GG_E_INVALID;
-  if (max_envs <= 0 || W <= 0 || H <= 0 || chunk < 0 || !(max_visible_frac > 0.f) || max_visible_frac > 1.f ||
-      !(keys_per_visible > 0.f))
+  const bool calibrated = max_visible_frac < 0.f;   // capacities from earlier synchronous renders
+  if (max_envs <= 0 || W <= 0 || H <= 0 || chunk < 0 || !(max_visible_frac != 0.f) || max_visible_frac > 1.f ||
+      (!calibrated && !(keys_per_visible > 0.f)) || !std::isfinite(max_visible_frac))
     return fail(ctx, GG_E_INVALID, "gg_reserve_async: bad arguments");
+  if (calibrated && (ctx->cal_W != W || ctx->cal_H != H || ctx->cal_vmax == 0))
+    return fail(ctx, GG_E_INVALID, "gg_reserve_async: calibrated capacities need a synchronous render at %dx%d first",
+                W, H);
   if (ctx->scenes.empty()) return fail(ctx, GG_E_INVALID, "gg_reserve_async: load the scenes first");
   const int TX = (W + TILE - 1) / TILE, TY = (H + TILE - 1) / TILE, ntiles = TX * TY;
   if (ntiles > MAX_TILES) return fail(ctx, GG_E_UNSUPPORTED, "gg_reserve_async: image too large");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->own;
   const int ch = chunk > 0 ? std::min(max_envs, chunk)
-                           : auto_chunk(ctx, max_envs, std::max(0.35, (double)max_visible_frac));
+                           : auto_chunk(ctx, max_envs, calibrated ? 0.3 : std::max(0.35, (double)max_visible_frac));
   const int nmax = std::max(max_scene_n(ctx), 1);
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   int maxdeg = 0;
   for (const auto& sc : ctx->scenes)
     if (sc.live) maxdeg = std::max(maxdeg, sc.d.degree);
-  const uint64_t vcap = (uint64_t)((double)ch * nmax * max_visible_frac) + 1;
-  const uint64_t kcap = (uint64_t)((double)vcap * keys_per_visible) + 1;
+  uint64_t vcap, kcap;
+  if (calibrated) {   // headroom h = -max_visible_frac over the densest observed chunk (and any single env)
+    const double h = -(double)max_visible_frac;
+    vcap = (uint64_t)(h * std::max(ch * ctx->cal_vmean, (double)ctx->cal_vmax)) + 1;
+    kcap = (uint64_t)(h * std::max(ch * ctx->cal_kmean, (double)ctx->cal_kmax)) + 1;
+  } else {
+    vcap = (uint64_t)((double)ch * nmax * max_visible_frac) + 1;
+    kcap = (uint64_t)((double)vcap * keys_per_visible) + 1;
+  }
   const uint64_t nbcap = vcap / (uint64_t)sort_block_size() + ch + 1;
   bool okb = ensure(ctx, ctx->aw.envc, sizeof(EnvConst) * max_envs, s) &&
              ensure(ctx, ctx->aw.flags, (size_t)ch * nblk * PROJ_WPB * 4, s) && ensure(ctx, ctx->aw.blkcnt, (size_t)ch * nblk * 4, s) &&

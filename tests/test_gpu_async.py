@@ -141,6 +141,26 @@ def test_graph_survives_sync_renders_and_scene_loads(gg):
     r.close()
 
 
+def test_calibrated_reservation(gg):
+    """gg_reserve_async(-h): capacities from a synchronous render at the same
+    size; refused without one; the sync-free render then equals the sync one."""
+    r = gg.Renderer(0)
+    sc = gi.config_scene("c1")
+    sid = r.load_scene(dev(sc.means), dev(sc.scales), dev(sc.quats), dev(sc.opacities), dev(sc.sh), sc.sh_degree)
+    E, W, H = 24, 64, 48
+    cams = gi.cameras(8, E, W, H, sc)
+    ids, vm, K = dev(np.full(E, sid, np.int32)), dev(cams.viewmats), dev(cams.intrinsics)
+    with pytest.raises(gg.GGError) as ei:
+        gg.gg_reserve_async(r.ctx, E, W, H, 0, -1.5, 0.0)
+    assert ei.value.status == gg.GG_E_INVALID
+    a = _render(gg, r, ids, vm, K, W, H)
+    gg.gg_reserve_async(r.ctx, E, W, H, 0, -1.5, 0.0)
+    b = _render(gg, r, ids, vm, K, W, H, flags=gg.GG_ASYNC)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    r.close()
+
+
 def test_async_capacity_overflow_is_reported(gg):
     r = gg.Renderer(0)
     sc = gi.config_scene("c1")

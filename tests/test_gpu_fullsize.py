@@ -86,9 +86,11 @@ def run_workload(gg, wl, flags=0, oflags=0, depth=True, n_image=N_IMAGE, n_int=N
         if mode == "sync":
             r.render(ids, vm, K, W, H, rgb=rgb, depth=dep, flags=flags)
         else:
-            # bench.py --mode graph: the GG_ASYNC render (bench's capacities) captured
-            # once in a CUDA graph, poses copied into the captured input, replayed
-            gg.gg_reserve_async(r.ctx, E, W, H, 0, 0.7, 4.0)
+            # bench.py --mode graph: capacities calibrated by a synchronous render (as the
+            # bench does), the GG_ASYNC render captured once in a CUDA graph, poses
+            # copied into the captured input, replayed
+            r.render(ids, dev(wl.viewmats[1 % wl.n_sets]), K, W, H, flags=flags)
+            gg.gg_reserve_async(r.ctx, E, W, H, 0, -1.5, 0.0)
             vm_static = dev(wl.viewmats[1 % wl.n_sets])
             opts = gg.default_opts(flags=flags | gg.GG_ASYNC)
             s = torch.cuda.Stream()
