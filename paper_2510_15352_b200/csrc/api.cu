@@ -111,14 +111,15 @@ struct gg_context {
   int scene_table_cap = 0;
   int chunk = DEFAULT_CHUNK;
   int last_chunk = 0;   // envs per pass of the last render
-  int ac_E = -1, ac_n = -1, ac_chunk = 0;   // auto_chunk cache
+  int ac_E = -1, ac_chunk = 0;   // auto_chunk cache
+  double ac_bytes = 0.0;
+  const void* ac_set = nullptr;
   // observed by synchronous renders (calibrates gg_reserve_async): the
   // densest chunk's records and keys per env, the largest single env, and
   // the image size they were seen at
   double cal_vmean = 0.0, cal_kmean = 0.0;
   uint64_t cal_vmax = 0, cal_kmax = 0;
   int cal_W = 0, cal_H = 0;
-  double ac_frac = 0.0;
   // workspace: sync path (sw) and sync-free path (aw), see Work
   Work sw, aw;
   const DevBuf* last_counters = nullptr;   // counters buffer of the last render
@@ -369,34 +370,36 @@ gg_status gg_destroy(gg_context* ctx) {
 // halves.  Fewer,
 // larger passes have fewer kernel tails and host round trips (c3: 24.08k,
 // 24.40k, 24.53k env-frames/s at 1024, 2048, 4096).
-static int auto_chunk(gg_context* ctx, int E, double vis_frac) {
+static int auto_chunk(gg_context* ctx, int E, double per_env_bytes, Work* reusable) {
   if (ctx->chunk > 0) return std::min(E, ctx->chunk);
-  // cached per (E, largest scene, estimate): cudaMemGetInfo costs milliseconds
-  // on a context holding tens of GB, too much to pay on every render
-  const int nmax = max_scene_n(ctx);
-  if (ctx->ac_E == E && ctx->ac_n == nmax && ctx->ac_frac == vis_frac) return ctx->ac_chunk;
+  // cached per (E, estimate, workspace set): cudaMemGetInfo costs
+  // milliseconds on a context holding tens of GB, too much for every render
+  if (ctx->ac_E == E && ctx->ac_bytes == per_env_bytes && ctx->ac_set == reusable) return ctx->ac_chunk;
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
     cudaGetLastError();
     return std::min(E, 1024);
   }
-  size_t held = 0;
-  for (Work* w : {&ctx->sw, &ctx->aw})
-    for (int i = 0; i < Work::count; ++i) held += w->all()[i].bytes;
+  size_t held = 0;   // the workspace this path already holds (it is reused, not added)
+  for (int i = 0; i < Work::count; ++i) held += reusable->all()[i].bytes;
   const double avail = 0.8 * (double)(fr + held);
-  const double per_env = (double)std::max(max_scene_n(ctx), 1) * vis_frac * 100.0;
   int c = std::min(E, 1024);
   for (int cand : {4096, 2048})
-    if ((double)std::min(E, cand) * per_env <= avail) {
+    if ((double)std::min(E, cand) * per_env_bytes <= avail) {
       c = std::min(E, cand);
       break;
     }
   ctx->ac_E = E;
-  ctx->ac_n = nmax;
-  ctx->ac_frac = vis_frac;
+  ctx->ac_bytes = per_env_bytes;
+  ctx->ac_set = reusable;
   ctx->ac_chunk = c;
   return c;
 }
+
+// ~100 B of workspace per visible record (records 64 B, depth-sort ping-pong
+// 16 B, keys ~2.2 x 4 B, order, histograms); the sync path budgets 30% of the
+// largest scene visible per env
+static double sync_env_bytes(const gg_context* ctx) { return (double)std::max(max_scene_n(ctx), 1) * 0.3 * 100.0; }
 
 static gg_status upload_scene_table(gg_context* ctx) {
   const int n = (int)ctx->scenes.size();
@@ -544,7 +547,7 @@ gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t W, int32_t H, in
   if (chunk > 0) ctx->chunk = chunk;
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->own;
-  const int ec = auto_chunk(ctx, max_envs, 0.3);
+  const int ec = auto_chunk(ctx, max_envs, sync_env_bytes(ctx), &ctx->sw);
   const int nmax = std::max(max_scene_n(ctx), 1);
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   const int ntiles = ((W + TILE - 1) / TILE) * ((H + TILE - 1) / TILE);
@@ -673,7 +676,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
   const int nmax = std::max(max_scene_n(ctx), 1);
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   const int nwords = nblk * (PROJ_BLOCK / 32);
-  int chunk = auto_chunk(ctx, E, 0.3);
+  int chunk = auto_chunk(ctx, E, sync_env_bytes(ctx), &ctx->sw);
   if (cb) chunk = std::min(chunk, 1024);   // host outputs: finer chunks interleave the frame copies with compute
   ctx->last_chunk = chunk;
   if (blur) chunk = std::max(blur->Kc, chunk / blur->Kc * blur->Kc);   // an env's samples never straddle chunks
@@ -1117,8 +1120,11 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
   if (ntiles > MAX_TILES) return fail(ctx, GG_E_UNSUPPORTED, "gg_reserve_async: image too large");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->own;
-  const int ch = chunk > 0 ? std::min(max_envs, chunk)
-                           : auto_chunk(ctx, max_envs, calibrated ? 0.3 : std::max(0.35, (double)max_visible_frac));
+  // records per env the reservation provides for, then the chunk (the sync
+  // workspace stays allocated, so only the async one counts as reusable)
+  const double h = calibrated ? -(double)max_visible_frac : 0.0;
+  const double rec_env = calibrated ? h * ctx->cal_vmean : (double)max_scene_n(ctx) * max_visible_frac;
+  const int ch = chunk > 0 ? std::min(max_envs, chunk) : auto_chunk(ctx, max_envs, rec_env * 100.0, &ctx->aw);
   const int nmax = std::max(max_scene_n(ctx), 1);
   const int nblk = (nmax + PROJ_BLOCK - 1) / PROJ_BLOCK;
   int maxdeg = 0;
@@ -1126,7 +1132,6 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
     if (sc.live) maxdeg = std::max(maxdeg, sc.d.degree);
   uint64_t vcap, kcap;
   if (calibrated) {   // headroom h = -max_visible_frac over the densest observed chunk (and any single env)
-    const double h = -(double)max_visible_frac;
     vcap = (uint64_t)(h * std::max(ch * ctx->cal_vmean, (double)ctx->cal_vmax)) + 1;
     kcap = (uint64_t)(h * std::max(ch * ctx->cal_kmean, (double)ctx->cal_kmax)) + 1;
   } else {
@@ -1304,7 +1309,7 @@ gg_status gg_render_blur(gg_context* ctx, int32_t E, const int32_t* scene_ids, c
   const bool need_depth = depth != nullptr;
   const int Kc = K + ((K % 2 == 0 && need_depth) ? 1 : 0);
   const int dk = (K % 2 == 1) ? (K - 1) / 2 : K;
-  const int ecb = std::max(1, std::min(E, auto_chunk(ctx, E * Kc, 0.35) / Kc));
+  const int ecb = std::max(1, std::min(E, auto_chunk(ctx, E * Kc, sync_env_bytes(ctx), &ctx->sw) / Kc));
   const size_t nk = (size_t)ecb * Kc;
   if (!ensure(ctx, ctx->blur_vm, nk * 64, s) || !ensure(ctx, ctx->blur_ids, nk * 4, s) ||
       !ensure(ctx, ctx->blur_intr, nk * 16, s))

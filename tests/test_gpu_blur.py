@@ -118,3 +118,21 @@ def test_blur_oracle_parity(gg, K):
     print(t)
     t.check()
     r.close()
+
+
+def test_blur_honours_tile_list_flags(gg):
+    """gg_render_blur keeps GG_TIGHT_TILES / GG_ELLIPSE_TILES; both
+    list variants give images identical to the paper's rects (R35, R37)."""
+    sc, cams, r, sid, lin, ang = _setup(gg, seed=11, E=5)
+    E, W, H = cams.n, cams.width, cams.height
+    outs = []
+    for flags in (0, gg.GG_TIGHT_TILES, gg.GG_ELLIPSE_TILES):
+        rgb, dep, al = _outs(E, H, W, 0)
+        gg.gg_render_blur(r.ctx, E, dev(np.full(E, sid, np.int32)), dev(cams.viewmats), dev(cams.intrinsics),
+                          dev(lin), dev(ang), 0.02, 3, W, H, gg.default_opts(flags=flags), rgb, dep, al)
+        torch.cuda.synchronize()
+        outs.append((rgb.cpu().numpy(), dep.cpu().numpy(), al.cpu().numpy()))
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert np.array_equal(a, b)
+    r.close()
