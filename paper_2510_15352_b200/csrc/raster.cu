@@ -432,6 +432,165 @@ raster_blur_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
   }
 }
 
+// ---------------------------------------------------------------------------
+// Producer/consumer variant (GG_RASTER_PC): warp 4 of a
+// 160-thread CTA loads each 32-record batch of the tile list ONCE per CTA,
+// evaluates the four 8x8-block box tests, and publishes the batch (records in
+// tile-relative form, plus a compacted index list per consumer warp) into a
+// ring of PC_NS shared-memory slots guarded by mbarriers (full: producer ->
+// consumers, empty: 4 consumer arrivals -> producer); warps 0-3 walk their
+// lists exactly as raster_warp_kernel does, with no CTA-wide barrier.  A
+// saturated consumer keeps releasing slots without work; once all four are
+// saturated the producer publishes a stop slot.  Bit-identical images.
+constexpr int PC_NS = 4;
+constexpr int PC_THREADS = 160;
+struct PcSlot {
+  float4 rec[32 * 3];       // tile_coefs, (A', B', C', z), (r, g, b, -)
+  uint8_t idx[4][32];       // per consumer warp: kept record indices, list order
+  uint32_t cnt[4];
+  uint32_t stop;
+};
+struct PcSmem {
+  PcSlot slot[PC_NS];
+  unsigned long long full[PC_NS], empty[PC_NS];
+  uint32_t ndone;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+template <bool RGB>
+__global__ void __launch_bounds__(PC_THREADS, 9)
+raster_pc_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, ChunkWS ws, void* __restrict__ rgb,
+                 float* __restrict__ depth, float* __restrict__ alpha_out) {
+  __shared__ PcSmem sm;
+  const int eloc = blockIdx.y, tile = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint2 rg = chunk_ok(ws.ok) ? ws.ranges[(size_t)eloc * rp.ntiles + tile] : make_uint2(0u, 0u);
+  const uint32_t nbatch = (rg.y - rg.x + 31u) / 32u;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PC_NS; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 4);
+    }
+    sm.ndone = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int tx = tile % rp.TX, ty = tile / rp.TX;
+  const float tox = (float)(tx * TILE) + 0.5f, toy = (float)(ty * TILE) + 0.5f;
+  if (warp == 4) {   // ---- producer
+    const float4* __restrict__ R0 = ws.rec0 + ws.rec_base[eloc];
+    const float4* __restrict__ R1 = ws.rec1 + ws.rec_base[eloc];
+    const float4* __restrict__ R2 = ws.rec2 + ws.rec_base[eloc];
+    const uint32_t* __restrict__ list = ws.sorted + ws.k_base[eloc];
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t nidx = rg.x + lane < rg.y ? __ldg(&list[rg.x + lane]) : 0u;
+    for (uint32_t bi = 0; bi < nbatch; ++bi) {
+      const int sl = (int)(bi % PC_NS);
+      const uint32_t ph = (bi / PC_NS) & 1u;
+      const uint32_t b = rg.x + 32u * bi;
+      const bool valid = b + lane < rg.y;
+      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
+      if (valid) { a0 = __ldg(&R0[nidx]); a1 = __ldg(&R1[nidx]); a2 = __ldg(&R2[nidx]); }
+      nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
+      const bool live = valid && a1.w >= 0.f && a0.z >= LOG2_CUTOFF;
+      const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
+      mbar_wait(&sm.empty[sl], ph ^ 1u);              // slot released by all four consumers
+      PcSlot& S = sm.slot[sl];
+      const bool stop = *((volatile uint32_t*)&sm.ndone) >= 4u;
+      if (lane == 0) S.stop = stop ? 1u : 0u;
+      if (!stop) {
+        S.rec[3 * lane] = tile_coefs(a0, a1, tox, toy);
+        S.rec[3 * lane + 1] = make_float4(a1.x, a1.y, a1.z, a0.w);
+        S.rec[3 * lane + 2] = a2;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const float bx0 = tox + 8.f * (w & 1), by0 = toy + 8.f * (w >> 1);
+          const bool mine = live && xh >= bx0 && xl <= bx0 + 7.f && yh >= by0 && yl <= by0 + 7.f;
+          const uint32_t m = __ballot_sync(0xffffffffu, mine);
+          if (mine) S.idx[w][__popc(m & lt)] = (uint8_t)lane;
+          if (lane == 0) S.cnt[w] = __popc(m);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.full[sl]);
+      if (stop) break;
+    }
+    return;
+  }
+  // ---- consumers: warp w = 8 x 8 block (bx, by) of the tile
+  int px, py0, py1;
+  const WarpGeom g = warp_geom(rp, tile, px, py0, py1);
+  f2 T = pk(1.f, 1.f), Cr = pk(0.f, 0.f), Cg = Cr, Cb = Cr, Dn = Cr;
+  const float INF = __int_as_float(0x7f800000);
+  float cut0 = g.in0 ? LOG2_CUTOFF : INF, cut1 = g.in1 ? LOG2_CUTOFF : INF;
+  bool done = false;
+  for (uint32_t bi = 0; bi < nbatch; ++bi) {
+    const int sl = (int)(bi % PC_NS);
+    mbar_wait(&sm.full[sl], (bi / PC_NS) & 1u);
+    const PcSlot& S = sm.slot[sl];
+    if (S.stop) break;
+    if (!done) {
+      const uint32_t cnt = S.cnt[warp];
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const uint32_t j = S.idx[warp][i];
+        const float4 r0 = S.rec[3 * j], r1 = S.rec[3 * j + 1];
+        const float P = fmaf(g.lx, fmaf(r1.x, g.lx, r0.y), r0.x);
+        const float Q = fmaf(r1.y, g.lx, r0.z);
+        float x0, x1;
+        upk(fma2(g.LY, fma2(pk(r1.z, r1.z), g.LY, pk(Q, Q)), pk(P, P)), x0, x1);
+        if (!__any_sync(0xffffffffu, x0 >= cut0 || x1 >= cut1)) continue;
+        const float al0 = x0 >= cut0 ? ex2_approx(fminf(x0, r0.w)) : 0.f;
+        const float al1 = x1 >= cut1 ? ex2_approx(fminf(x1, r0.w)) : 0.f;
+        f2 W = mul2(pk(al0, al1), T);
+        float tn0, tn1, w0, w1;
+        upk(sub2(T, W), tn0, tn1);
+        upk(W, w0, w1);
+        const bool s0 = tn0 < 1e-4f, s1 = tn1 < 1e-4f;
+        W = pk(s0 ? 0.f : w0, s1 ? 0.f : w1);
+        cut0 = s0 ? INF : cut0;
+        cut1 = s1 ? INF : cut1;
+        if (RGB) {
+          const float4 r2 = S.rec[3 * j + 2];
+          Cr = fma2(W, pk(r2.x, r2.x), Cr);
+          Cg = fma2(W, pk(r2.y, r2.y), Cg);
+          Cb = fma2(W, pk(r2.z, r2.z), Cb);
+        }
+        Dn = fma2(W, pk(r1.w, r1.w), Dn);
+        T = sub2(T, W);
+      }
+      done = __all_sync(0xffffffffu, cut0 == INF && cut1 == INF);
+      if (done && lane == 0) atomicAdd(&sm.ndone, 1u);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[sl]);
+  }
+  float t[2], cr[2], cg[2], cb[2], dn[2];
+  upk(T, t[0], t[1]); upk(Cr, cr[0], cr[1]); upk(Cg, cg[0], cg[1]); upk(Cb, cb[0], cb[1]);
+  upk(Dn, dn[0], dn[1]);
+  const int e = envs[e0 + eloc].out_index;
+  const size_t p0 = ((size_t)e * rp.H + py0) * rp.W + px;
+  if (g.in0) write_pixel(rp, RGB ? rgb : nullptr, depth, alpha_out, p0, t[0], cr[0], cg[0], cb[0], dn[0]);
+  if (g.in1) write_pixel(rp, RGB ? rgb : nullptr, depth, alpha_out, p0 + (size_t)(py1 - py0) * rp.W, t[1], cr[1], cg[1], cb[1], dn[1]);
+}
+
+#ifndef GG_RASTER_PC
+#define GG_RASTER_PC 0   // 1: the producer/consumer raster (A/B switch)
+#endif
+
 void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp, const ChunkWS& ws, void* rgb,
                    float* depth, float* alpha, bool counters, unsigned long long* env_counts, int32_t* dbg_neval,
                    int dbg_eloc, cudaStream_t s) {
@@ -445,6 +604,10 @@ void launch_raster(int e0, int ec, const EnvConst* envs, const RenderParams& rp,
   }
   if (counters)
     raster_kernel<true><<<grid, TILE_PX, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha, co);
+  else if (GG_RASTER_PC && rgb)
+    raster_pc_kernel<true><<<grid, PC_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
+  else if (GG_RASTER_PC)
+    raster_pc_kernel<false><<<grid, PC_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
   else if (rgb)
     raster_warp_kernel<true><<<grid, RW_THREADS, 0, s>>>(e0, envs, rp, ws, rgb, depth, alpha);
   else
