@@ -404,9 +404,10 @@ def main():
     vm_d = t(vm)
     ids = t(ids_np)
     if use_async:
-        # sync-free capacities calibrated by a synchronous render of the first pose set: 1.5x the densest
+        # sync-free capacities calibrated by synchronous renders of the first two pose sets: 1.5x the densest
         # chunk it saw (gg_reserve_async with a negative max_visible_frac)
-        gg.gg_render(R.ctx, E, ids, vm_d[0], intr, W, H, gg.default_opts(flags=tiles_flag), None, None, None)
+        for s_ in range(min(n_sets, 2)):
+            gg.gg_render(R.ctx, E, ids, vm_d[s_], intr, W, H, gg.default_opts(flags=tiles_flag), None, None, None)
         gg.gg_reserve_async(R.ctx, E, W, H, args.chunk, -1.5, 0.0)
     rgb = torch.empty((E, H, W, 3), dtype=torch.uint8, device=dev) if want_rgb else None
     depth = torch.empty((E, H, W), dtype=torch.float32, device=dev) if want_depth else None

@@ -125,8 +125,9 @@ gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t width, int32_t h
  * keys = records * keys_per_visible.  A NEGATIVE max_visible_frac = -h sizes
  * both from what earlier synchronous renders at this width x height saw
  * instead: h times the densest observed chunk's records (keys) per env times
- * the chunk, and at least h times the largest single env; keys_per_visible
- * is then ignored (GG_E_INVALID if no such render happened).  Envs are processed in caller order in
+ * the chunk, and at least h times min(chunk, 4) times the largest single env
+ * seen (records capped at chunk x the largest scene); keys_per_visible is
+ * then ignored (GG_E_INVALID if no such render happened).  Envs are processed in caller order in
  * groups of 16 (sort envs by scene id for best projection efficiency).  On
  * overflow that chunk's frames are background and gg_check_errors returns
  * GG_E_CAPACITY.  Counters (GG_COUNTERS) are supported; intermediates are not. */

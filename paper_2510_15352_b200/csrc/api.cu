@@ -1132,8 +1132,11 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
     if (sc.live) maxdeg = std::max(maxdeg, sc.d.degree);
   uint64_t vcap, kcap;
   if (calibrated) {   // headroom h = -max_visible_frac over the densest observed chunk (and any single env)
-    vcap = (uint64_t)(h * std::max(ch * ctx->cal_vmean, (double)ctx->cal_vmax)) + 1;
-    kcap = (uint64_t)(h * std::max(ch * ctx->cal_kmean, (double)ctx->cal_kmax)) + 1;
+    // small chunks vary most between pose sets: they get room for min(ch, 4)
+    // envs at the largest single env seen; never more than every Gaussian
+    const double few = (double)std::min(ch, 4);
+    vcap = (uint64_t)std::min(h * std::max(ch * ctx->cal_vmean, few * ctx->cal_vmax), (double)ch * nmax) + 1;
+    kcap = (uint64_t)(h * std::max(ch * ctx->cal_kmean, few * ctx->cal_kmax)) + 1;
   } else {
     vcap = (uint64_t)((double)ch * nmax * max_visible_frac) + 1;
     kcap = (uint64_t)((double)vcap * keys_per_visible) + 1;
