@@ -521,7 +521,9 @@ def main():
         h_vm = [pin(vm[k]) for k in range(min(n_sets, 4))]
         h_in = pin(np.tile(gi.pinhole(W, H).astype(np.float32), (E, 1)))
         outs = []
-        for _ in range(2):   # two host frame sets: the pipelined loop alternates them
+        # two host frame sets the pipelined loop alternates (one per rank when several ranks share a host:
+        # 8 ranks x 2 x 8.8 GB of pinned memory would crowd the node)
+        for _ in range(2 if world == 1 else 1):
             outs.append((torch.empty((E, H, W, 3), dtype=torch.uint8, pin_memory=True) if want_rgb else None,
                          torch.empty((E, H, W), dtype=torch.float32, pin_memory=True) if want_depth else None))
         hopts = gg.default_opts(flags=tiles_flag)
@@ -534,7 +536,7 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for k in range(ke):
-                o = outs[k % 2]
+                o = outs[k % len(outs)]
                 if pipelined:   # the RL loop's double-buffered observations: step k+1 renders while k copies out
                     gg.gg_render_host_async(R.ctx, E, h_ids, h_vm[k % len(h_vm)], h_in, W, H, hopts, o[0], o[1],
                                             None, stream)
