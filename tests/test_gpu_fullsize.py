@@ -166,3 +166,34 @@ def test_c5_share_sampled(gg):
     """One GPU's share of c5: 2,500 scenes x 0.5M SH0 (75 GB of scenes), 4,096
     envs (~1.6 envs per scene: env groups of 1-2 envs)."""
     run_workload(gg, gi.Workload("c5", n_envs=4096), flags=gg.GG_TIGHT_TILES, oflags=oracle.F_TIGHT)
+
+
+def test_c3_blur_sampled(gg):
+    """Motion blur at the bench's scale (bench.py --blur 3): 4,096 envs x 3
+    sample cameras through the fused raster average (R32-R34), 4 envs
+    compared with the oracle's blur (three renders and the nominal pose each)."""
+    wl = gi.Workload("c3")
+    E, W, H = wl.n_envs, wl.width, wl.height
+    r = gg.Renderer(0)
+    try:
+        (k, sc), = list(wl.scenes())
+        sid = r.load_scene(dev(sc.means), dev(sc.scales), dev(sc.quats), dev(sc.opacities), dev(sc.sh), sc.sh_degree)
+        g = gi.rng(gi.KIND_CAMERAS, 777)
+        lin = np.float32(g.normal(0.0, 0.5, (E, 3)))
+        ang = np.float32(g.normal(0.0, 1.0, (E, 3)))
+        rgb = torch.empty((E, H, W, 3), dtype=torch.uint8, device="cuda")
+        dep = torch.empty((E, H, W), dtype=torch.float32, device="cuda")
+        gg.gg_render_blur(r.ctx, E, dev(np.full(E, sid, np.int32)), dev(wl.viewmats[0]), dev(wl.intrinsics), dev(lin),
+                          dev(ang), 0.01, 3, W, H, gg.default_opts(flags=gg.GG_TIGHT_TILES), rgb, dep, None)
+        gg.gg_check_errors(r.ctx)
+        torch.cuda.synchronize()
+        osc = oracle.OracleScene.from_inputs(sc)
+        t = Tally()
+        for e in samples(E, 4, 3):
+            o = oracle.render_blur_env(osc, wl.viewmats[0][e], wl.intrinsics[e], W, H, lin[e], ang[e], 0.01, 3,
+                                       flags=oracle.F_TIGHT)
+            t.add(rgb[e].cpu().numpy(), dep[e].cpu().numpy(), None, o)
+        print(t)
+        t.check()
+    finally:
+        r.close()
