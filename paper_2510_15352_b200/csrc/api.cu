@@ -27,11 +27,12 @@ void launch_block_bounds(int n, const float4* pos_op, const float2* aux, float4*
 void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, const float* viewmats,
                        const float* intr, const DevScene* scenes, int nscenes, int W, int H, int sh_degree,
                        EnvConst* out, uint32_t* err, cudaStream_t s);
-void launch_cull_count(int e0, int ngroups, int nblk, const EnvGroup* groups, const EnvConst* envs,
+void launch_cull_count(int e0, int ngroups, int nblk, int bpc, const EnvGroup* groups, const EnvConst* envs,
                        const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
 void launch_scan_blocks(int ec, int nblk, uint32_t* data, uint32_t* totals, cudaStream_t s);
-void launch_project(int e0, int ngroups, int nblk, int max_degree, const EnvGroup* groups, const EnvConst* envs,
-                    const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s);
+void launch_project(int e0, int ngroups, int nblk, int bpc, int max_degree, const EnvGroup* groups,
+                    const EnvConst* envs, const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws,
+                    cudaStream_t s);
 cudaError_t project_init();
 cudaError_t sort_bin_init();
 uint32_t sort_blocks(uint32_t V);
@@ -400,6 +401,16 @@ static int auto_chunk(gg_context* ctx, int E, double per_env_bytes, Work* reusab
 // 16 B, keys ~2.2 x 4 B, order, histograms); the sync path budgets 30% of the
 // largest scene visible per env
 static double sync_env_bytes(const gg_context* ctx) { return (double)std::max(max_scene_n(ctx), 1) * 0.3 * 100.0; }
+
+// Storage blocks per cull/project CTA: 1 when env groups are full (c3: 16
+// envs of one view cell), up to 8 when they are small (c5: ~1.6 envs per
+// scene), so a CTA's camera staging and launch are shared by more work.
+static int blocks_per_cta(int ec, int ngroups) {
+  const double avg = ngroups > 0 ? (double)ec / ngroups : ENV_GROUP;
+  int b = 1;
+  while (b < 8 && avg * b * 2 <= ENV_GROUP) b *= 2;
+  return b;
+}
 
 static gg_status upload_scene_table(gg_context* ctx) {
   const int n = (int)ctx->scenes.size();
@@ -817,7 +828,10 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     const EnvGroup* groups = P<EnvGroup>(ctx->sw.groups);
     TREC(0);
     // K1a + K2
-    launch_cull_count(e0, ngroups, nblk, groups, P<EnvConst>(ctx->sw.envc), P<DevScene>(ctx->scene_table), rp, ws, s);
+    // storage blocks per CTA: small env groups share a CTA's setup over several blocks
+    const int bpc = blocks_per_cta(ec, ngroups);
+    launch_cull_count(e0, ngroups, nblk, bpc, groups, P<EnvConst>(ctx->sw.envc), P<DevScene>(ctx->scene_table), rp, ws,
+                      s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
     ctx->launches += 2;
     CK(cudaGetLastError());
@@ -852,7 +866,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     ws.dconic = keep ? P<float4>(ctx->sw.dconic) : nullptr;
     ws.dp0 = P<uint64_t>(ctx->sw.dk0); ws.dp1 = P<uint64_t>(ctx->sw.dk1); ws.order = P<uint32_t>(ctx->sw.dv0);
     // K1b
-    launch_project(e0, ngroups, nblk, max_deg, groups, P<EnvConst>(ctx->sw.envc), P<DevScene>(ctx->scene_table), rp,
+    launch_project(e0, ngroups, nblk, bpc, max_deg, groups, P<EnvConst>(ctx->sw.envc), P<DevScene>(ctx->scene_table), rp,
                    ws, s);
     ctx->launches++;
     CK(cudaGetLastError());
@@ -1076,11 +1090,12 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     TREC(0);
     CK(cudaMemsetAsync(ws.kcnt, 0, ec * 8, s));
     CK(cudaMemsetAsync(ok, 0x01, 4, s));
-    launch_cull_count(e0, ngroups, nblk, nullptr, P<EnvConst>(ctx->aw.envc), P<DevScene>(ctx->scene_table), rp, ws, s);
+    launch_cull_count(e0, ngroups, nblk, 1, nullptr, P<EnvConst>(ctx->aw.envc), P<DevScene>(ctx->scene_table), rp,
+                      ws, s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
     launch_tables_v(ec, ws.vcnt, P<uint64_t>(ctx->aw.rbase), ctx->a_vcap, ok, err, s);
     TREC(1);
-    launch_project(e0, ngroups, nblk, ctx->a_maxdeg, nullptr, P<EnvConst>(ctx->aw.envc), P<DevScene>(ctx->scene_table),
+    launch_project(e0, ngroups, nblk, 1, ctx->a_maxdeg, nullptr, P<EnvConst>(ctx->aw.envc), P<DevScene>(ctx->scene_table),
                    rp, ws, s);
     launch_tables_k(ec, ws.vcnt, ws.kcnt, P<uint64_t>(ctx->aw.kbase), P<uint32_t>(ctx->aw.blkbase), sort_block_size(),
                     ctx->a_kcap, ctx->a_nbcap, ok, err, s);

@@ -180,66 +180,75 @@ __device__ __forceinline__ bool block_may_see(const EnvConst& c, float4 b0, floa
   return true;
 }
 
-__global__ void __launch_bounds__(PROJ_BLOCK)
+// A CTA handles `bpc` consecutive storage blocks of its env group (bpc > 1
+// when groups are small, e.g. ~1.6 envs per scene in c5: the camera staging
+// and launch cost per CTA is then shared by several blocks).
+template <bool MULTI>   // false: one storage block per CTA (bpc = 1, full env groups)
+__global__ void __launch_bounds__(PROJ_BLOCK, 6)
 cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
-                  const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
+                  const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws, int bpc) {
   __shared__ EnvConst cams[ENV_GROUP];
   __shared__ uint32_t wc[ENV_GROUP][PROJ_BLOCK / 32];
   __shared__ uint32_t bvis;   // bit k: env k may see some Gaussian of this storage block
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0) return;
   load_group_cams(cams, envs, e0, grp);
-  if (threadIdx.x == 0) bvis = 0u;
-  __syncthreads();
-  if (threadIdx.x < grp.cnt) {
-    const EnvConst c = load_cam(&cams[threadIdx.x]);
-    if (c.n > (int)(blockIdx.y * PROJ_BLOCK)) {
-      const DevScene& sc = scenes[c.scene];
-      if (block_may_see(c, __ldg(&sc.bbox[2 * blockIdx.y]), __ldg(&sc.bbox[2 * blockIdx.y + 1]), rp))
-        atomicOr(&bvis, 1u << threadIdx.x);
-    }
-  }
-  __syncthreads();
-  const uint32_t bv = bvis;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (bv == 0u) {   // the whole block is outside every camera of the group
-    if (lane < grp.cnt) ws.flags[(size_t)(grp.elo + lane) * ws.nwords + blockIdx.y * (PROJ_BLOCK / 32) + warp] = 0u;
-    if (threadIdx.x < grp.cnt) ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blockIdx.y] = 0u;
-    return;
-  }
-  const int i = blockIdx.y * PROJ_BLOCK + threadIdx.x;
-  int cur = -2;                       // scene whose Gaussian i is in registers
-  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-  float smax2 = 0.f;
-  const int wi = blockIdx.y * (PROJ_BLOCK / 32) + warp;
-  // lane k keeps env k's visibility word (no per-env branch in the loop;
-  // ENV_GROUP <= 32)
-  uint32_t my_word = 0u;
-  for (uint32_t bm = bv; bm; bm &= bm - 1u) {   // only the envs whose block test passed (CTA-uniform)
-    const int k = __ffs(bm) - 1;
-    const EnvConst c = load_cam(&cams[k]);
-    if (c.scene != cur) {             // uniform across the CTA
-      cur = c.scene;
-      if (i < c.n) {
+  const int b0 = MULTI ? blockIdx.y * bpc : blockIdx.y;
+  const int b1 = MULTI ? min(ws.nblk, (int)(blockIdx.y + 1) * bpc) : b0 + 1;
+  for (int blk = b0; blk < b1; ++blk) {
+    __syncthreads();            // cameras staged; the previous block's wc fully read
+    if (threadIdx.x == 0) bvis = 0u;
+    __syncthreads();
+    if (threadIdx.x < grp.cnt) {
+      const EnvConst c = load_cam(&cams[threadIdx.x]);
+      if (c.n > blk * PROJ_BLOCK) {
         const DevScene& sc = scenes[c.scene];
-        g = __ldg(&sc.pos_op[i]);
-        smax2 = __ldg(&sc.aux[i]).y;
+        if (block_may_see(c, __ldg(&sc.bbox[2 * blk]), __ldg(&sc.bbox[2 * blk + 1]), rp))
+          atomicOr(&bvis, 1u << threadIdx.x);
       }
     }
-    const bool keep = i < c.n && maybe_visible(c, g, smax2, rp);
-    const uint32_t word = __ballot_sync(0xffffffffu, keep);
-    if (lane == k) my_word = word;
-  }
-  if (lane < grp.cnt) {
-    ws.flags[(size_t)(grp.elo + lane) * ws.nwords + wi] = my_word;
-    wc[lane][warp] = __popc(my_word);
-  }
-  __syncthreads();
-  if (threadIdx.x < grp.cnt) {
-    uint32_t s = 0;
+    __syncthreads();
+    const uint32_t bv = bvis;
+    if (bv == 0u) {   // the whole block is outside every camera of the group
+      if (lane < grp.cnt) ws.flags[(size_t)(grp.elo + lane) * ws.nwords + blk * (PROJ_BLOCK / 32) + warp] = 0u;
+      if (threadIdx.x < grp.cnt) ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blk] = 0u;
+      continue;
+    }
+    const int i = blk * PROJ_BLOCK + threadIdx.x;
+    int cur = -2;                       // scene whose Gaussian i is in registers
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    float smax2 = 0.f;
+    const int wi = blk * (PROJ_BLOCK / 32) + warp;
+    // lane k keeps env k's visibility word (no per-env branch in the loop;
+    // ENV_GROUP <= 32)
+    uint32_t my_word = 0u;
+    for (uint32_t bm = bv; bm; bm &= bm - 1u) {   // only the envs whose block test passed (CTA-uniform)
+      const int k = __ffs(bm) - 1;
+      const EnvConst c = load_cam(&cams[k]);
+      if (c.scene != cur) {             // uniform across the CTA
+        cur = c.scene;
+        if (i < c.n) {
+          const DevScene& sc = scenes[c.scene];
+          g = __ldg(&sc.pos_op[i]);
+          smax2 = __ldg(&sc.aux[i]).y;
+        }
+      }
+      const bool keep = i < c.n && maybe_visible(c, g, smax2, rp);
+      const uint32_t word = __ballot_sync(0xffffffffu, keep);
+      if (lane == k) my_word = word;
+    }
+    if (lane < grp.cnt) {
+      ws.flags[(size_t)(grp.elo + lane) * ws.nwords + wi] = my_word;
+      wc[lane][warp] = __popc(my_word);
+    }
+    __syncthreads();
+    if (threadIdx.x < grp.cnt) {
+      uint32_t s = 0;
 #pragma unroll
-    for (int w = 0; w < PROJ_BLOCK / 32; ++w) s += wc[threadIdx.x][w];
-    ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blockIdx.y] = s;
+      for (int w = 0; w < PROJ_BLOCK / 32; ++w) s += wc[threadIdx.x][w];
+      ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blk] = s;
+    }
   }
 }
 
@@ -421,23 +430,27 @@ struct ProjSmem {
 // block word by word (all envs of word w before word w + 1), so the 32
 // Gaussians being projected stay in L1.  With the Morton storage order a
 // non-empty word is ~90% full (visibility is spatially coherent).
-template <bool ELL>   // GG_ELLIPSE_TILES (reading R37): per-record tile masks
+template <bool ELL, bool MULTI>   // GG_ELLIPSE_TILES (reading R37): per-record tile masks; bpc > 1
 #ifndef GG_PROJ_MINB
 #define GG_PROJ_MINB (1024 / PROJ_BLOCK)   // 4 CTAs x 256 threads at <= 64 registers
 #endif
 __global__ void __launch_bounds__(PROJ_BLOCK, GG_PROJ_MINB)
 project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
-               const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws) {
+               const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws, int bpc) {
   __shared__ ProjSmem sm;
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0 || !chunk_ok(ws.ok)) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gblk = blockIdx.y;
-  const int i0 = gblk * PROJ_BLOCK;
   {
     const CamWord* src = reinterpret_cast<const CamWord*>(envs + e0 + grp.elo);
     for (int i = threadIdx.x; i < grp.cnt * CAM_F2; i += blockDim.x) sm.camT[i % CAM_F2][i / CAM_F2] = src[i];
   }
+  if (tid < ENV_GROUP) sm.kacc[tid] = 0;
+  const int gblk0 = MULTI ? blockIdx.y * bpc : blockIdx.y;
+  const int gblk1 = MULTI ? min(ws.nblk, (int)(blockIdx.y + 1) * bpc) : gblk0 + 1;
+  for (int gblk = gblk0; gblk < gblk1; ++gblk) {   // bpc storage blocks per CTA (cull_count_kernel)
+  const int i0 = gblk * PROJ_BLOCK;
+  __syncthreads();   // cameras staged; the previous block's units all processed
   for (int q = tid; q < ENV_GROUP * PROJ_WPB; q += PROJ_BLOCK) {
     const int k = q / PROJ_WPB, w = q % PROJ_WPB;
     uint32_t word = 0;
@@ -445,7 +458,6 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     sm.fw[q] = word;
     sm.cnt[q] = __popc(word);
   }
-  if (tid < ENV_GROUP) sm.kacc[tid] = 0;
   __syncthreads();
   if (tid < ENV_GROUP) {   // per env: exclusive prefix of its word counts
     uint32_t run = 0;
@@ -599,6 +611,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     for (int o = 16; o > 0; o >>= 1) ntiles += __shfl_xor_sync(0xffffffffu, ntiles, o);
     if (lane == 0 && ntiles) atomicAdd(&sm.kacc[k], ntiles);
   }
+  }   // storage blocks of this CTA
   __syncthreads();
   if (tid < grp.cnt && sm.kacc[tid]) atomicAdd(&ws.kcnt[grp.elo + tid], (unsigned long long)sm.kacc[tid]);
 }
@@ -612,21 +625,29 @@ void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, con
                                                     sh_degree, out, err);
 }
 
-void launch_cull_count(int e0, int ngroups, int nblk, const EnvGroup* groups, const EnvConst* envs,
+void launch_cull_count(int e0, int ngroups, int nblk, int bpc, const EnvGroup* groups, const EnvConst* envs,
                        const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
-  cull_count_kernel<<<dim3(ngroups, nblk), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws);
+  if (bpc > 1)
+    cull_count_kernel<true><<<dim3(ngroups, (nblk + bpc - 1) / bpc), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp,
+                                                                                       ws, bpc);
+  else
+    cull_count_kernel<false><<<dim3(ngroups, nblk), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws, 1);
 }
 
 void launch_scan_blocks(int ec, int nblk, uint32_t* data, uint32_t* totals, cudaStream_t s) {
   scan_blocks_kernel<<<ec, 1024, 0, s>>>(data, nblk, totals);
 }
 
-void launch_project(int e0, int ngroups, int nblk, int max_degree, const EnvGroup* groups, const EnvConst* envs,
-                    const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
+void launch_project(int e0, int ngroups, int nblk, int bpc, int max_degree, const EnvGroup* groups,
+                    const EnvConst* envs, const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws,
+                    cudaStream_t s) {
+  const dim3 grid(ngroups, (nblk + bpc - 1) / bpc);
   if (rp.ellipse)
-    project_kernel<true><<<dim3(ngroups, nblk), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws);
+    bpc > 1 ? project_kernel<true, true><<<grid, PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws, bpc)
+            : project_kernel<true, false><<<grid, PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws, 1);
   else
-    project_kernel<false><<<dim3(ngroups, nblk), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws);
+    bpc > 1 ? project_kernel<false, true><<<grid, PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws, bpc)
+            : project_kernel<false, false><<<grid, PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp, ws, 1);
 }
 
 }  // namespace gg
