@@ -43,6 +43,9 @@ constexpr int PD_THREADS = GG_PD_THREADS;        // placement downsweep: 16 warp
 constexpr int PD_MINB = 1536 / PD_THREADS;       // resident CTAs per SM the smem budget below allows
 constexpr int PD_SMEM = 216 * 1024 / PD_MINB;    // shared-memory budget per CTA
 constexpr int PD_WARPS = PD_THREADS / 32;
+#ifndef GG_PD_OWNER
+#define GG_PD_OWNER 1   // pair owners from a window bitmask (0: the shuffle binary search, 0.6 ms slower per c3 step)
+#endif
 #ifndef GG_SORT_BLK
 #define GG_SORT_BLK 6144   // measured: sort stage 56.4 (4096), 54.9 (5120), 53.4 (6144), 53.7 (7168), 59.9 (8192) ms per c3 step
 #endif
@@ -625,6 +628,10 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
   uint8_t* st = stamps + (size_t)warp * nt;
   uint32_t* pm = pmask + warp * 32;
   const uint32_t lt = lanemask_lt();
+#if GG_PD_OWNER
+  __shared__ uint8_t own_s[PD_WARPS][32];
+  uint8_t* own = own_s[warp];
+#endif
   for (uint32_t base = s0; base < s1; base += 32) {
     const uint32_t j = base + lane;
     uint32_t idx = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
@@ -646,15 +653,31 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
     const uint32_t excl = incl - np;
     const uint32_t xy0 = x0 | (y0 << 16);
+#if GG_PD_OWNER
+    int carry = 0;   // lane owning the first pair of the next window
+#endif
     for (uint32_t f0 = 0; f0 < tot; f0 += 32) {
       const uint32_t f = f0 + lane;
       const bool ok = f < tot;
+#if GG_PD_OWNER
+      // lanes whose first pair falls in this window mark its position; pair f
+      // belongs to the last mark at or before it, else to the carried owner
+      const bool starts = np > 0 && excl >= f0 && excl < f0 + 32;
+      const uint32_t M = __reduce_or_sync(0xffffffffu, starts ? 1u << (excl - f0) : 0u);
+      if (starts) own[excl - f0] = (uint8_t)lane;
+      __syncwarp();
+      const uint32_t mm = M & ((2u << lane) - 1u);
+      int src = mm ? (int)own[31 - __clz(mm)] : carry;
+      __syncwarp();
+      carry = __shfl_sync(0xffffffffu, src, 31);
+#else
       int src = 0;   // first lane whose inclusive pair count exceeds f
 #pragma unroll
       for (int step = 16; step > 0; step >>= 1) {
         const uint32_t v = __shfl_sync(0xffffffffu, incl, src + step - 1);
         if (v <= f) src += step;
       }
+#endif
       const uint32_t o_ex = __shfl_sync(0xffffffffu, excl, src);
       const uint32_t o_w = __shfl_sync(0xffffffffu, w, src);
       const uint32_t o_xy = __shfl_sync(0xffffffffu, xy0, src);
