@@ -320,8 +320,16 @@ def run_reference(args):
     if rank != 0:
         return 0
     c, name = workload(args)
-    scene = gi.config_scene(args.config, n_gauss=c["n_gauss"], sh_degree=c["sh_degree"])
-    cams = gi.cameras(0, max(1, args.steps + args.warmup), c["width"], c["height"], scene)
+    # the first envs of the bench's own global workload (scene 0's, for multi-scene configs)
+    wl = gi.Workload(args.config, n_envs=c["n_envs"], n_sets=1, n_scenes=c["n_scenes"], n_gauss=c["n_gauss"],
+                     sh_degree=c["sh_degree"])
+    k0 = int(wl.binding[0])
+    scene = wl.scene(k0)
+    envs0 = np.flatnonzero(wl.binding == k0)
+    wl.place(k0, scene.free_boxes, scene.half_extent)
+    need = max(1, args.steps + args.warmup)
+    sel = np.resize(envs0, need)
+    cams = gi.Cameras(wl.viewmats[0][sel], wl.intrinsics[sel], c["width"], c["height"])
     import oracle
     oracle.use_all_cores()
     osc = oracle.OracleScene.from_inputs(scene)
