@@ -54,13 +54,27 @@ def launches():
     return agg, tot, len(rs)
 
 
+def _raw(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    return list(csv.reader(out.splitlines()))
+
+
 def full(kernel):
     path = os.path.join(SRC, f"full_{kernel}.ncu-rep")
-    if not os.path.exists(path):
-        return None
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
-    h, u, v = rows[0], rows[1], rows[2]
+    if os.path.exists(path):
+        rows = _raw(path)
+        h, u, v = rows[0], rows[1], rows[2]
+    else:   # one multi-kernel capture (tools/profile_round.sh <round> full): first launch of that kernel
+        allp = os.path.join(SRC, "full_all.ncu-rep")
+        if not os.path.exists(allp):
+            return None
+        rows = _raw(allp)
+        h, u = rows[0], rows[1]
+        ki = h.index("Kernel Name")
+        hit = [r for r in rows[2:] if kernel in r[ki]]
+        if not hit:
+            return None
+        v = hit[0]
     res = {"kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else kernel}
     for m in METRICS:
         if m in h:
@@ -90,8 +104,8 @@ summary = {"round": R, "step_kernel_seconds": tot, "per_kernel_step": agg, "full
            "capture_envs_per_launch": 512,
            "notes": "launch list: ncu --metrics gpu__time_duration.sum --clock-control none of "
                     "`bench.py --steps 2 --warmup 3 --no-e2e --no-cpu` (cold-cache, serialised: compare shares); "
-                    "full captures: ncu --set full on one steady-state launch of each kernel of "
-                    "`bench.py --envs 512` (one launch = 512 envs; the default bench launch covers 1024)."}
+                    "full captures: ncu --set full (caches flushed per kernel) on the first launch of each kernel "
+                    "of `bench.py --envs 512` (one launch = 512 envs; the default bench launch covers 1024)."}
 json.dump(summary, open(os.path.join(DST, "ncu_summary.json"), "w"), indent=1)
 with open(os.path.join(DST, "ncu_summary.md"), "w") as f:
     f.write(f"# ncu summary — {R}\n\nLaunch list (last gg_render of the bench run = one step, {nl} launches "

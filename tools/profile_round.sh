@@ -7,14 +7,18 @@
 # into profiles/<round>/.
 set -e
 R=${1:-r01}
+MODE=${2:-launches}   # launches | full  (one ncu tool per gpurun call: run the two modes as two calls)
 O=gpurun_out/prof_$R
 mkdir -p $O
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu"
-$CMD > $O/bench_plain.json 2> $O/bench_plain.err
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > /dev/null 2>&1
 SMALL="python bench.py --envs 512 --steps 1 --warmup 3 --no-e2e --no-cpu"
-$SMALL > $O/small_plain.json 2>&1
-for k in raster_warp_kernel project_kernel cull_count_kernel depth_downsweep place_downsweep depth_upsweep place_upsweep depth_ties depth_scan place_scan; do
-  ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o $O/full_$k $SMALL > $O/ncu_$k.log 2>&1 || echo "ncu $k failed"
-done
+if [ "$MODE" = launches ]; then
+  $CMD > $O/bench_plain.json 2> $O/bench_plain.err
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > /dev/null 2>&1
+else
+  $SMALL > $O/small_plain.json 2>&1
+  # one ncu invocation: the first launch of each hot kernel (+ the 3 depth passes) of the first render
+  K='regex:raster_warp_kernel|project_kernel|cull_count_kernel|depth_downsweep|place_downsweep|depth_upsweep|place_upsweep|depth_ties|depth_scan|place_scan'
+  ncu --set full --clock-control none --import-source on -k "$K" -c 14 -o $O/full_all $SMALL > $O/ncu_full.log 2>&1 || echo "ncu failed"
+fi
 ls -la $O
