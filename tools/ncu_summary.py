@@ -42,7 +42,7 @@ def launches():
     agg = OrderedDict()
     for r in last:
         name = r[ki].split("(")[0].replace("void ", "").strip()
-        if not name.startswith("gg::"):
+        if not name.startswith("gg::") or "checksum" in name:   # the digest runs after the timed region
             continue
         v = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1e-9)
         a = agg.setdefault(name, {"launches": 0, "seconds": 0.0})
@@ -74,7 +74,7 @@ def full(kernel):
         hit = [r for r in rows[2:] if kernel in r[ki]]
         if not hit:
             return None
-        v = hit[0]
+        v = hit[-1]   # the last capture: the bench's own render configuration (not a counters pass)
     res = {"kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else kernel}
     for m in METRICS:
         if m in h:
@@ -104,7 +104,7 @@ summary = {"round": R, "step_kernel_seconds": tot, "per_kernel_step": agg, "full
            "capture_envs_per_launch": 512,
            "notes": "launch list: ncu --metrics gpu__time_duration.sum --clock-control none of "
                     "`bench.py --steps 2 --warmup 3 --no-e2e --no-cpu` (cold-cache, serialised: compare shares); "
-                    "full captures: ncu --set full (caches flushed per kernel) on the first launch of each kernel "
+                    "full captures: ncu --set full (caches flushed per kernel) on the last captured launch of each kernel "
                     "of `bench.py --envs 512` (one launch = 512 envs; the default bench launch covers 1024)."}
 json.dump(summary, open(os.path.join(DST, "ncu_summary.json"), "w"), indent=1)
 with open(os.path.join(DST, "ncu_summary.md"), "w") as f:
