@@ -607,8 +607,7 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
     if (ws.dconic) ws.dconic[r] = make_float4(cA, cB, cC, exp2f(L));
     }
     // the unit's tile keys -> its env's key count (one shared atomic per unit)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ntiles += __shfl_xor_sync(0xffffffffu, ntiles, o);
+    ntiles = __reduce_add_sync(0xffffffffu, ntiles);   // REDUX.SUM: one instruction for the warp total
     if (lane == 0 && ntiles) atomicAdd(&sm.kacc[k], ntiles);
   }
   }   // storage blocks of this CTA

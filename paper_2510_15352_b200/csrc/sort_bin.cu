@@ -689,8 +689,12 @@ __device__ __forceinline__ void place_downsweep_block(uint32_t b, const BlockTab
         // else the qq-th tile of the rect (row-major)
         uint32_t qq = f - o_ex;
         if (o_msk != 0xffffffffu) qq = __fns(o_msk, 0u, (int)qq + 1);
-        // qq / o_w for small integers via the f32 reciprocal (exact: qq < 2^20, o_w < 2^16)
-        const uint32_t row = (uint32_t)__fdividef((float)qq + 0.5f, (float)o_w);
+        // qq / o_w for small integers via the approximate f32 reciprocal: (qq + 0.5) / o_w lies
+        // >= 0.5 / o_w from an integer and rcp.approx + the product err by <= (qq + 0.5) 2^-22 / o_w,
+        // so the truncation is exact for qq < 2^21 (qq < MAX_TILES here)
+        float rw;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rw) : "f"((float)o_w));
+        const uint32_t row = (uint32_t)(((float)qq + 0.5f) * rw);
         t = ((o_xy >> 16) + row) * rp.TX + (o_xy & 0xffffu) + (qq - row * o_w);
       }
       uint32_t peers;

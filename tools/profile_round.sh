@@ -17,8 +17,8 @@ if [ "$MODE" = launches ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > /dev/null 2>&1
 else
   $SMALL > $O/small_plain.json 2>&1
-  # one ncu invocation: the first launch of each hot kernel (the first three renders: the first two are the counters passes, whose raster is raster_kernel<COUNTERS>)
+  # one ncu invocation: the first launch of each hot kernel (the third render: the first two are the counters passes, 15 matching launches each, whose raster is raster_kernel<COUNTERS>)
   K='regex:raster_warp_kernel|project_kernel|cull_count_kernel|depth_downsweep|place_downsweep|depth_upsweep|place_upsweep|depth_ties|depth_scan|place_scan'
-  ncu --set full --clock-control none --import-source on -k "$K" -c 48 -o $O/full_all $SMALL > $O/ncu_full.log 2>&1 || echo "ncu failed"
+  ncu --set full --clock-control none --import-source on -k "$K" --launch-skip 30 -c 16 -o $O/full_all $SMALL > $O/ncu_full.log 2>&1 || echo "ncu failed"
 fi
 ls -la $O
