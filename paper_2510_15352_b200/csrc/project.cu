@@ -184,7 +184,10 @@ __device__ __forceinline__ bool block_may_see(const EnvConst& c, float4 b0, floa
 // when groups are small, e.g. ~1.6 envs per scene in c5: the camera staging
 // and launch cost per CTA is then shared by several blocks).
 template <bool MULTI>   // false: one storage block per CTA (bpc = 1, full env groups)
-__global__ void __launch_bounds__(PROJ_BLOCK, 6)
+#ifndef GG_CULL_MINB
+#define GG_CULL_MINB 6   // 40 registers; measured: 5 (48 registers) 5.08 vs 4.69 ms per c3 step
+#endif
+__global__ void __launch_bounds__(PROJ_BLOCK, GG_CULL_MINB)
 cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
                   const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws, int bpc) {
   __shared__ EnvConst cams[ENV_GROUP];
@@ -192,10 +195,10 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
   __shared__ uint32_t bvis;   // bit k: env k may see some Gaussian of this storage block
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0) return;
-  load_group_cams(cams, envs, e0, grp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b0 = MULTI ? blockIdx.y * bpc : blockIdx.y;
   const int b1 = MULTI ? min(ws.nblk, (int)(blockIdx.y + 1) * bpc) : b0 + 1;
+  load_group_cams(cams, envs, e0, grp);
   for (int blk = b0; blk < b1; ++blk) {
     __syncthreads();            // cameras staged; the previous block's wc fully read
     if (threadIdx.x == 0) bvis = 0u;
@@ -441,22 +444,28 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0 || !chunk_ok(ws.ok)) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gblk0 = MULTI ? blockIdx.y * bpc : blockIdx.y;
+  const int gblk1 = MULTI ? min(ws.nblk, (int)(blockIdx.y + 1) * bpc) : gblk0 + 1;
+  // the first block's visibility words are loaded before the camera staging
+  // (their latencies overlap instead of adding up across the first barrier)
+  static_assert(ENV_GROUP * PROJ_WPB <= PROJ_BLOCK, "one visibility word per thread");
+  uint32_t wpre = 0;
+  if (tid < ENV_GROUP * PROJ_WPB && tid / PROJ_WPB < grp.cnt)
+    wpre = ws.flags[(size_t)(grp.elo + tid / PROJ_WPB) * ws.nwords + gblk0 * PROJ_WPB + tid % PROJ_WPB];
   {
     const CamWord* src = reinterpret_cast<const CamWord*>(envs + e0 + grp.elo);
     for (int i = threadIdx.x; i < grp.cnt * CAM_F2; i += blockDim.x) sm.camT[i % CAM_F2][i / CAM_F2] = src[i];
   }
   if (tid < ENV_GROUP) sm.kacc[tid] = 0;
-  const int gblk0 = MULTI ? blockIdx.y * bpc : blockIdx.y;
-  const int gblk1 = MULTI ? min(ws.nblk, (int)(blockIdx.y + 1) * bpc) : gblk0 + 1;
   for (int gblk = gblk0; gblk < gblk1; ++gblk) {   // bpc storage blocks per CTA (cull_count_kernel)
   const int i0 = gblk * PROJ_BLOCK;
   __syncthreads();   // cameras staged; the previous block's units all processed
-  for (int q = tid; q < ENV_GROUP * PROJ_WPB; q += PROJ_BLOCK) {
-    const int k = q / PROJ_WPB, w = q % PROJ_WPB;
-    uint32_t word = 0;
-    if (k < grp.cnt) word = ws.flags[(size_t)(grp.elo + k) * ws.nwords + gblk * PROJ_WPB + w];
-    sm.fw[q] = word;
-    sm.cnt[q] = __popc(word);
+  if (tid < ENV_GROUP * PROJ_WPB) {
+    const int k = tid / PROJ_WPB, w = tid % PROJ_WPB;
+    uint32_t word = wpre;
+    if (gblk != gblk0 && k < grp.cnt) word = ws.flags[(size_t)(grp.elo + k) * ws.nwords + gblk * PROJ_WPB + w];
+    sm.fw[tid] = word;
+    sm.cnt[tid] = __popc(word);
   }
   __syncthreads();
   if (tid < ENV_GROUP) {   // per env: exclusive prefix of its word counts
