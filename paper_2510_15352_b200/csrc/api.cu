@@ -412,6 +412,17 @@ static int blocks_per_cta(int ec, int ngroups) {
   return b;
 }
 
+// storage blocks per cull CTA: up to 16 (the CTA's block tests then run in
+// one step and its camera staging is shared; measured at c3: 1 -> 4.64, 4 ->
+// 4.11, 8 -> 3.98, 16 -> 3.96 ms), as long as the grid keeps >= 12 CTAs per SM
+static int cull_blocks_per_cta(int ngroups, int nblk, int bpc) {
+  static const int env = getenv("GG_CULL_BPC") ? atoi(getenv("GG_CULL_BPC")) : 0;   // A/B switch
+  if (env > 0) return env;
+  int b = 16;
+  while (b > bpc && (long long)ngroups * ((nblk + b - 1) / b) < 148LL * 12) b /= 2;
+  return std::max(b, bpc);
+}
+
 static gg_status upload_scene_table(gg_context* ctx) {
   const int n = (int)ctx->scenes.size();
   std::vector<DevScene> h(n);
@@ -830,7 +841,7 @@ static gg_status render_impl(gg_context* ctx, int32_t E, const int32_t* scene_id
     // K1a + K2
     // storage blocks per CTA: small env groups share a CTA's setup over several blocks
     const int bpc = blocks_per_cta(ec, ngroups);
-    launch_cull_count(e0, ngroups, nblk, bpc, groups, P<EnvConst>(ctx->sw.envc), P<DevScene>(ctx->scene_table), rp, ws,
+    launch_cull_count(e0, ngroups, nblk, cull_blocks_per_cta(ngroups, nblk, bpc), groups, P<EnvConst>(ctx->sw.envc), P<DevScene>(ctx->scene_table), rp, ws,
                       s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
     ctx->launches += 2;
@@ -1090,8 +1101,8 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     TREC(0);
     CK(cudaMemsetAsync(ws.kcnt, 0, ec * 8, s));
     CK(cudaMemsetAsync(ok, 0x01, 4, s));
-    launch_cull_count(e0, ngroups, nblk, 1, nullptr, P<EnvConst>(ctx->aw.envc), P<DevScene>(ctx->scene_table), rp,
-                      ws, s);
+    launch_cull_count(e0, ngroups, nblk, cull_blocks_per_cta(ngroups, nblk, 1), nullptr, P<EnvConst>(ctx->aw.envc),
+                      P<DevScene>(ctx->scene_table), rp, ws, s);
     launch_scan_blocks(ec, nblk, ws.blkcnt, ws.vcnt, s);
     launch_tables_v(ec, ws.vcnt, P<uint64_t>(ctx->aw.rbase), ctx->a_vcap, ok, err, s);
     TREC(1);

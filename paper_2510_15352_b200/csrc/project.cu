@@ -183,6 +183,7 @@ __device__ __forceinline__ bool block_may_see(const EnvConst& c, float4 b0, floa
 // A CTA handles `bpc` consecutive storage blocks of its env group (bpc > 1
 // when groups are small, e.g. ~1.6 envs per scene in c5: the camera staging
 // and launch cost per CTA is then shared by several blocks).
+constexpr int CULL_BPC_MAX = PROJ_BLOCK / ENV_GROUP;   // storage blocks per cull CTA (one test thread per env and block)
 template <bool MULTI>   // false: one storage block per CTA (bpc = 1, full env groups)
 #ifndef GG_CULL_MINB
 #define GG_CULL_MINB 6   // 40 registers; measured: 5 (48 registers) 5.08 vs 4.69 ms per c3 step
@@ -191,29 +192,37 @@ __global__ void __launch_bounds__(PROJ_BLOCK, GG_CULL_MINB)
 cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __restrict__ envs,
                   const DevScene* __restrict__ scenes, RenderParams rp, ChunkWS ws, int bpc) {
   __shared__ EnvConst cams[ENV_GROUP];
-  __shared__ uint32_t wc[ENV_GROUP][PROJ_BLOCK / 32];
-  __shared__ uint32_t bvis;   // bit k: env k may see some Gaussian of this storage block
+  __shared__ uint32_t wc[2][ENV_GROUP][PROJ_BLOCK / 32];   // double-buffered per processed block
+  __shared__ uint32_t bvis[CULL_BPC_MAX];   // bit k: env k may see some Gaussian of block b0 + j
   const EnvGroup grp = group_of(groups, blockIdx.x, ws.ec);
   if (grp.cnt <= 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b0 = MULTI ? blockIdx.y * bpc : blockIdx.y;
   const int b1 = MULTI ? min(ws.nblk, (int)(blockIdx.y + 1) * bpc) : b0 + 1;
+  const int nb = b1 - b0;                     // <= CULL_BPC_MAX (launch_cull_count)
   load_group_cams(cams, envs, e0, grp);
-  for (int blk = b0; blk < b1; ++blk) {
-    __syncthreads();            // cameras staged; the previous block's wc fully read
-    if (threadIdx.x == 0) bvis = 0u;
-    __syncthreads();
-    if (threadIdx.x < grp.cnt) {
-      const EnvConst c = load_cam(&cams[threadIdx.x]);
+  if (threadIdx.x < CULL_BPC_MAX) bvis[threadIdx.x] = 0u;
+  __syncthreads();
+  // the block tests of all the CTA's storage blocks at once: thread j * 16 + k
+  // tests env k against block b0 + j (one barrier for the whole CTA)
+  {
+    const int j = threadIdx.x / ENV_GROUP, k = threadIdx.x % ENV_GROUP;
+    if (j < nb && k < grp.cnt) {
+      const EnvConst c = load_cam(&cams[k]);
+      const int blk = b0 + j;
       if (c.n > blk * PROJ_BLOCK) {
         const DevScene& sc = scenes[c.scene];
         if (block_may_see(c, __ldg(&sc.bbox[2 * blk]), __ldg(&sc.bbox[2 * blk + 1]), rp))
-          atomicOr(&bvis, 1u << threadIdx.x);
+          atomicOr(&bvis[j], 1u << k);
       }
     }
-    __syncthreads();
-    const uint32_t bv = bvis;
-    if (bv == 0u) {   // the whole block is outside every camera of the group
+  }
+  __syncthreads();
+  int nproc = 0;   // processed (not skipped) blocks: selects the wc buffer
+  for (int j = 0; j < nb; ++j) {
+    const int blk = b0 + j;
+    const uint32_t bv = bvis[j];
+    if (bv == 0u) {   // the whole block is outside every camera of the group (CTA-uniform)
       if (lane < grp.cnt) ws.flags[(size_t)(grp.elo + lane) * ws.nwords + blk * (PROJ_BLOCK / 32) + warp] = 0u;
       if (threadIdx.x < grp.cnt) ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blk] = 0u;
       continue;
@@ -241,15 +250,19 @@ cull_count_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* _
       const uint32_t word = __ballot_sync(0xffffffffu, keep);
       if (lane == k) my_word = word;
     }
+    // two processed blocks that use the same wc buffer are separated by the
+    // barrier of the processed block between them
+    uint32_t (*w)[PROJ_BLOCK / 32] = wc[nproc & 1];
+    ++nproc;
     if (lane < grp.cnt) {
       ws.flags[(size_t)(grp.elo + lane) * ws.nwords + wi] = my_word;
-      wc[lane][warp] = __popc(my_word);
+      w[lane][warp] = __popc(my_word);
     }
     __syncthreads();
     if (threadIdx.x < grp.cnt) {
       uint32_t s = 0;
 #pragma unroll
-      for (int w = 0; w < PROJ_BLOCK / 32; ++w) s += wc[threadIdx.x][w];
+      for (int q = 0; q < PROJ_BLOCK / 32; ++q) s += w[threadIdx.x][q];
       ws.blkcnt[(size_t)(grp.elo + threadIdx.x) * ws.nblk + blk] = s;
     }
   }
@@ -635,6 +648,7 @@ void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, con
 
 void launch_cull_count(int e0, int ngroups, int nblk, int bpc, const EnvGroup* groups, const EnvConst* envs,
                        const DevScene* scenes, const RenderParams& rp, const ChunkWS& ws, cudaStream_t s) {
+  bpc = std::min(bpc, CULL_BPC_MAX);
   if (bpc > 1)
     cull_count_kernel<true><<<dim3(ngroups, (nblk + bpc - 1) / bpc), PROJ_BLOCK, 0, s>>>(e0, groups, envs, scenes, rp,
                                                                                        ws, bpc);
