@@ -50,24 +50,26 @@ constexpr float LOG2_099 = -0.014499569695115089f;      // log2(0.99): the alpha
 //   x = c0 + lx (c1 + A' lx) + ly (c2 + B' lx + C' ly),
 //   c0 = x(D), c1 = -(2A'Dx + B'Dy), c2 = -(B'Dx + 2C'Dy).
 // Both raster kernels evaluate exactly this sequence (bit-identical images).
-// Returns (c0, c1, c2, w) with w = min(log2 o, log2 0.99): alpha = 2^min(x, w)
-// is min(0.99, o e^(-q/2)) with q >= 0 enforced (R10, R13).
+// Returns (c0, -c1, -c2, w) with w = min(log2 o, log2 0.99): alpha = 2^min(x, w)
+// is min(0.99, o e^(-q/2)) with q >= 0 enforced (R10, R13).  c1, c2 are kept
+// negated: the walks add them with a negated FFMA operand (free, and exact),
+// which saves the loader two negations.
 __device__ __forceinline__ float4 tile_coefs(const float4 a0, const float4 a1, float tox, float toy) {
   const float Dx = a0.x - tox, Dy = a0.y - toy;
   const float c0 = fmaf(Dx, fmaf(a1.x, Dx, a1.y * Dy), fmaf(a1.z * Dy, Dy, a0.z));
-  const float c1 = -fmaf(2.f * a1.x, Dx, a1.y * Dy);
-  const float c2 = -fmaf(2.f * a1.z, Dy, a1.y * Dx);
-  return make_float4(c0, c1, c2, fminf(a0.z, LOG2_099));
+  const float c1n = fmaf(2.f * a1.x, Dx, a1.y * Dy);   // -c1
+  const float c2n = fmaf(2.f * a1.z, Dy, a1.y * Dx);   // -c2
+  return make_float4(c0, c1n, c2n, fminf(a0.z, LOG2_099));
 }
 
 // One pixel-Gaussian step (R12-R15 with the R30 log2-domain cutoff).  s0 =
-// (c0, c1, c2, w), s1 = (A', B', C', z), s2 = (r, g, b, -).  Alpha is not
+// (c0, -c1, -c2, w), s1 = (A', B', C', z), s2 = (r, g, b, -).  Alpha is not
 // accumulated: A = 1 - T at the end (R15).
 __device__ __forceinline__ void blend_step(const float4 s0, const float4 s1, const float4 s2, float lx, float ly,
                                            float& T, float& Cr, float& Cg, float& Cb, float& Dn,
                                            bool& done, uint32_t& nc) {
-  const float P = fmaf(lx, fmaf(s1.x, lx, s0.y), s0.x);
-  const float Q = fmaf(s1.y, lx, s0.z);
+  const float P = fmaf(lx, fmaf(s1.x, lx, -s0.y), s0.x);
+  const float Q = fmaf(s1.y, lx, -s0.z);
   const float x = fminf(fmaf(ly, fmaf(s1.z, ly, Q), P), s0.w);
   if (x >= LOG2_CUTOFF) {
     const float al = ex2_approx(x);
@@ -266,15 +268,14 @@ __device__ __forceinline__ void warp_walk(const ChunkWS& ws, const RenderParams&
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
     if (__all_sync(0xffffffffu, cut0 == INF && cut1 == INF)) break;
     const bool valid = b + lane < rg.y;
-    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
-    if (valid) { a0 = __ldg(&R0[nidx]); a1 = __ldg(&R1[nidx]); a2 = __ldg(&R2[nidx]); }
+    // unconditional: an idle lane reads record 0 of the env (it exists: the list is not empty)
+    const float4 a0 = __ldg(&R0[nidx]), a1 = __ldg(&R1[nidx]), a2 = __ldg(&R2[nidx]);
     nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
     const float lx0 = g.bx0, lx1 = g.bx0 + BW, ly0 = g.by0, ly1 = g.by0 + BH;
-    bool mine = false;
-    if (valid && a1.w >= 0.f && a0.z >= LOG2_CUTOFF) {
-      const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
-      mine = xh >= lx0 && xl <= lx1 && yh >= ly0 && yl <= ly1;
-    }
+    // branch-free (bitwise &): one predicate chain instead of a branch around the box test
+    const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
+    const bool mine = valid & (a1.w >= 0.f) & (a0.z >= LOG2_CUTOFF) & (xh >= lx0) & (xl <= lx1) & (yh >= ly0) &
+                      (yl <= ly1);
     const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (mine) {
       const int pos = __popc(m & lt);
@@ -297,8 +298,8 @@ __device__ __forceinline__ void warp_walk(const ChunkWS& ws, const RenderParams&
       const float4 r0 = srec[3 * i], r1 = srec[3 * i + 1];
 #endif
       // x = c0 + lx (c1 + A' lx) + ly (c2 + B' lx + C' ly)  (tile_coefs)
-      const float P = fmaf(g.lx, fmaf(r1.x, g.lx, r0.y), r0.x);
-      const float Q = fmaf(r1.y, g.lx, r0.z);
+      const float P = fmaf(g.lx, fmaf(r1.x, g.lx, -r0.y), r0.x);
+      const float Q = fmaf(r1.y, g.lx, -r0.z);
       float x0, x1;
       upk(fma2(g.LY, fma2(pk(r1.z, r1.z), g.LY, pk(Q, Q)), pk(P, P)), x0, x1);
       // no pixel of the warp passes: nothing to blend, nothing stops (exact)
@@ -503,8 +504,8 @@ raster_pc_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, Chu
       const uint32_t ph = (bi / PC_NS) & 1u;
       const uint32_t b = rg.x + 32u * bi;
       const bool valid = b + lane < rg.y;
-      float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
-      if (valid) { a0 = __ldg(&R0[nidx]); a1 = __ldg(&R1[nidx]); a2 = __ldg(&R2[nidx]); }
+      // an idle lane reads record 0 (the list is not empty)
+      const float4 a0 = __ldg(&R0[nidx]), a1 = __ldg(&R1[nidx]), a2 = __ldg(&R2[nidx]);
       nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
       const bool live = valid && a1.w >= 0.f && a0.z >= LOG2_CUTOFF;
       const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
@@ -548,8 +549,8 @@ raster_pc_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, Chu
       for (uint32_t i = 0; i < cnt; ++i) {
         const uint32_t j = S.idx[warp][i];
         const float4 r0 = S.rec[3 * j], r1 = S.rec[3 * j + 1];
-        const float P = fmaf(g.lx, fmaf(r1.x, g.lx, r0.y), r0.x);
-        const float Q = fmaf(r1.y, g.lx, r0.z);
+        const float P = fmaf(g.lx, fmaf(r1.x, g.lx, -r0.y), r0.x);
+        const float Q = fmaf(r1.y, g.lx, -r0.z);
         float x0, x1;
         upk(fma2(g.LY, fma2(pk(r1.z, r1.z), g.LY, pk(Q, Q)), pk(P, P)), x0, x1);
         if (!__any_sync(0xffffffffu, x0 >= cut0 || x1 >= cut1)) continue;
