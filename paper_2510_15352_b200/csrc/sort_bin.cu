@@ -415,7 +415,10 @@ __device__ __noinline__ void sort_run_by_gid(uint32_t* __restrict__ o, uint32_t 
 // step in two 128-bit loads; the rare tie (an equal successor) is resolved by
 // the thread owning the run's first position.  (A warp per block measured
 // slower: 0.95 vs 0.74 ms per 1,024 envs.)
-constexpr int TIES_THREADS = 256;
+#ifndef GG_TIES_THREADS
+#define GG_TIES_THREADS 256
+#endif
+constexpr int TIES_THREADS = GG_TIES_THREADS;
 __device__ __forceinline__ void ties_block(uint32_t b, const BlockTable& bt, const ChunkWS& ws, const uint32_t* keys) {
   const int e = block_env(bt, b);
   const uint32_t V = ws.vcnt[e];
