@@ -54,12 +54,13 @@ constexpr float LOG2_099 = -0.014499569695115089f;      // log2(0.99): the alpha
 // is min(0.99, o e^(-q/2)) with q >= 0 enforced (R10, R13).  c1, c2 are kept
 // negated: the walks add them with a negated FFMA operand (free, and exact),
 // which saves the loader two negations.
+template <bool NEG = true>   // false: (c0, c1, c2, w) (the blur walk: fewer spills there)
 __device__ __forceinline__ float4 tile_coefs(const float4 a0, const float4 a1, float tox, float toy) {
   const float Dx = a0.x - tox, Dy = a0.y - toy;
   const float c0 = fmaf(Dx, fmaf(a1.x, Dx, a1.y * Dy), fmaf(a1.z * Dy, Dy, a0.z));
   const float c1n = fmaf(2.f * a1.x, Dx, a1.y * Dy);   // -c1
   const float c2n = fmaf(2.f * a1.z, Dy, a1.y * Dx);   // -c2
-  return make_float4(c0, c1n, c2n, fminf(a0.z, LOG2_099));
+  return NEG ? make_float4(c0, c1n, c2n, fminf(a0.z, LOG2_099)) : make_float4(c0, -c1n, -c2n, fminf(a0.z, LOG2_099));
 }
 
 // One pixel-Gaussian step (R12-R15 with the R30 log2-domain cutoff).  s0 =
@@ -246,7 +247,13 @@ struct WarpGeom {
   bool in0, in1;
 };
 
-template <bool RGB>
+// LEAN (the single-camera raster): unconditional gathers, a branch-free box
+// test and negated tile coefficients (fewer loader instructions at 40
+// registers); the blur raster, which keeps two pixels' sample sums live
+// across its walks, uses the guarded form with plain coefficients (the lean
+// one makes ptxas spill there: 224 vs 16 bytes of spill loads).  Both give
+// the same bits (negation is exact).
+template <bool RGB, bool LEAN = true>
 __device__ __forceinline__ void warp_walk(const ChunkWS& ws, const RenderParams& rp, int eloc, int tile,
                                           const WarpGeom& g, bool col, float4* __restrict__ srec, f2& T, f2& Cr,
                                           f2& Cg, f2& Cb, f2& Dn) {
@@ -268,18 +275,29 @@ __device__ __forceinline__ void warp_walk(const ChunkWS& ws, const RenderParams&
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
     if (__all_sync(0xffffffffu, cut0 == INF && cut1 == INF)) break;
     const bool valid = b + lane < rg.y;
-    // unconditional: an idle lane reads record 0 of the env (it exists: the list is not empty)
-    const float4 a0 = __ldg(&R0[nidx]), a1 = __ldg(&R1[nidx]), a2 = __ldg(&R2[nidx]);
-    nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
     const float lx0 = g.bx0, lx1 = g.bx0 + BW, ly0 = g.by0, ly1 = g.by0 + BH;
-    // branch-free (bitwise &): one predicate chain instead of a branch around the box test
-    const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
-    const bool mine = valid & (a1.w >= 0.f) & (a0.z >= LOG2_CUTOFF) & (xh >= lx0) & (xl <= lx1) & (yh >= ly0) &
-                      (yl <= ly1);
+    float4 a0, a1, a2;
+    bool mine = false;
+    if (LEAN) {
+      // unconditional: an idle lane reads record 0 of the env (it exists: the list is not empty)
+      a0 = __ldg(&R0[nidx]); a1 = __ldg(&R1[nidx]); a2 = __ldg(&R2[nidx]);
+      // branch-free (bitwise &): one predicate chain instead of a branch around the box test
+      const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
+      mine = valid & (a1.w >= 0.f) & (a0.z >= LOG2_CUTOFF) & (xh >= lx0) & (xl <= lx1) & (yh >= ly0) & (yl <= ly1);
+    } else {
+      a0 = make_float4(0.f, 0.f, 0.f, 0.f); a1 = a0; a2 = a0;
+      if (valid) { a0 = __ldg(&R0[nidx]); a1 = __ldg(&R1[nidx]); a2 = __ldg(&R2[nidx]); }
+      nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
+      if (valid && a1.w >= 0.f && a0.z >= LOG2_CUTOFF) {
+        const float xl = a0.x - a1.w, xh = a0.x + a1.w, yl = a0.y - a2.w, yh = a0.y + a2.w;
+        mine = xh >= lx0 && xl <= lx1 && yh >= ly0 && yl <= ly1;
+      }
+    }
+    if (LEAN) nidx = b + 32 + lane < rg.y ? __ldg(&list[b + 32 + lane]) : 0u;
     const uint32_t m = __ballot_sync(0xffffffffu, mine);
     if (mine) {
       const int pos = __popc(m & lt);
-      srec[3 * pos] = tile_coefs(a0, a1, g.tox, g.toy);
+      srec[3 * pos] = tile_coefs<LEAN>(a0, a1, g.tox, g.toy);
       srec[3 * pos + 1] = make_float4(a1.x, a1.y, a1.z, a0.w);
       srec[3 * pos + 2] = a2;
     }
@@ -298,8 +316,8 @@ __device__ __forceinline__ void warp_walk(const ChunkWS& ws, const RenderParams&
       const float4 r0 = srec[3 * i], r1 = srec[3 * i + 1];
 #endif
       // x = c0 + lx (c1 + A' lx) + ly (c2 + B' lx + C' ly)  (tile_coefs)
-      const float P = fmaf(g.lx, fmaf(r1.x, g.lx, -r0.y), r0.x);
-      const float Q = fmaf(r1.y, g.lx, -r0.z);
+      const float P = fmaf(g.lx, fmaf(r1.x, g.lx, LEAN ? -r0.y : r0.y), r0.x);
+      const float Q = fmaf(r1.y, g.lx, LEAN ? -r0.z : r0.z);
       float x0, x1;
       upk(fma2(g.LY, fma2(pk(r1.z, r1.z), g.LY, pk(Q, Q)), pk(P, P)), x0, x1);
       // no pixel of the warp passes: nothing to blend, nothing stops (exact)
@@ -391,7 +409,7 @@ raster_blur_kernel(int e0, const EnvConst* __restrict__ envs, RenderParams rp, C
   float x0[2][4], sm[2][4], dep[2] = {0.f, 0.f};
   for (int k = 0; k < Kc; ++k) {
     f2 T, Cr, Cg, Cb, Dn;
-    warp_walk<RGB>(ws, rp, c0 + k, tile, g, k < K, srec[threadIdx.x >> 5], T, Cr, Cg, Cb, Dn);
+    warp_walk<RGB, false>(ws, rp, c0 + k, tile, g, k < K, srec[threadIdx.x >> 5], T, Cr, Cg, Cb, Dn);
     float t[2], cr[2], cg[2], cb[2], dn[2];
     upk(T, t[0], t[1]); upk(Cr, cr[0], cr[1]); upk(Cg, cg[0], cg[1]); upk(Cb, cb[0], cb[1]);
     upk(Dn, dn[0], dn[1]);

@@ -4,7 +4,7 @@ mkdir -p gpurun_out/var2
 python bench.py > gpurun_out/var2/default.json 2> gpurun_out/var2/default.err; echo default rc=$?
 B="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu"
 i=0
-for v in "--outputs rgb" "--outputs depth" "--sh 0" "--tiles paper" "--tiles ellipse" "--mode async" "--mode graph" "--config c4 --scenes 128" "--config c4" "--config c2" "--config c1" "--blur 3" "--config c5 --envs 4096"; do
+for v in "--outputs rgb" "--outputs depth" "--sh 0" "--tiles paper" "--tiles ellipse" "--mode async" "--mode graph" "--config c4 --scenes 128" "--config c4" "--config c2" "--config c1" "--blur 3" "--config c5 --envs 4096" "--config c1 --mode graph"; do
   i=$((i+1))
   $B $v > gpurun_out/var2/v$i.json 2>gpurun_out/var2/v$i.err; echo "$v rc=$?"
   python -c "
