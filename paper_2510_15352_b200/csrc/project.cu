@@ -180,9 +180,9 @@ __device__ __forceinline__ bool block_may_see(const EnvConst& c, float4 b0, floa
   return true;
 }
 
-// A CTA handles `bpc` consecutive storage blocks of its env group (bpc > 1
-// when groups are small, e.g. ~1.6 envs per scene in c5: the camera staging
-// and launch cost per CTA is then shared by several blocks).
+// A CTA handles `bpc` consecutive storage blocks of its env group (up to 16,
+// api.cu cull_blocks_per_cta): the camera staging is shared and all the
+// (env, block) frustum tests run in one step before the per-Gaussian tests.
 constexpr int CULL_BPC_MAX = PROJ_BLOCK / ENV_GROUP;   // storage blocks per cull CTA (one test thread per env and block)
 template <bool MULTI>   // false: one storage block per CTA (bpc = 1, full env groups)
 #ifndef GG_CULL_MINB
