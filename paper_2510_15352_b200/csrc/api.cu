@@ -160,6 +160,7 @@ struct gg_context {
   bool async_ready = false;
   int a_max_envs = 0, a_W = 0, a_H = 0, a_chunk = 0, a_nblk = 0, a_maxdeg = 0;
   uint64_t a_vcap = 0, a_kcap = 0, a_nbcap = 0;
+  bool a_loop = true;   // async sort/placement: bounded-grid work-counter kernels (else capacity-sized grids)
   DevBuf okflag;
 };
 
@@ -1117,7 +1118,7 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
 #endif
     ctx->launches += launch_sort_bin(ec, (uint32_t)ctx->a_nbcap, P<uint32_t>(ctx->aw.blkbase), P<uint32_t>(ctx->aw.blkenv),
                                      passes, rp, ws,
-                                     P<uint32_t>(ctx->aw.ghist), P<uint32_t>(ctx->aw.thist), s, true,
+                                     P<uint32_t>(ctx->aw.ghist), P<uint32_t>(ctx->aw.thist), s, ctx->a_loop,
                                      P<uint32_t>(ctx->aw.qctr), tev ? tev[3] : nullptr);
     TREC(4);
     launch_raster(e0, ec, P<EnvConst>(ctx->aw.envc), rp, ws, rgb, depth, alpha, counters,
@@ -1189,6 +1190,12 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
                         (unsigned long long)vcap, (unsigned long long)kcap);
   ctx->a_max_envs = max_envs; ctx->a_W = W; ctx->a_H = H; ctx->a_chunk = ch; ctx->a_nblk = nblk;
   ctx->a_maxdeg = maxdeg; ctx->a_vcap = vcap; ctx->a_kcap = kcap; ctx->a_nbcap = nbcap;
+  // a calibrated capacity is within h of the blocks that exist, so the sync
+  // kernels on a capacity-sized grid (surplus CTAs exit at once) beat the
+  // bounded-grid work-counter variants (graph mode c3: depth stage 28.5 ->
+  // 26.5 ms); a fraction-sized capacity may be far above them: keep the latter
+  static const int env_loop = getenv("GG_ASYNC_LOOP") ? atoi(getenv("GG_ASYNC_LOOP")) : -1;   // A/B switch
+  ctx->a_loop = env_loop >= 0 ? env_loop != 0 : !calibrated;
   ctx->async_ready = true;
   return GG_OK;
 }

@@ -30,6 +30,7 @@
 // identical inputs give bit-identical lists.
 #include "gg_internal.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace gg {
 
@@ -878,7 +879,8 @@ static int launch_sort_bin_t(int ec, uint32_t nb, BlockTable bt, int passes, con
 }
 
 // Enqueue K3-K5 for a chunk.  blk_base: device [ec+1] block prefix; nb total
-// blocks (a capacity if nb_is_capacity); ghist >= nb*DS_RADIX u32; thist >=
+// blocks; nb_is_capacity: nb is a capacity and the bounded-grid work-counter
+// variants run (else one CTA per block of nb, surplus CTAs exit); ghist >= nb*DS_RADIX u32; thist >=
 // nb*ntiles u32.  Returns the number of launches.
 int launch_sort_bin(int ec, uint32_t nb, const uint32_t* blk_base, uint32_t* blk_env, int passes,
                     const RenderParams& rp, const ChunkWS& ws, uint32_t* ghist, uint32_t* thist, cudaStream_t s,
