@@ -48,7 +48,8 @@ constexpr int PD_WARPS = PD_THREADS / 32;
 #define GG_PD_OWNER 1   // pair owners from a window bitmask (0: the shuffle binary search, 0.6 ms slower per c3 step)
 #endif
 #ifndef GG_SORT_BLK
-#define GG_SORT_BLK 6144   // measured: sort stage 56.4 (4096), 54.9 (5120), 53.4 (6144), 53.7 (7168), 59.9 (8192) ms per c3 step
+#define GG_SORT_BLK 6144   // measured: sort stage 56.4 (4096), 54.9 (5120), 53.4 (6144), 53.7 (7168), 59.9 (8192) ms per c3 step;
+                           // round 2 at HEAD (depth + placement): 54.67 (5120), 53.45 (6144), 55.26 (7168), 59.12 (8192)
 #endif
 constexpr int SORT_BLK = GG_SORT_BLK;                // records per sort block (depth and placement)
 constexpr int DS_THREADS = 512;                 // depth passes: 16 warps x 8 elements
