@@ -176,3 +176,27 @@ def test_async_capacity_overflow_is_reported(gg):
     assert ei.value.status == gg.GG_E_CAPACITY
     assert float(al.abs().max()) == 0.0          # the invalid chunk renders as background
     r.close()
+
+
+def test_calibrated_capacity_overflow_is_reported(gg):
+    """A calibrated reservation (capacity-sized grids of the sync kernels) that
+    the next poses outgrow: the chunk is flagged, renders as background, and
+    gg_check_errors reports GG_E_CAPACITY (no out-of-bounds work)."""
+    r = gg.Renderer(0)
+    sc = gi.config_scene("c1")
+    sid = r.load_scene(dev(sc.means), dev(sc.scales), dev(sc.quats), dev(sc.opacities), dev(sc.sh), sc.sh_degree)
+    E, W, H = 8, 64, 48
+    cams = gi.cameras(5, E, W, H, sc)
+    ids, K = dev(np.full(E, sid, np.int32)), dev(cams.intrinsics)
+    same = np.repeat(cams.viewmats[:1], E, axis=0)   # every env: env 0's view (V0 visible each)
+    away = same.copy()
+    away[1:, 2, 3] -= 1e4                     # envs 1.. see nothing (every Gaussian behind the camera)
+    _render(gg, r, ids, dev(away), K, W, H)   # calibrates: mean V0 / 8, max V0 -> capacity 1.5 * 4 V0
+    gg.gg_reserve_async(r.ctx, E, W, H, 0, -1.5, 0.0)
+    rgb, dep, al = _outs(E, H, W)
+    gg.gg_render(r.ctx, E, ids, dev(same), K, W, H, gg.default_opts(flags=gg.GG_ASYNC), rgb, dep, al)   # 8 V0
+    with pytest.raises(gg.GGError) as ei:
+        gg.gg_check_errors(r.ctx)
+    assert ei.value.status == gg.GG_E_CAPACITY
+    assert float(al.abs().max()) == 0.0
+    r.close()
