@@ -24,6 +24,8 @@ void launch_pack(int64_t n, int K, int sh_stride, const float* means, const floa
 int launch_spatial_order(int64_t n, const float* means, uint32_t* box, uint32_t* tmp, uint32_t* hist,
                          uint32_t* perm, cudaStream_t s);
 void launch_block_bounds(int n, const float4* pos_op, const float2* aux, float4* bbox, cudaStream_t s);
+bool launch_env_order(int E, const int32_t* scene_ids, const float* viewmats, int nscenes, const DevScene* scenes,
+                      int32_t* perm, cudaStream_t s);
 void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, const float* viewmats,
                        const float* intr, const DevScene* scenes, int nscenes, int W, int H, int sh_degree,
                        EnvConst* out, uint32_t* err, cudaStream_t s);
@@ -1070,8 +1072,14 @@ static gg_status render_async(gg_context* ctx, int32_t E, const int32_t* scene_i
     CK(cudaMemsetAsync(ctx->aw.counters.p, 0, (size_t)E * 32, s));
     ctx->last_counters = &ctx->aw.counters;
   }
-  launch_setup_envs(E, nullptr, scene_ids, viewmats, intr, P<DevScene>(ctx->scene_table), (int)ctx->scenes.size(), W,
-                    H, opts.sh_degree, P<EnvConst>(ctx->aw.envc), err, s);
+  // envs in (scene, view) order on the device (the sync path sorts on the host)
+  static const bool no_order = getenv("GG_NO_ENV_ORDER") != nullptr;   // A/B switch
+  const bool ordered = !no_order && launch_env_order(E, scene_ids, viewmats, (int)ctx->scenes.size(),
+                                                    P<DevScene>(ctx->scene_table), P<int32_t>(ctx->aw.perm), s);
+  ctx->launches += ordered ? 1 : 0;
+  launch_setup_envs(E, ordered ? P<int32_t>(ctx->aw.perm) : nullptr, scene_ids, viewmats, intr,
+                    P<DevScene>(ctx->scene_table), (int)ctx->scenes.size(), W, H, opts.sh_degree,
+                    P<EnvConst>(ctx->aw.envc), err, s);
   ctx->launches++;
   const int nchunks = (E + chunk - 1) / chunk;
   ctx->last_chunk = chunk;
@@ -1169,7 +1177,7 @@ gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t W, int32_t
     kcap = (uint64_t)((double)vcap * keys_per_visible) + 1;
   }
   const uint64_t nbcap = vcap / (uint64_t)sort_block_size() + ch + 1;
-  bool okb = ensure(ctx, ctx->aw.envc, sizeof(EnvConst) * max_envs, s) &&
+  bool okb = ensure(ctx, ctx->aw.envc, sizeof(EnvConst) * max_envs, s) && ensure(ctx, ctx->aw.perm, (size_t)max_envs * 4, s) &&
              ensure(ctx, ctx->aw.flags, (size_t)ch * nblk * PROJ_WPB * 4, s) && ensure(ctx, ctx->aw.blkcnt, (size_t)ch * nblk * 4, s) &&
              ensure(ctx, ctx->aw.vcnt, ch * 4, s) && ensure(ctx, ctx->aw.kcnt, ch * 8, s) && ensure(ctx, ctx->aw.rbase, ch * 8, s) &&
              ensure(ctx, ctx->aw.kbase, ch * 8, s) &&

@@ -16,6 +16,7 @@ constexpr int PROJ_WPB = PROJ_BLOCK / 32;  // visibility words per (env, block)
 constexpr int PROJ_LB = PROJ_BLOCK == 512 ? 9 : 8;   // bits of a block-local Gaussian index
 static_assert(PROJ_BLOCK == 256 || PROJ_BLOCK == 512, "projection block size");
 constexpr int MAX_TILES = 8192;        // tile table limit (e.g. 1024x2048 px)
+constexpr int ENV_ORDER_MAX = 16384;   // sync-free renders order their envs on the device up to this many
 
 // Scene store (SoA, 16-B aligned; DESIGN.md §4 "HBM layout").  O1 results
 // (Sigma3, DC colour) are precomputed at load (K0 scene_pack).

@@ -79,6 +79,97 @@ __global__ void setup_envs_kernel(int E, const int32_t* __restrict__ perm, const
   out[pos] = c;
 }
 
+// Processing order of a sync-free render's envs (GG_ASYNC; the sync path
+// sorts on the host, api.cu): by scene, then view cell (the forward axis's
+// cube face and quadrant), then the Morton code of the camera centre in the
+// batch's bounding box -- so the 16 envs of a projection group tend to share
+// a scene and see the same storage blocks.  Only a work heuristic: every
+// env's outputs go to its caller index, so any order gives the same frames.
+// One CTA; (key << 32 | env) sorted by a shared-memory bitonic network
+// (unique keys: deterministic); E <= ENV_ORDER_MAX, N = E rounded up to a
+// power of two.
+__device__ __forceinline__ float3 cam_centre(const float* V) {
+  float c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float x = -(V[0 * 4 + k] * V[3] + V[1 * 4 + k] * V[7] + V[2 * 4 + k] * V[11]);
+    c[k] = isfinite(x) ? x : 0.f;
+  }
+  return make_float3(c[0], c[1], c[2]);
+}
+
+__global__ void __launch_bounds__(1024) env_order_kernel(int E, int N, const int32_t* __restrict__ scene_ids,
+                                                         const float* __restrict__ viewmats, int nscenes,
+                                                         const DevScene* __restrict__ scenes, int32_t* perm) {
+  extern __shared__ unsigned long long so[];   // [N]
+  __shared__ float red[6][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float lo[3] = {3.0e38f, 3.0e38f, 3.0e38f}, hi[3] = {-3.0e38f, -3.0e38f, -3.0e38f};
+  for (int e = tid; e < E; e += 1024) {
+    const float3 c = cam_centre(viewmats + (size_t)e * 16);
+    lo[0] = fminf(lo[0], c.x); lo[1] = fminf(lo[1], c.y); lo[2] = fminf(lo[2], c.z);
+    hi[0] = fmaxf(hi[0], c.x); hi[1] = fmaxf(hi[1], c.y); hi[2] = fmaxf(hi[2], c.z);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { red[k][warp] = lo[k]; red[3 + k][warp] = hi[k]; }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float l = red[k][lane], h = red[3 + k][lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      l = fminf(l, __shfl_xor_sync(0xffffffffu, l, o));
+      h = fmaxf(h, __shfl_xor_sync(0xffffffffu, h, o));
+    }
+    lo[k] = l; hi[k] = h;
+  }
+  for (int e = tid; e < N; e += 1024) {
+    if (e >= E) { so[e] = ~0ull; continue; }
+    const float* V = viewmats + (size_t)e * 16;
+    const float F[3] = {V[8], V[9], V[10]};   // forward axis (row 2 of R)
+    int ax = 0;
+    if (fabsf(F[1]) > fabsf(F[ax])) ax = 1;
+    if (fabsf(F[2]) > fabsf(F[ax])) ax = 2;
+    const float m = fabsf(F[ax]) > 0.f ? fabsf(F[ax]) : 1.f;
+    const float a = F[(ax + 1) % 3] / m, b = F[(ax + 2) % 3] / m;
+    const uint32_t face = (uint32_t)(2 * ax + (F[ax] < 0.f));
+    const uint32_t cell = (a >= 0.f ? 1u : 0u) | (b >= 0.f ? 2u : 0u);
+    const float3 c = cam_centre(V);
+    const float cc[3] = {c.x, c.y, c.z};
+    uint32_t pos = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float ext = hi[k] - lo[k];
+      const uint32_t qk = ext > 0.f ? (uint32_t)fminf(15.f, fmaxf(0.f, (cc[k] - lo[k]) / ext * 16.f)) : 0u;
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) pos |= ((qk >> bb) & 1u) << (3 * bb + k);
+    }
+    const int sid = scene_ids[e];
+    const uint32_t sk = (sid < 0 || sid >= nscenes || !scenes[sid].valid) ? 0xffffu : (uint32_t)min(sid, 0xfffe);
+    so[e] = ((unsigned long long)((sk << 16) | ((face * 4 + cell) << 12) | pos) << 32) | (uint32_t)e;
+  }
+  __syncthreads();
+  for (int k = 2; k <= N; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < N / 2; i += 1024) {
+        const int l = 2 * i - (i & (j - 1)), r = l + j;
+        const bool up = (l & k) == 0;
+        const unsigned long long x = so[l], y = so[r];
+        if ((x > y) == up) { so[l] = y; so[r] = x; }
+      }
+      __syncthreads();
+    }
+  for (int p = tid; p < E; p += 1024) perm[p] = (int32_t)(uint32_t)so[p];
+}
+
 // p = R mu + t in the canonical order: ((R_k0 mu_x + R_k1 mu_y) + R_k2 mu_z) + t_k
 __device__ __forceinline__ float3 to_cam(const EnvConst& c, float4 g) {
   float3 p;
@@ -637,13 +728,25 @@ project_kernel(int e0, const EnvGroup* __restrict__ groups, const EnvConst* __re
   if (tid < grp.cnt && sm.kacc[tid]) atomicAdd(&ws.kcnt[grp.elo + tid], (unsigned long long)sm.kacc[tid]);
 }
 
-cudaError_t project_init() { return cudaSuccess; }
+cudaError_t project_init() {
+  return cudaFuncSetAttribute(env_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ENV_ORDER_MAX * 8);
+}
 
 void launch_setup_envs(int E, const int32_t* perm, const int32_t* scene_ids, const float* viewmats,
                        const float* intr, const DevScene* scenes, int nscenes, int W, int H, int sh_degree,
                        EnvConst* out, uint32_t* err, cudaStream_t s) {
   setup_envs_kernel<<<(E + 127) / 128, 128, 0, s>>>(E, perm, scene_ids, viewmats, intr, scenes, nscenes, W, H,
                                                     sh_degree, out, err);
+}
+
+// returns false (no launch: identity order) above ENV_ORDER_MAX envs
+bool launch_env_order(int E, const int32_t* scene_ids, const float* viewmats, int nscenes, const DevScene* scenes,
+                      int32_t* perm, cudaStream_t s) {
+  if (E < 2 || E > ENV_ORDER_MAX) return false;
+  int N = 2;
+  while (N < E) N <<= 1;
+  env_order_kernel<<<1, 1024, (size_t)N * 8, s>>>(E, N, scene_ids, viewmats, nscenes, scenes, perm);
+  return true;
 }
 
 void launch_cull_count(int e0, int ngroups, int nblk, int bpc, const EnvGroup* groups, const EnvConst* envs,
