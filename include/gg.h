@@ -127,10 +127,14 @@ gg_status gg_reserve(gg_context* ctx, int32_t max_envs, int32_t width, int32_t h
  * instead: h times the densest observed chunk's records (keys) per env times
  * the chunk, and at least h times min(chunk, 4) times the largest single env
  * seen (records capped at chunk x the largest scene); keys_per_visible is
- * then ignored (GG_E_INVALID if no such render happened).  Envs are processed in caller order in
- * groups of 16 (sort envs by scene id for best projection efficiency).  On
- * overflow that chunk's frames are background and gg_check_errors returns
- * GG_E_CAPACITY.  Counters (GG_COUNTERS) are supported; intermediates are not. */
+ * then ignored (GG_E_INVALID if no such render happened).  Envs are processed in groups of 16
+ * in (scene, view direction, camera position) order computed on the device
+ * for up to 16384 envs (caller order beyond; outputs always go to the caller's
+ * env index).  With a calibrated reservation the sort and placement run one
+ * CTA per capacity block (surplus CTAs exit), otherwise bounded grids that take
+ * blocks from work counters.  On overflow that chunk's frames are background
+ * and gg_check_errors returns GG_E_CAPACITY.  Counters (GG_COUNTERS) are
+ * supported; intermediates are not. */
 gg_status gg_reserve_async(gg_context* ctx, int32_t max_envs, int32_t width, int32_t height, int32_t chunk_envs,
                            float max_visible_frac, float keys_per_visible);
 
