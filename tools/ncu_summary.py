@@ -113,7 +113,8 @@ with open(os.path.join(DST, "ncu_summary.md"), "w") as f:
     f.write("| kernel | launches/step | ms/step | share |\n|---|---|---|---|\n")
     for k, a in sorted(agg.items(), key=lambda x: -x[1]["seconds"]):
         f.write(f"| {k} | {a['launches']} | {a['seconds']*1e3:.2f} | {a['share']*100:.1f}% |\n")
-    f.write("\nFull captures (one launch = one 512-env chunk):\n\n| kernel | ms | DRAM read GB | DRAM write GB | "
+    f.write("\nFull captures (one launch = one 512-env chunk; from the `full` pass, which can predate the launch list — "
+            "see the round's commit log):\n\n| kernel | ms | DRAM read GB | DRAM write GB | "
             "issue % | FMA pipe % | ALU pipe % | XU (MUFU) inst % | L1 % | L2 % | warps active % | regs |\n"
             "|---|---|---|---|---|---|---|---|---|---|---|---|\n")
     for k, r in kern.items():
