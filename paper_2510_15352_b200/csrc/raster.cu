@@ -241,6 +241,17 @@ constexpr int RW_THREADS = 128;
 // One warp's walk of one camera's tile list for its 8 x 8 block (the lane's
 // pixels (lx, ly) and (lx, ly + 4)); `col` (runtime, warp-uniform) turns the
 // colour accumulation off for a depth-only sample of a motion-blur render.
+#ifdef GG_RW_STATS
+__device__ unsigned long long g_rw_stats[8];
+extern "C" int gg_debug_rw_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, g_rw_stats, sizeof(unsigned long long) * 8) != cudaSuccess) return 1;
+  if (reset) {
+    static const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_rw_stats, z, sizeof z);
+  }
+  return 0;
+}
+#endif
 struct WarpGeom {
   float lx, tox, toy, bx0, by0;
   f2 LY;
@@ -274,8 +285,8 @@ __device__ __forceinline__ void warp_walk(const ChunkWS& ws, const RenderParams&
   uint32_t nidx = rg.x + lane < rg.y ? __ldg(&list[rg.x + lane]) : 0u;
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
     if (__all_sync(0xffffffffu, cut0 == INF && cut1 == INF)) break;
-    const bool valid = b + lane < rg.y;
     const float lx0 = g.bx0, lx1 = g.bx0 + BW, ly0 = g.by0, ly1 = g.by0 + BH;
+    const bool valid = b + lane < rg.y;
     float4 a0, a1, a2;
     bool mine = false;
     if (LEAN) {
@@ -320,6 +331,19 @@ __device__ __forceinline__ void warp_walk(const ChunkWS& ws, const RenderParams&
       const float Q = fmaf(r1.y, g.lx, LEAN ? -r0.z : r0.z);
       float x0, x1;
       upk(fma2(g.LY, fma2(pk(r1.z, r1.z), g.LY, pk(Q, Q)), pk(P, P)), x0, x1);
+#ifdef GG_RW_STATS   // instrumentation build: kept records, vote failures, geometric failures, live pixels
+      if (LEAN) {
+        const bool geo = __any_sync(0xffffffffu, (g.in0 && x0 >= LOG2_CUTOFF) || (g.in1 && x1 >= LOG2_CUTOFF));
+        const bool any = __any_sync(0xffffffffu, x0 >= cut0 || x1 >= cut1);
+        const uint32_t live = __popc(__ballot_sync(0xffffffffu, cut0 != INF)) + __popc(__ballot_sync(0xffffffffu, cut1 != INF));
+        if ((threadIdx.x & 31) == 0) {
+          atomicAdd(&g_rw_stats[0], 1ull);
+          if (!any) atomicAdd(&g_rw_stats[1], 1ull);
+          if (!geo) atomicAdd(&g_rw_stats[2], 1ull);
+          atomicAdd(&g_rw_stats[3], (unsigned long long)live);
+        }
+      }
+#endif
       // no pixel of the warp passes: nothing to blend, nothing stops (exact)
       if (!__any_sync(0xffffffffu, x0 >= cut0 || x1 >= cut1)) continue;
       const float al0 = x0 >= cut0 ? ex2_approx(fminf(x0, r0.w)) : 0.f;
